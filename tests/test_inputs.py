@@ -1,0 +1,48 @@
+"""The seeded input generators: determinism and numpy/torch bit-equality (CPU)."""
+import numpy as np
+import pytest
+import torch
+
+from inputs import graphs, rng
+
+
+def test_hash_numpy_equals_torch():
+    idx = np.arange(0, 5000, 7, dtype=np.uint64)
+    for seed, stream in [(0, 0), (1, 100), (2**40 + 3, 401)]:
+        a = rng.counter_hash_np(seed, stream, idx)
+        b = rng.counter_hash_torch(seed, stream, torch.from_numpy(idx.astype(np.int64))).numpy().view(np.uint64)
+        np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("kw", [dict(kind="rmat", seed=1, scale=10),
+                                dict(kind="rmat", seed=3, scale=11, permute=True),
+                                dict(kind="er", seed=2, n=3000, m_raw=40000),
+                                dict(kind="rmat", seed=5, scale=10, permute=True, values=True, transpose=True)])
+def test_graph_numpy_equals_torch_cpu(kw):
+    kind = kw.pop("kind")
+    a = graphs.make_graph(kind, **kw)
+    b = graphs.make_graph(kind, backend="torch", device="cpu", **kw).to_numpy()
+    np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
+    np.testing.assert_array_equal(a.col, b.col)
+    if a.values is not None:
+        np.testing.assert_array_equal(a.values, b.values)
+
+
+def test_csr_canonical_and_config_shapes():
+    g = graphs.make_config("c1")
+    assert g.n_src == 1024 and 11000 < g.m < 13000          # ~16K raw edges, ~25% duplicates
+    for u in range(g.n_src):
+        row = g.col[g.row_ptr[u]:g.row_ptr[u + 1]].astype(np.int64)
+        assert np.all(np.diff(row) > 0)
+    # unpermuted RMAT: low IDs are hubs (BASELINE config 1 has no relabelling)
+    deg = np.diff(g.row_ptr)
+    assert deg[:256].sum() > 0.45 * g.m
+    # determinism
+    g2 = graphs.make_config("c1")
+    np.testing.assert_array_equal(g.col, g2.col)
+
+
+def test_values_exact_in_unit_interval():
+    v = graphs.make_x(100000, 5)
+    assert v.dtype == np.float32 and v.min() >= -1 and v.max() < 1
+    assert abs(float(v.mean())) < 0.01
