@@ -1,0 +1,153 @@
+/*
+ * pcpm.h -- C ABI of the B200-native Partition-Centric PageRank / SpMV hot path
+ * (Lakhotia, Kannan, Prasanna, "Accelerating PageRank using Partition-Centric
+ * Processing", arXiv:1709.07122).  "P:<n>" cites /root/reference/PAPER.md
+ * line n; readings R1..R19 are listed in DESIGN.md.
+ *
+ * The library (libpcpm.so, built from paper_1709_07122_b200/csrc/) runs every
+ * step on one sm_100a GPU: the one-time layout build (§3.1-3.3), the PNG
+ * scatter (Alg. 4), the branch-avoiding gather (Alg. 5) and the apply step
+ * (Eq. 1).  There is no CPU fallback: every entry point that needs the GPU
+ * returns PCPM_ECUDA when no device is usable.
+ *
+ * Conventions
+ *  - Pointers are plain host or device pointers; the library detects which
+ *    with cudaPointerGetAttributes.  Host inputs are copied to the device
+ *    inside the call; host outputs are copied back before the call returns.
+ *  - All device work is ordered on the handle's stream (pcpm_set_stream;
+ *    default: the legacy default stream).  With device outputs the calls are
+ *    asynchronous with respect to the host, except pcpm_build which
+ *    synchronises once to size E'.
+ *  - Return value 0 = success, negative = PCPM_E* code; pcpm_last_error()
+ *    gives a thread-local message for the last failure.
+ *  - Limits: n_src, n_dst < 2^31 (the MSB of a 4-byte ID is the run flag,
+ *    P:172-173); nnz < 2^32 (u32 bin positions); partition_bits in [1, 15]
+ *    (one destination partition's accumulator, 2^b x 4 B, lives in one CTA's
+ *    shared memory); k_src * k_dst <= 2^26 (the O(k^2) offset matrices of
+ *    P:148 / P:246).
+ */
+#ifndef PCPM_H
+#define PCPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCPM_OK 0
+#define PCPM_EINVAL -1   /* NULL pointer, partition_bits out of range, d not in (0,1), iters < 0 ... */
+#define PCPM_ETOOBIG -2  /* n >= 2^31, nnz >= 2^32, k_src*k_dst > 2^26 */
+#define PCPM_EBADCSR -3  /* row_ptr not monotone / row_ptr[0] != 0 / row_ptr[n] != nnz, col >= n_dst,
+                            or a row whose columns are not strictly increasing (R6) */
+#define PCPM_ENOMEM -4   /* device allocation failed */
+#define PCPM_ECUDA -5    /* any other CUDA error (text in pcpm_last_error) */
+#define PCPM_ESTATE -6   /* operation not valid for this handle (e.g. PageRank on a non-square matrix) */
+
+/* pcpm_build_ex flags */
+#define PCPM_NO_COMPRESS 0x1u  /* uncompressed bins: every ID flagged, one update per edge (E' = m);
+                                  the BVGAS-like traffic baseline of P:342-345, measured with our layout */
+#define PCPM_BUILD_PULL 0x2u   /* also build the in-adjacency (CSC) for pcpm_pull_pagerank */
+#define PCPM_KEEP_VALUES 0x4u  /* keep weight bins even if values == NULL (all ones) */
+
+/* A CSR matrix M with n_src rows and n_dst columns: row u lists the columns
+ * v with M[u][v] != 0, i.e. the out-neighbours of u (push form).
+ * For PageRank n_src == n_dst == |V| and M is the 0/1 adjacency A; for SpMV
+ * the library computes y = M^T x (Eq. 2 orientation; reading R17). */
+typedef struct {
+  int64_t n_src;            /* rows (source vertices) */
+  int64_t n_dst;            /* columns (destination vertices) */
+  int64_t nnz;              /* nonzeros / edges, after deduplication (R10) */
+  const int64_t* row_ptr;   /* n_src+1 entries, row_ptr[0] = 0, monotone, row_ptr[n_src] = nnz */
+  const uint32_t* col_idx;  /* nnz entries, < n_dst, strictly increasing within each row */
+  const float* values;      /* nnz entries or NULL (= all ones; PageRank ignores values) */
+} pcpm_csr;
+
+typedef struct pcpm_handle pcpm_handle;
+
+/* Facts about a built layout (sizes are element counts). */
+typedef struct {
+  int64_t n_src, n_dst, nnz;
+  int32_t partition_bits;   /* b, q = 2^b */
+  int64_t q, k_src, k_dst;  /* partitions: P_i = [i q, (i+1) q) */
+  int64_t e_prime;          /* |E'| = #distinct (u, floor(v/q)) pairs */
+  double r;                 /* compression ratio m / E' (Table 2) */
+  int64_t n_dangling;       /* vertices with out-degree 0 */
+  int32_t weighted;         /* weight bins present */
+  int32_t compressed;       /* 0 when built with PCPM_NO_COMPRESS */
+  int64_t device_bytes;     /* device memory held by the handle */
+  double build_ms;          /* device time of the build (event-timed) */
+  int64_t gather_items, scatter_items;  /* work-list sizes of the two kernels */
+  int32_t fixed_point_bits; /* F of the last pcpm_pagerank / pcpm_spmv call */
+} pcpm_info;
+
+/* Device pointers to the built layout, for bit-exact tests (read-only). */
+typedef struct {
+  const uint32_t* ids;           /* [nnz] destID bins concatenated in j order; v | flag<<31 */
+  const float* w;                /* [nnz] weights aligned with ids, or NULL */
+  const uint32_t* png_src;       /* [E'] PNG sources grouped (p, j), u ascending */
+  const uint32_t* png_off;       /* [k_src*(k_dst+1)] start of group (p,j) in png_src; row p ends with
+                                    png_off[p][k_dst] = end of partition p */
+  const uint32_t* upd_off;       /* [k_src*k_dst] write offset of source partition p into the
+                                    concatenated update bins, P:148 */
+  const uint32_t* bin_id_start;  /* [k_dst+1] first ID of bin j */
+  const uint32_t* bin_upd_start; /* [k_dst+1] first update of bin j */
+  const uint32_t* chunk_base;    /* [nnz/128 + 2] #flags in ids[0 .. 128 c) (decode anchors) */
+  const uint32_t* out_degree;    /* [n_src] |N_o(u)| */
+  float* upd;                    /* [E'] update bins of the last scatter (scratch) */
+  int64_t chunk_ids;             /* IDs per chunk_base entry (128) */
+} pcpm_layout_view;
+
+/* Build the PCPM layout on the GPU (§3.1-3.3): validation,
+ * partitioning into k = ceil(n/q) partitions of q = 2^partition_bits
+ * vertices, the k x k write offsets of P:148, the destID bins with MSB run
+ * flags, the per-partition transposed PNG and the
+ * decode anchors.  Integer work only; the result is bit-identical to the
+ * oracle's layout.  csr arrays are borrowed for the duration of the call and
+ * may be host or device memory.  Returns NULL on error (see pcpm_last_error;
+ * pcpm_last_status gives the code). */
+pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits);
+pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned flags, void* cuda_stream);
+
+/* PageRank, Eq. 1 with PR_0 = 1/n (R2), damping d in (0,1), and the
+ * dangling-mass rule R1: PR_{t+1}(v) = (1-d)/n + d*(sum_{u->v} PR_t(u)/|N_o(u)|
+ * + D_t/n).  Runs `iters` iterations of scatter (Alg. 4) -> gather (Alg. 5)
+ * -> apply, captured in a CUDA graph.  out: n floats (host or device) receive
+ * the unscaled PR_iters (R4).  iters = 0 returns 1/n.  PCPM_ESTATE if the
+ * handle is not square. */
+int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out);
+
+/* y = M^T x (§3.5): y[v] = sum over CSR entries (u -> v) of
+ * w(u,v) * x[u], with w = values given at build (1 if none).  x: n_src floats,
+ * y: n_dst floats, host or device. */
+int pcpm_spmv(pcpm_handle* h, const float* x, float* y);
+
+/* Same PageRank computed by the naive pull-direction kernel (Alg. 1, P:86-99;
+ * the in-house comparison of BASELINE.json).  Needs PCPM_BUILD_PULL. */
+int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out);
+
+void pcpm_destroy(pcpm_handle* h);
+
+/* Support: stream, errors, introspection. */
+int pcpm_set_stream(pcpm_handle* h, void* cuda_stream);
+int pcpm_last_error(char* buf, int cap);   /* copies the message, returns its length */
+int pcpm_last_status(void);                /* code of the last failure on this thread */
+int pcpm_get_info(const pcpm_handle* h, pcpm_info* out);
+int pcpm_export_layout(pcpm_handle* h, pcpm_layout_view* out);
+/* Per-iteration diagnostics of the last pcpm_pagerank: host[2*t] = D_t (dangling
+ * mass of PR_t), host[2*t+1] = sum_v |PR_{t+1}(v) - PR_t(v)|.  Returns the
+ * number of doubles written (synchronises the stream). */
+int pcpm_get_residuals(pcpm_handle* h, double* host, int cap);
+/* Run only the scatter (Alg. 4) of x (n_src floats, device) into the handle's
+ * update bins (exported as pcpm_layout_view.upd); for bit-exact tests. */
+int pcpm_scatter(pcpm_handle* h, const float* x);
+/* Select a kernel variant for A/B experiments.
+ * key "gather_threads", "scatter_split", ... ; returns PCPM_EINVAL for unknown keys. */
+int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value);
+/* Kernel launches issued by the last pcpm_pagerank / pcpm_spmv call (per call). */
+int64_t pcpm_last_launch_count(const pcpm_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCPM_H */

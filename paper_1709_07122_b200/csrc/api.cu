@@ -1,0 +1,461 @@
+// api.cu -- the C ABI of include/pcpm.h: handle lifecycle, the PageRank
+// iteration driver (a4: init -> iters x [scatter -> gather+apply], captured in
+// a CUDA graph), SpMV (a5), the pull comparison, and introspection.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "pcpm_internal.cuh"
+
+namespace pcpm {
+
+namespace {
+thread_local int g_status = 0;
+thread_local std::string g_msg;
+
+int ceil_log2(uint64_t x) {
+  int r = 0;
+  while ((uint64_t(1) << r) < x) ++r;
+  return r;
+}
+}  // namespace
+
+void set_error(int code, const std::string& msg) {
+  g_status = code;
+  g_msg = msg;
+}
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s failed: %s (%s:%d)", what, cudaGetErrorString(e), file, line);
+  int code = (e == cudaErrorMemoryAllocation) ? PCPM_ENOMEM : PCPM_ECUDA;
+  cudaGetLastError();
+  set_error(code, buf);
+  return code;
+}
+
+int dev_alloc(pcpm_handle* h, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(PCPM_ENOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    *p = nullptr;
+    return PCPM_ENOMEM;
+  }
+  h->allocs.push_back(*p);
+  h->device_bytes += (int64_t)bytes;
+  return PCPM_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr;
+  cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+namespace {
+
+void free_graph(pcpm_handle* h) {
+  if (h->graph.exec) cudaGraphExecDestroy(h->graph.exec);
+  h->graph = Graph{};
+}
+
+int ensure_red(pcpm_handle* h, int iters) {
+  const int need = 2 * (iters + 2);
+  if (h->red_cap >= need) return PCPM_OK;
+  if (h->red) {
+    cudaFree(h->red);
+    for (auto& p : h->allocs)
+      if (p == h->red) p = nullptr;
+    h->red = nullptr;
+  }
+  free_graph(h);
+  int cap = std::max(need, 64);
+  int rc = dev_alloc_t(h, &h->red, cap);
+  if (rc) return rc;
+  h->red_cap = cap;
+  return PCPM_OK;
+}
+
+int pr_fixed_bits(int64_t n) {
+  // F: typical SPR ~ 1/(n*deg) lands near 2^22 in the low word; PR <= 1 so the
+  // u64 never overflows; resolution 2^-(F+1) ~ 1e-8 (1-d)/n per term.
+  return std::min(60, std::max(30, 26 + ceil_log2((uint64_t)n)));
+}
+
+int spmv_fixed_bits(uint32_t max_in_degree) {
+  // |y| <= in-degree (|w|, |x| <= 1 for the BASELINE inputs); keep 2 bits of headroom.
+  return std::min(52, 61 - ceil_log2((uint64_t)max_in_degree + 1));
+}
+
+GatherArgs base_args(pcpm_handle* h, int fbits) {
+  GatherArgs a{};
+  a.ids = h->ids;
+  a.w = h->w;
+  a.upd = h->upd;
+  a.chunk_base = h->chunk_base;
+  a.items = h->gitems;
+  a.n_items = h->n_gitems;
+  a.bin_nslices = h->bin_nslices;
+  a.counters = h->counters;
+  a.bin_arrive = h->bin_arrive;
+  a.part = h->part;
+  a.hi = h->hi;
+  a.item_red = h->item_red;
+  a.b = h->b;
+  a.n_dst = h->n_dst;
+  a.fbits = fbits;
+  a.outdeg = h->outdeg;
+  return a;
+}
+
+int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
+  int rc;
+  const int fbits = pr_fixed_bits(h->n_src);
+  h->fixed_bits = fbits;
+  if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, s))) return rc;
+  if (iters == 0) {
+    PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
+    return PCPM_OK;
+  }
+  for (int t = 0; t < iters; ++t) {
+    if ((rc = launch_scatter(h, h->spr, s))) return rc;          // Alg. 4
+    GatherArgs a = base_args(h, fbits);
+    a.d = d;
+    a.n = (double)h->n_src;
+    a.red_in = h->red + 2 * t;
+    a.red_out = h->red + 2 * t;
+    a.pr_old = h->pr[t & 1];
+    a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
+    a.spr_new = h->spr;
+    if ((rc = launch_gather(h, a, false, true, s))) return rc;  // Alg. 5 + apply
+  }
+  return PCPM_OK;
+}
+
+int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
+  int rc;
+  float* sprb[2] = {h->spr, h->xbuf};
+  if ((rc = launch_pr_init(h, h->pr[0], sprb[0], h->red, h->red_cap, s))) return rc;
+  if (iters == 0) {
+    PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
+    return PCPM_OK;
+  }
+  for (int t = 0; t < iters; ++t) {
+    float* pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
+    if ((rc = launch_pull_iteration(h, sprb[t & 1], h->pr[t & 1], pr_new, sprb[(t + 1) & 1], h->red + 2 * t, d, s)))
+      return rc;
+  }
+  return PCPM_OK;
+}
+
+int run_captured(pcpm_handle* h, int kind, float d, int iters, float* dst) {
+  cudaStream_t s = h->stream;
+  auto enq = [&](cudaStream_t st) { return kind == 0 ? enqueue_pagerank(h, d, iters, dst, st)
+                                                      : enqueue_pull(h, d, iters, dst, st); };
+  h->launches = 0;
+  if (!h->opt_use_graph) return enq(s);
+  Graph& g = h->graph;
+  if (!(g.exec && g.iters == iters && g.d == d && g.out == dst && g.kind == kind)) {
+    free_graph(h);
+    cudaStream_t cs;
+    PCPM_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      cudaStreamDestroy(cs);
+      return cuda_fail(e, "cudaStreamBeginCapture", __FILE__, __LINE__);
+    }
+    int rc = enq(cs);
+    e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc) {
+      if (e == cudaSuccess) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture", __FILE__, __LINE__);
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+    g.iters = iters;
+    g.d = d;
+    g.out = dst;
+    g.kind = kind;
+    g.launches = h->launches;
+  }
+  h->launches = g.launches;
+  PCPM_CK(cudaGraphLaunch(g.exec, s));
+  return PCPM_OK;
+}
+
+int pagerank_common(pcpm_handle* h, float d, int iters, float* out, int kind) {
+  if (!h || !out) {
+    set_error(PCPM_EINVAL, "NULL handle or output");
+    return PCPM_EINVAL;
+  }
+  if (!(d > 0.f && d < 1.f) || iters < 0) {
+    set_error(PCPM_EINVAL, "d must be in (0,1) and iters >= 0");
+    return PCPM_EINVAL;
+  }
+  if (h->n_src != h->n_dst) {
+    set_error(PCPM_ESTATE, "PageRank needs a square matrix (n_src == n_dst)");
+    return PCPM_ESTATE;
+  }
+  if (kind == 1 && !h->has_pull) {
+    set_error(PCPM_ESTATE, "pcpm_pull_pagerank needs a handle built with PCPM_BUILD_PULL");
+    return PCPM_ESTATE;
+  }
+  int rc = ensure_red(h, iters);
+  if (rc) return rc;
+  const bool dev_out = is_device_ptr(out);
+  float* dst = dev_out ? out : h->ybuf;
+  rc = run_captured(h, kind, d, iters, dst);
+  if (rc) return rc;
+  h->last_iters = iters;
+  if (!dev_out) {
+    PCPM_CK(cudaMemcpyAsync(out, dst, sizeof(float) * h->n_src, cudaMemcpyDeviceToHost, h->stream));
+    PCPM_CK(cudaStreamSynchronize(h->stream));
+  }
+  return PCPM_OK;
+}
+
+}  // namespace
+}  // namespace pcpm
+
+using namespace pcpm;
+
+extern "C" {
+
+pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned flags, void* cuda_stream) {
+  set_error(PCPM_OK, "");
+  if (!csr || !csr->row_ptr || (csr->nnz > 0 && !csr->col_idx)) {
+    set_error(PCPM_EINVAL, "NULL csr / row_ptr / col_idx");
+    return nullptr;
+  }
+  if (partition_bits < 1 || partition_bits > kMaxBits) {
+    set_error(PCPM_EINVAL, "partition_bits must be in [1, 15]");
+    return nullptr;
+  }
+  if (csr->n_src < 1 || csr->n_dst < 1 || csr->nnz < 0) {
+    set_error(PCPM_EINVAL, "n_src, n_dst must be >= 1 and nnz >= 0");
+    return nullptr;
+  }
+  if (csr->n_src >= (int64_t(1) << 31) || csr->n_dst >= (int64_t(1) << 31)) {
+    set_error(PCPM_ETOOBIG, "n >= 2^31: the MSB of a 4-byte ID is the run flag (P:172-173)");
+    return nullptr;
+  }
+  if (csr->nnz >= (int64_t(1) << 32) - kTileIds) {
+    set_error(PCPM_ETOOBIG, "nnz >= 2^32: bin positions are 32-bit");
+    return nullptr;
+  }
+  const int64_t q = int64_t(1) << partition_bits;
+  const int64_t ks = (csr->n_src + q - 1) / q, kd = (csr->n_dst + q - 1) / q;
+  if (ks * kd > (int64_t(1) << 26)) {
+    set_error(PCPM_ETOOBIG, "k_src * k_dst > 2^26: the O(k^2) offset matrices (P:148) are too large");
+    return nullptr;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error(PCPM_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    return nullptr;
+  }
+  pcpm_handle* h = new pcpm_handle();
+  h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  h->b = partition_bits;
+  cudaGetDevice(&h->device);
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  int rc = prepare_gather(h);
+  if (rc == PCPM_OK) rc = prepare_scatter(h);
+  if (rc == PCPM_OK) rc = build_layout(h, csr, flags);
+  if (rc == PCPM_OK) {
+    cudaEventRecord(e1, h->stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    h->build_ms = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc != PCPM_OK) {
+    int st = g_status;
+    std::string msg = g_msg;
+    pcpm_destroy(h);
+    set_error(st ? st : rc, msg);
+    return nullptr;
+  }
+  return h;
+}
+
+pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits) {
+  return pcpm_build_ex(csr, partition_bits, 0u, nullptr);
+}
+
+int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out) { return pagerank_common(h, d, iters, out, 0); }
+
+int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out) {
+  return pagerank_common(h, d, iters, out, 1);
+}
+
+int pcpm_spmv(pcpm_handle* h, const float* x, float* y) {
+  if (!h || !x || !y) {
+    set_error(PCPM_EINVAL, "NULL handle, x or y");
+    return PCPM_EINVAL;
+  }
+  cudaStream_t s = h->stream;
+  const bool dev_x = is_device_ptr(x), dev_y = is_device_ptr(y);
+  const float* xd = x;
+  if (!dev_x) {
+    PCPM_CK(cudaMemcpyAsync(h->xbuf, x, sizeof(float) * h->n_src, cudaMemcpyHostToDevice, s));
+    xd = h->xbuf;
+  }
+  float* yd = dev_y ? y : h->ybuf;
+  h->launches = 0;
+  int rc = launch_scatter(h, xd, s);                                       // Alg. 4 on x
+  if (rc) return rc;
+  const int fbits = spmv_fixed_bits(h->max_in_degree);
+  h->fixed_bits = fbits;
+  GatherArgs a = base_args(h, fbits);
+  a.y = yd;
+  rc = launch_gather(h, a, h->weighted, false, s);                         // Alg. 5 with weights (§3.5)
+  if (rc) return rc;
+  if (!dev_y) {
+    PCPM_CK(cudaMemcpyAsync(y, yd, sizeof(float) * h->n_dst, cudaMemcpyDeviceToHost, s));
+    PCPM_CK(cudaStreamSynchronize(s));
+  }
+  return PCPM_OK;
+}
+
+int pcpm_scatter(pcpm_handle* h, const float* x) {
+  if (!h || !x) {
+    set_error(PCPM_EINVAL, "NULL handle or x");
+    return PCPM_EINVAL;
+  }
+  const float* xd = x;
+  if (!is_device_ptr(x)) {
+    PCPM_CK(cudaMemcpyAsync(h->xbuf, x, sizeof(float) * h->n_src, cudaMemcpyHostToDevice, h->stream));
+    xd = h->xbuf;
+  }
+  h->launches = 0;
+  return launch_scatter(h, xd, h->stream);
+}
+
+void pcpm_destroy(pcpm_handle* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  else cudaDeviceSynchronize();
+  free_graph(h);
+  for (void* p : h->allocs)
+    if (p) cudaFree(p);
+  delete h;
+}
+
+int pcpm_set_stream(pcpm_handle* h, void* cuda_stream) {
+  if (!h) {
+    set_error(PCPM_EINVAL, "NULL handle");
+    return PCPM_EINVAL;
+  }
+  h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return PCPM_OK;
+}
+
+int pcpm_last_error(char* buf, int cap) {
+  const int len = (int)g_msg.size();
+  if (buf && cap > 0) {
+    const int k = std::min(len, cap - 1);
+    memcpy(buf, g_msg.data(), k);
+    buf[k] = 0;
+  }
+  return len;
+}
+
+int pcpm_last_status(void) { return g_status; }
+
+int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
+  if (!h || !out) {
+    set_error(PCPM_EINVAL, "NULL handle or info");
+    return PCPM_EINVAL;
+  }
+  pcpm_info i{};
+  i.n_src = h->n_src;
+  i.n_dst = h->n_dst;
+  i.nnz = h->m;
+  i.partition_bits = h->b;
+  i.q = h->q;
+  i.k_src = h->k_src;
+  i.k_dst = h->k_dst;
+  i.e_prime = h->e_prime;
+  i.r = h->e_prime ? (double)h->m / (double)h->e_prime : 0.0;
+  i.n_dangling = h->n_dangling;
+  i.weighted = h->weighted;
+  i.compressed = h->compressed;
+  i.device_bytes = h->device_bytes;
+  i.build_ms = h->build_ms;
+  i.gather_items = h->n_gitems;
+  i.scatter_items = h->n_sitems;
+  i.fixed_point_bits = h->fixed_bits;
+  *out = i;
+  return PCPM_OK;
+}
+
+int pcpm_export_layout(pcpm_handle* h, pcpm_layout_view* out) {
+  if (!h || !out) {
+    set_error(PCPM_EINVAL, "NULL handle or view");
+    return PCPM_EINVAL;
+  }
+  pcpm_layout_view v{};
+  v.ids = h->ids;
+  v.w = h->w;
+  v.png_src = h->png_src;
+  v.png_off = h->png_off;
+  v.upd_off = h->upd_off;
+  v.bin_id_start = h->bin_id_start;
+  v.bin_upd_start = h->bin_upd_start;
+  v.chunk_base = h->chunk_base;
+  v.out_degree = h->outdeg;
+  v.upd = h->upd;
+  v.chunk_ids = kChunkIds;
+  *out = v;
+  return PCPM_OK;
+}
+
+int pcpm_get_residuals(pcpm_handle* h, double* host, int cap) {
+  if (!h || !host) {
+    set_error(PCPM_EINVAL, "NULL handle or buffer");
+    return PCPM_EINVAL;
+  }
+  if (!h->red) return 0;
+  const int n = std::min(cap, 2 * (h->last_iters + 1));
+  PCPM_CK(cudaMemcpyAsync(host, h->red, sizeof(double) * n, cudaMemcpyDeviceToHost, h->stream));
+  PCPM_CK(cudaStreamSynchronize(h->stream));
+  return n;
+}
+
+int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
+  if (!h || !key) {
+    set_error(PCPM_EINVAL, "NULL handle or key");
+    return PCPM_EINVAL;
+  }
+  if (!strcmp(key, "use_graph")) {
+    h->opt_use_graph = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  set_error(PCPM_EINVAL, std::string("unknown option ") + key);
+  return PCPM_EINVAL;
+}
+
+int64_t pcpm_last_launch_count(const pcpm_handle* h) { return h ? h->launches : 0; }
+
+}  // extern "C"

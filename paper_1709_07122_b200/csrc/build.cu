@@ -1,0 +1,555 @@
+// build.cu -- a0: the one-time, GPU-built PCPM layout (§3.1-3.3).
+//
+// From a CSR (row u lists its out-neighbours v ascending) build, all on
+// the device and integer-only (bit-identical to the oracle's layout):
+//   * destID bins: edges stably sorted by destination
+//     partition j = v >> b, so bin j lists IDs in (u, v) order; the MSB flags
+//     the first ID of each (u, j) run (Alg. 2's prev_bin test);
+//   * the PNG: flagged edges (one per (u, j) pair = Eff_1) stably
+//     sorted by (p = u >> b, j) -- the per-partition transposition -- so group
+//     (p, j) lists its sources u ascending; png_off are the group starts;
+//   * write offsets: upd_off[p][j] = bin_upd_start[j] + sum_{p'<p}
+//     |group (p', j)|; bin starts are exclusive scans over j;
+//   * chunk_base[c] = #flags in ids[0 .. 128 c): the anchors of the global
+//     decode identity used by the gather;
+//   * out-degrees, dangling count, work lists for the scatter and gather.
+// Sorting replaces the paper's two counting scans because a stable
+// radix sort is deterministic and bandwidth-bound on B200; the result is the
+// same layout.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "pcpm_internal.cuh"
+
+namespace pcpm {
+namespace {
+
+constexpr int kT = 256;
+
+inline int grid_for(int64_t n, int threads = kT) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 32) g = 148 * 32;
+  return static_cast<int>(g);
+}
+
+inline int bits_for(uint64_t maxval) {  // bits needed to represent values in [0, maxval]
+  int bits = 1;
+  while (bits < 64 && (maxval >> bits) != 0) ++bits;
+  return bits;
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_check_rows(int64_t n, const int64_t* __restrict__ row_ptr, int64_t m, uint32_t* err) {
+  GRID_STRIDE(u, n) {
+    int64_t a = row_ptr[u], c = row_ptr[u + 1];
+    if (a > c || a < 0 || c > m) atomicOr(err, 1u);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (row_ptr[0] != 0 || row_ptr[n] != m) atomicOr(err, 1u);
+  }
+}
+
+__global__ void k_mark_rows(int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* rowid) {
+  GRID_STRIDE(u, n) {
+    if (row_ptr[u] < row_ptr[u + 1]) rowid[row_ptr[u]] = static_cast<uint32_t>(u);
+  }
+}
+
+struct MaxOp {
+  __device__ __forceinline__ uint32_t operator()(uint32_t a, uint32_t b) const { return a > b ? a : b; }
+};
+
+__global__ void k_iota(int64_t n, uint32_t* out) {
+  GRID_STRIDE(i, n) out[i] = static_cast<uint32_t>(i);
+}
+
+// Per edge: bin j, run flag (Alg. 2 prev_bin / MSB demarcation P:172-173), validation.
+__global__ void k_classify(int64_t m, const uint32_t* __restrict__ col, const uint32_t* __restrict__ rowid,
+                           int b, int64_t n_dst, bool compress, uint32_t* keyj, uint32_t* enc,
+                           uint8_t* flags, uint32_t* err) {
+  GRID_STRIDE(e, m) {
+    uint32_t u = rowid[e];
+    uint32_t v = col[e];
+    bool first = (e == 0) || rowid[e - 1] != u;
+    uint32_t pv = first ? 0u : col[e - 1];
+    if (v >= n_dst) atomicOr(err, 2u);
+    if (!first && pv >= v) atomicOr(err, 4u);
+    uint32_t j = v >> b;
+    bool flag = compress ? (first || (pv >> b) != j) : true;
+    keyj[e] = j;
+    enc[e] = v | (flag ? 0x80000000u : 0u);
+    flags[e] = flag ? 1 : 0;
+  }
+}
+
+// starts[key] = first position x with sorted_keys[x] >= key, for key in [0, nkeys]
+__global__ void k_boundaries(int64_t m, const uint32_t* __restrict__ sorted_keys, int64_t nkeys, uint32_t* starts) {
+  GRID_STRIDE(x, m + 1) {
+    int64_t kx = x < m ? (int64_t)sorted_keys[x] : nkeys;
+    int64_t kp = x > 0 ? (int64_t)sorted_keys[x - 1] : -1;
+    for (int64_t k = kp + 1; k <= kx && k <= nkeys; ++k) starts[k] = static_cast<uint32_t>(x);
+  }
+}
+
+__global__ void k_gather_ids(int64_t m, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ enc,
+                             const float* __restrict__ values, uint32_t* ids, float* w) {
+  GRID_STRIDE(x, m) {
+    uint32_t e = perm[x];
+    ids[x] = enc[e];
+    if (w) w[x] = values ? values[e] : 1.0f;
+  }
+}
+
+__global__ void k_png_keys(int64_t ep, const uint32_t* __restrict__ sel, const uint32_t* __restrict__ rowid,
+                           const uint32_t* __restrict__ col, int b, int64_t k_dst, uint32_t* key, uint32_t* val) {
+  GRID_STRIDE(i, ep) {
+    uint32_t e = sel[i];
+    uint32_t u = rowid[e];
+    key[i] = static_cast<uint32_t>((int64_t)(u >> b) * k_dst + (col[e] >> b));
+    val[i] = u;
+  }
+}
+
+// png_off[p][j] = G[p*k_dst + j] for j <= k_dst
+__global__ void k_png_off(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, uint32_t* png_off) {
+  GRID_STRIDE(i, k_src * (k_dst + 1)) {
+    int64_t p = i / (k_dst + 1), j = i % (k_dst + 1);
+    png_off[i] = G[p * k_dst + j];
+  }
+}
+
+// Column scans of the group sizes: upd_off[p][j] = sum_{p'<p} |(p', j)|, col_tot[j].
+__global__ void k_col_scan(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, uint32_t* upd_off,
+                           uint32_t* col_tot) {
+  GRID_STRIDE(j, k_dst) {
+    uint32_t run = 0;
+    for (int64_t p = 0; p < k_src; ++p) {
+      int64_t g = p * k_dst + j;
+      upd_off[g] = run;
+      run += G[g + 1] - G[g];
+    }
+    col_tot[j] = run;
+  }
+}
+
+__global__ void k_add_bin_start(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ bin_upd_start,
+                                uint32_t* upd_off) {
+  GRID_STRIDE(i, k_src * k_dst) upd_off[i] += bin_upd_start[i % k_dst];
+}
+
+// flags per kChunkIds-ID chunk: one warp per chunk, 4 IDs per lane
+__global__ void k_chunk_counts(int64_t nchunks, const uint32_t* __restrict__ ids, uint32_t* cnt) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = warp; c < nchunks; c += nw) {
+    uint4 v = reinterpret_cast<const uint4*>(ids + c * kChunkIds)[lane];
+    uint32_t f = (v.x >> 31) + (v.y >> 31) + (v.z >> 31) + (v.w >> 31);
+    for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    if (lane == 0) cnt[c] = f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[nchunks] = 0;
+}
+
+__global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* outdeg,
+                         unsigned long long* n_dangling) {
+  __shared__ unsigned int s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  unsigned int local = 0;
+  GRID_STRIDE(u, n) {
+    uint32_t dg = static_cast<uint32_t>(row_ptr[u + 1] - row_ptr[u]);
+    outdeg[u] = dg;
+    local += dg == 0;
+  }
+  atomicAdd(&s, local);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicAdd(n_dangling, (unsigned long long)s);
+}
+
+__global__ void k_indeg_hist(int64_t m, const uint32_t* __restrict__ col, uint32_t* indeg) {
+  GRID_STRIDE(e, m) atomicAdd(&indeg[col[e]], 1u);
+}
+
+__global__ void k_max(int64_t n, const uint32_t* __restrict__ a, uint32_t* out) {
+  uint32_t mx = 0;
+  GRID_STRIDE(i, n) mx = max(mx, a[i]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+__global__ void k_item_f(int n_items, GatherItem* items, const uint32_t* __restrict__ chunk_base,
+                         const uint32_t* __restrict__ bin_upd_start) {
+  GRID_STRIDE(i, n_items) {
+    GatherItem it = items[i];
+    it.fx0 = (it.x0 % kChunkIds == 0) ? chunk_base[it.x0 / kChunkIds] : bin_upd_start[it.j];
+    it.fx1 = (it.x1 % kChunkIds == 0) ? chunk_base[it.x1 / kChunkIds] : bin_upd_start[it.j + 1];
+    items[i] = it;
+  }
+}
+
+// CSC for the pull comparison: in_src[x] = rowid[perm[x]]
+__global__ void k_gather_u32(int64_t m, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ src,
+                             uint32_t* out) {
+  GRID_STRIDE(x, m) out[x] = src[perm[x]];
+}
+
+struct Temp {
+  std::vector<void*> ptrs;
+  ~Temp() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) ptrs.push_back(q);
+    *p = reinterpret_cast<T*>(q);
+    return e;
+  }
+};
+
+#define TK(call)                                                                 \
+  do {                                                                           \
+    cudaError_t _e = (call);                                                     \
+    if (_e == cudaErrorMemoryAllocation) {                                       \
+      cudaGetLastError();                                                        \
+      set_error(PCPM_ENOMEM, std::string("device allocation failed: ") + #call); \
+      return PCPM_ENOMEM;                                                        \
+    }                                                                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call, __FILE__, __LINE__);     \
+  } while (0)
+
+template <typename KeyT, typename ValT>
+cudaError_t radix_sort_pairs(Temp& tmp, const KeyT* kin, KeyT* kout, const ValT* vin, ValT* vout, int64_t n,
+                             int end_bit, cudaStream_t s) {
+  size_t bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, n, 0, end_bit, s);
+  if (e != cudaSuccess) return e;
+  void* t = nullptr;
+  e = tmp.alloc(reinterpret_cast<uint8_t**>(&t), bytes);
+  if (e != cudaSuccess) return e;
+  return cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, n, 0, end_bit, s);
+}
+
+}  // namespace
+
+int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+  cudaStream_t s = h->stream;
+  const int64_t n_src = csr->n_src, n_dst = csr->n_dst, m = csr->nnz;
+  const int b = h->b;
+  const int64_t q = int64_t(1) << b;
+  const int64_t k_src = (n_src + q - 1) / q, k_dst = (n_dst + q - 1) / q;
+  h->k_src = k_src;
+  h->k_dst = k_dst;
+  h->q = q;
+  h->n_src = n_src;
+  h->n_dst = n_dst;
+  h->m = m;
+  h->compressed = !(flags & PCPM_NO_COMPRESS);
+  h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
+  h->m_pad = ((m + kTileIds - 1) / kTileIds) * kTileIds;
+  if (h->m_pad == 0) h->m_pad = kTileIds;
+
+  Temp tmp;
+  // ---- inputs on the device
+  const int64_t* row_ptr = csr->row_ptr;
+  const uint32_t* col = csr->col_idx;
+  const float* values = csr->values;
+  if (!is_device_ptr(row_ptr)) {
+    int64_t* d;
+    TK(tmp.alloc(&d, n_src + 1));
+    TK(cudaMemcpyAsync(d, row_ptr, sizeof(int64_t) * (n_src + 1), cudaMemcpyHostToDevice, s));
+    row_ptr = d;
+  }
+  if (m > 0 && !is_device_ptr(col)) {
+    uint32_t* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, col, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, s));
+    col = d;
+  }
+  if (m > 0 && values && !is_device_ptr(values)) {
+    float* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, values, sizeof(float) * m, cudaMemcpyHostToDevice, s));
+    values = d;
+  }
+
+  uint32_t* err;
+  TK(tmp.alloc(&err, 4));
+  TK(cudaMemsetAsync(err, 0, 16, s));
+  k_check_rows<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, m, err);
+  TK(cudaGetLastError());
+  uint32_t herr[4] = {0, 0, 0, 0};
+  TK(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  if (herr[0]) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+
+  // ---- layout arrays owned by the handle
+  int rc;
+  if ((rc = dev_alloc_t(h, &h->ids, h->m_pad))) return rc;
+  if (h->weighted && (rc = dev_alloc_t(h, &h->w, h->m_pad))) return rc;
+  if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1)))) return rc;
+  if ((rc = dev_alloc_t(h, &h->upd_off, k_src * k_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_id_start, k_dst + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_upd_start, k_dst + 1))) return rc;
+  const int64_t nchunks = h->m_pad / kChunkIds;
+  if ((rc = dev_alloc_t(h, &h->chunk_base, nchunks + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->outdeg, n_src))) return rc;
+  TK(cudaMemsetAsync(h->ids, 0, sizeof(uint32_t) * h->m_pad, s));
+  if (h->w) TK(cudaMemsetAsync(h->w, 0, sizeof(float) * h->m_pad, s));
+
+  // ---- out-degrees and dangling count
+  unsigned long long* d_dang;
+  TK(tmp.alloc(&d_dang, 1));
+  TK(cudaMemsetAsync(d_dang, 0, 8, s));
+  k_outdeg<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, h->outdeg, d_dang);
+  TK(cudaGetLastError());
+
+  uint32_t* G = nullptr;  // flat (p, j) group starts, k_src*k_dst + 1 entries
+  TK(tmp.alloc(&G, k_src * k_dst + 1));
+  int64_t ep = 0;
+  if (m > 0) {
+    // ---- row id of every edge: mark row starts, inclusive max-scan
+    uint32_t *rowmark, *rowid;
+    TK(tmp.alloc(&rowmark, m));
+    TK(tmp.alloc(&rowid, m));
+    TK(cudaMemsetAsync(rowmark, 0, sizeof(uint32_t) * m, s));
+    k_mark_rows<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, rowmark);
+    TK(cudaGetLastError());
+    {
+      size_t bytes = 0;
+      TK(cub::DeviceScan::InclusiveScan(nullptr, bytes, rowmark, rowid, MaxOp(), m, s));
+      uint8_t* t;
+      TK(tmp.alloc(&t, bytes));
+      TK(cub::DeviceScan::InclusiveScan(t, bytes, rowmark, rowid, MaxOp(), m, s));
+    }
+    // ---- classify + validate
+    uint32_t *keyj, *enc;
+    uint8_t* fl;
+    TK(tmp.alloc(&keyj, m));
+    TK(tmp.alloc(&enc, m));
+    TK(tmp.alloc(&fl, m));
+    k_classify<<<grid_for(m), kT, 0, s>>>(m, col, rowid, b, n_dst, h->compressed, keyj, enc, fl, err);
+    TK(cudaGetLastError());
+    TK(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+    if (herr[0] & 2u) {
+      set_error(PCPM_EBADCSR, "col_idx has an entry >= n_dst");
+      return PCPM_EBADCSR;
+    }
+    if (herr[0] & 4u) {
+      set_error(PCPM_EBADCSR, "a row's columns are not strictly increasing (sorted, deduplicated) (R6)");
+      return PCPM_EBADCSR;
+    }
+    // ---- destID bins: stable sort of edge indices by j
+    uint32_t *iota, *keyj_s, *perm;
+    TK(tmp.alloc(&iota, m));
+    TK(tmp.alloc(&keyj_s, m));
+    TK(tmp.alloc(&perm, m));
+    k_iota<<<grid_for(m), kT, 0, s>>>(m, iota);
+    TK(cudaGetLastError());
+    TK(radix_sort_pairs(tmp, keyj, keyj_s, iota, perm, m, bits_for((uint64_t)std::max<int64_t>(k_dst - 1, 0)), s));
+    k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keyj_s, k_dst, h->bin_id_start);
+    TK(cudaGetLastError());
+    k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, h->ids, h->w);
+    TK(cudaGetLastError());
+
+    // ---- PNG: flagged edges, stable sort by (p, j)
+    uint32_t* sel;
+    int64_t* d_nsel;
+    TK(tmp.alloc(&sel, m));
+    TK(tmp.alloc(&d_nsel, 1));
+    {
+      size_t bytes = 0;
+      TK(cub::DeviceSelect::Flagged(nullptr, bytes, iota, fl, sel, d_nsel, m, s));
+      uint8_t* t;
+      TK(tmp.alloc(&t, bytes));
+      TK(cub::DeviceSelect::Flagged(t, bytes, iota, fl, sel, d_nsel, m, s));
+    }
+    TK(cudaMemcpyAsync(&ep, d_nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+    h->e_prime = ep;
+    if ((rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+    if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
+    TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+    uint32_t *pk, *pv, *pk_s;
+    TK(tmp.alloc(&pk, ep));
+    TK(tmp.alloc(&pv, ep));
+    TK(tmp.alloc(&pk_s, ep));
+    k_png_keys<<<grid_for(ep), kT, 0, s>>>(ep, sel, rowid, col, b, k_dst, pk, pv);
+    TK(cudaGetLastError());
+    TK(radix_sort_pairs(tmp, pk, pk_s, pv, h->png_src, ep, bits_for((uint64_t)(k_src * k_dst - 1)), s));
+    k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk_s, k_src * k_dst, G);
+    TK(cudaGetLastError());
+
+    // ---- pull comparison: CSC (in-adjacency), sources ascending per destination
+    if (flags & PCPM_BUILD_PULL) {
+      if ((rc = dev_alloc_t(h, &h->in_ptr, n_dst + 1))) return rc;
+      if ((rc = dev_alloc_t(h, &h->in_src, m))) return rc;
+      uint32_t *ck, *ck_s, *cperm;
+      TK(tmp.alloc(&ck, m));
+      TK(tmp.alloc(&ck_s, m));
+      TK(tmp.alloc(&cperm, m));
+      TK(cudaMemcpyAsync(ck, col, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
+      TK(radix_sort_pairs(tmp, ck, ck_s, iota, cperm, m, bits_for((uint64_t)std::max<int64_t>(n_dst - 1, 0)), s));
+      k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, ck_s, n_dst, h->in_ptr);
+      TK(cudaGetLastError());
+      k_gather_u32<<<grid_for(m), kT, 0, s>>>(m, cperm, rowid, h->in_src);
+      TK(cudaGetLastError());
+      h->has_pull = true;
+    }
+    // ---- max in-degree (fixed-point range of the signed SpMV accumulator)
+    {
+      uint32_t *indeg, *mx;
+      TK(tmp.alloc(&indeg, n_dst));
+      TK(tmp.alloc(&mx, 1));
+      TK(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * n_dst, s));
+      TK(cudaMemsetAsync(mx, 0, 4, s));
+      k_indeg_hist<<<grid_for(m), kT, 0, s>>>(m, col, indeg);
+      k_max<<<grid_for(n_dst), kT, 0, s>>>(n_dst, indeg, mx);
+      TK(cudaGetLastError());
+      TK(cudaMemcpyAsync(&h->max_in_degree, mx, 4, cudaMemcpyDeviceToHost, s));
+    }
+  } else {
+    h->e_prime = 0;
+    if ((rc = dev_alloc_t(h, &h->png_src, 8))) return rc;
+    if ((rc = dev_alloc_t(h, &h->upd, 8))) return rc;
+    TK(cudaMemsetAsync(h->upd, 0, 32, s));
+    TK(cudaMemsetAsync(G, 0, sizeof(uint32_t) * (k_src * k_dst + 1), s));
+    TK(cudaMemsetAsync(h->bin_id_start, 0, sizeof(uint32_t) * (k_dst + 1), s));
+    if (flags & PCPM_BUILD_PULL) {
+      if ((rc = dev_alloc_t(h, &h->in_ptr, n_dst + 1))) return rc;
+      if ((rc = dev_alloc_t(h, &h->in_src, 1))) return rc;
+      TK(cudaMemsetAsync(h->in_ptr, 0, sizeof(uint32_t) * (n_dst + 1), s));
+      h->has_pull = true;
+    }
+  }
+
+  // ---- offsets: png_off, column scans, bin update starts
+  k_png_off<<<grid_for(k_src * (k_dst + 1)), kT, 0, s>>>(k_src, k_dst, G, h->png_off);
+  uint32_t* col_tot;
+  TK(tmp.alloc(&col_tot, k_dst + 1));
+  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, G, h->upd_off, col_tot);
+  TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
+  {
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+  }
+  k_add_bin_start<<<grid_for(k_src * k_dst), kT, 0, s>>>(k_src, k_dst, h->bin_upd_start, h->upd_off);
+  TK(cudaGetLastError());
+
+  // ---- decode anchors: chunk_base[c] = #flags in ids[0 .. c*kChunkIds)
+  {
+    uint32_t* cnt;
+    TK(tmp.alloc(&cnt, nchunks + 1));
+    k_chunk_counts<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, h->ids, cnt);
+    TK(cudaGetLastError());
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, h->chunk_base, nchunks + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, h->chunk_base, nchunks + 1, s));
+  }
+
+  // ---- host-side work lists (small copies)
+  std::vector<uint32_t> hbin(k_dst + 1), hG(k_src * k_dst + 1);
+  unsigned long long hdang = 0;
+  TK(cudaMemcpyAsync(hbin.data(), h->bin_id_start, sizeof(uint32_t) * (k_dst + 1), cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(hG.data(), G, sizeof(uint32_t) * (k_src * k_dst + 1), cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(&hdang, d_dang, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  h->n_dangling = (int64_t)hdang;
+
+  // gather items: every destination partition gets >= 1 item (its apply runs even
+  // when the bin is empty); heavy bins are cut at tile-aligned points so no
+  // item exceeds ~m / (2 SMs) IDs; largest first (LPT, the GPU analogue of the
+  // paper's dynamic scheduling).
+  std::vector<GatherItem> gi;
+  std::vector<uint32_t> nsl(k_dst, 0);
+  int64_t slice = std::max<int64_t>(4 * kTileIds, ((m / (2 * h->num_sms)) / kTileIds + 1) * kTileIds);
+  for (int64_t j = 0; j < k_dst; ++j) {
+    int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
+    int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
+    int64_t per = (sz + nslc - 1) / nslc;
+    std::vector<int64_t> cuts{s0};
+    for (int64_t i = 1; i < nslc; ++i) {
+      int64_t c = ((s0 + i * per + kTileIds - 1) / kTileIds) * kTileIds;
+      if (c > cuts.back() && c < s1) cuts.push_back(c);
+    }
+    cuts.push_back(s1);
+    for (size_t i = 0; i + 1 < cuts.size(); ++i) {
+      GatherItem it{};
+      it.j = (uint32_t)j;
+      it.x0 = (uint32_t)cuts[i];
+      it.x1 = (uint32_t)cuts[i + 1];
+      gi.push_back(it);
+    }
+    nsl[j] = (uint32_t)(cuts.size() - 1);
+  }
+  std::stable_sort(gi.begin(), gi.end(),
+                   [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
+  h->n_gitems = (int)gi.size();
+  if ((rc = dev_alloc_t(h, &h->gitems, gi.size()))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
+  TK(cudaMemcpyAsync(h->gitems, gi.data(), sizeof(GatherItem) * gi.size(), cudaMemcpyHostToDevice, s));
+  TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
+  TK(cudaGetLastError());
+
+  // scatter items: (p, [j0, j1)) holding ~E' / (2 SMs) updates each
+  std::vector<ScatterItem> si;
+  int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
+  for (int64_t p = 0; p < k_src; ++p) {
+    int64_t acc = 0, j0 = 0;
+    for (int64_t j = 0; j < k_dst; ++j) {
+      acc += hG[p * k_dst + j + 1] - hG[p * k_dst + j];
+      if (acc >= target) {
+        si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)(j + 1), (uint32_t)acc});
+        acc = 0;
+        j0 = j + 1;
+      }
+    }
+    if (acc > 0) si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)k_dst, (uint32_t)acc});
+  }
+  std::stable_sort(si.begin(), si.end(), [](const ScatterItem& a, const ScatterItem& c) { return a.pad > c.pad; });
+  h->n_sitems = (int)si.size();
+  if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(si.size(), 1)))) return rc;
+  if (!si.empty())
+    TK(cudaMemcpyAsync(h->sitems, si.data(), sizeof(ScatterItem) * si.size(), cudaMemcpyHostToDevice, s));
+
+  // ---- iteration scratch (kept zero between uses by the kernels)
+  const int64_t nv = std::max(n_src, n_dst);
+  if ((rc = dev_alloc_t(h, &h->pr[0], nv + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->pr[1], nv + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->spr, n_src + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->xbuf, n_src + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->part, n_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
+  TK(cudaMemsetAsync(h->part, 0, sizeof(uint64_t) * n_dst, s));
+  TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
+  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
+  TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
+  TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
+  TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
+  TK(cudaStreamSynchronize(s));
+  return PCPM_OK;
+}
+
+}  // namespace pcpm

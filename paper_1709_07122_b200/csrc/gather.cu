@@ -1,0 +1,362 @@
+// gather.cu -- a2 + a3: the branch-avoiding gather of PAPER.md Alg. 5
+// with the apply step of Eq. 1 / Alg. 2 fused into its
+// epilogue, or the SpMV epilogue of §3.5.
+//
+// Alg. 5:  update_ptr += MSB(id);  id &= mask;  PR[id] += update_bins[p][update_ptr]
+//
+// GPU form:
+//  * Persistent CTAs (one per SM, 128 KB accumulator = one destination
+//    partition of q = 2^15 vertices in shared memory).  Work items are slices
+//    of destination bins, largest first, claimed with an atomic counter.
+//  * Warp 0 is the producer: for each 2048-ID tile it issues three bulk async
+//    copies (TMA engine, cp.async.bulk) into a 4-stage ring: the IDs, the
+//    window of update values those IDs reference, and 16 decode anchors.
+//  * 16 consumer warps each decode one 128-ID sub-chunk of the tile.  The
+//    update pointer of Alg. 5 becomes a warp prefix count of MSB flags:
+//    ptr = anchor + popc(ballot(flags) & lanemask_le) - 1  (reading R5's -1
+//    start), with no data-dependent branch.
+//  * Accumulation is 64-bit fixed point (F fractional bits): the low word
+//    lives in shared memory and is updated with native 32-bit integer
+//    ATOMS.ADD; the rare carries go to a global high word (and a smem bitmap
+//    marks them).  Integer sums are exact and order-independent, so results
+//    are bit-reproducible (fp32 atomics fail the
+//    1e-5 bound at the scale-26 hubs and are CAS loops on sm_100a).
+//  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
+//    PR'/outdeg; per-item dangling mass and L1 residual, reduced in fixed
+//    order by the last CTA.  Split bins flush their low words to a global
+//    u64 partial and the last-arriving slice runs the epilogue.
+#include "pcpm_internal.cuh"
+
+namespace pcpm {
+namespace {
+
+constexpr uint32_t kFlagLast = 1u, kFlagEmpty = 2u, kFlagStop = 4u;
+
+struct StageMeta {
+  int item;
+  uint32_t lo, hi;       // valid ID range of this tile [lo, hi)
+  uint32_t tile_base;    // first ID position of the tile
+  uint32_t win_base;     // update index of win[0]
+  uint32_t flags;
+  uint32_t pad[2];
+};
+
+template <bool W>
+struct Cfg {
+  static constexpr int kStages = W ? 3 : 4;
+  static constexpr int kIdsBytes = kTileIds * 4;
+  static constexpr int kWinBytes = kWinCap * 4;
+  static constexpr int kWBytes = W ? kTileIds * 4 : 0;
+  static constexpr int kCbBytes = kChunksPerTile * 4;
+  static constexpr int kStageBytes = kIdsBytes + kWinBytes + kWBytes + kCbBytes;
+};
+
+__device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint64_t ldcg_u64(const uint64_t* p) {
+  return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+template <bool W, bool PR>
+__global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a) {
+  using C = Cfg<W>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t q = int64_t(1) << a.b;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // q words (128 B rounded)
+  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;                           // q/32 words (>= 4)
+  const int bm_words = (int)((q + 31) / 32) < 4 ? 4 : (int)((q + 31) / 32);
+  uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + ((bm_words + 31) / 32) * 32);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
+  uint64_t* empty = full + S;
+  double* red_s = reinterpret_cast<double*>(empty + S);                    // 2*kConsumerWarps
+  uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * kConsumerWarps);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (;;) {
+        const uint32_t it = atomicAdd(&a.counters[0], 1u);
+        const bool stop = it >= (uint32_t)a.n_items;
+        GatherItem item;
+        if (!stop) item = a.items[it];
+        if (stop || item.x0 == item.x1) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          StageMeta m{};
+          m.item = stop ? -1 : (int)it;
+          m.flags = stop ? kFlagStop : (kFlagLast | kFlagEmpty);
+          meta[stage] = m;
+          mbar_arrive(&full[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+          if (stop) break;
+          continue;
+        }
+        const uint32_t t0 = item.x0 / kTileIds, t1 = (item.x1 - 1) / kTileIds;
+        for (uint32_t t = t0; t <= t1; ++t) {
+          const uint32_t tb = t * kTileIds;
+          const uint32_t lo = max(tb, item.x0), hi = min(tb + kTileIds, item.x1);
+          const uint32_t flo = (lo == item.x0) ? item.fx0 : __ldg(a.chunk_base + lo / kChunkIds);
+          const uint32_t fhi = (hi == item.x1) ? item.fx1 : __ldg(a.chunk_base + hi / kChunkIds);
+          const uint32_t wlo = flo > 0 ? flo - 1 : 0;
+          const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
+          mbar_wait(&empty[stage], phase ^ 1);
+          StageMeta m{};
+          m.item = (int)it;
+          m.lo = lo;
+          m.hi = hi;
+          m.tile_base = tb;
+          m.win_base = alo;
+          m.flags = (t == t1) ? kFlagLast : 0u;
+          meta[stage] = m;
+          uint8_t* sb = stage_base + stage * C::kStageBytes;
+          const uint32_t win_bytes = (ahi - alo) * 4;
+          mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
+          bulk_g2s(sb, a.ids + tb, C::kIdsBytes, &full[stage], pol);
+          bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
+          bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
+                   &full[stage], pol);
+          if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ================= consumers =================
+  const int cw = warp - 1;                  // 0..15: sub-chunk owned in every tile
+  const int ctid = threadIdx.x - 32;        // 0..511
+  constexpr int kCons = 32 * kConsumerWarps;
+  const uint32_t qmask = (uint32_t)(q - 1);
+  const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F
+  const double dscale = (double)fscale;
+  const double inv_scale = 1.0 / dscale;
+  for (int64_t i = ctid; i < q; i += kCons) acc[i] = 0u;
+  for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
+  double base_pr = 0.0;
+  if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+  named_bar_sync(1, kCons);
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    mbar_wait(&full[stage], phase);
+    const StageMeta m = meta[stage];
+    if (m.flags & kFlagStop) break;
+    const GatherItem item = a.items[m.item];
+    const uint32_t v0 = item.j << a.b;
+    if (!(m.flags & kFlagEmpty)) {
+      const uint8_t* sb = stage_base + stage * C::kStageBytes;
+      const uint32_t* ids_s = reinterpret_cast<const uint32_t*>(sb);
+      const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
+      const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
+      const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
+      const uint32_t xs = m.tile_base + cw * kChunkIds;
+      if (xs < m.hi && xs + kChunkIds > m.lo) {
+        uint32_t fb = cb_s[cw];               // #flags before xs (global decode identity)
+        const uint32_t lmask = lanemask_le();
+#pragma unroll
+        for (int st = 0; st < kChunkIds / 32; ++st) {
+          const uint32_t off = cw * kChunkIds + st * 32 + lane;
+          const uint32_t x = m.tile_base + off;
+          const uint32_t id = ids_s[off];
+          const uint32_t bal = __ballot_sync(0xffffffffu, id >> 31);
+          const uint32_t ptr = fb + __popc(bal & lmask) - 1;   // Alg. 5: update_ptr += MSB(id)
+          fb += __popc(bal);
+          if (x >= m.lo && x < m.hi) {
+            const uint32_t li = id & qmask;                      // id &= bitmask (partition-local)
+            const float val = win_s[ptr - m.win_base];
+            uint32_t tlo, thi;
+            if constexpr (PR) {
+              // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
+              const unsigned long long T = __float2ull_rn(val * fscale);
+              tlo = (uint32_t)T;
+              thi = (uint32_t)(T >> 32);
+            } else {
+              // SpMV: signed two's-complement fixed point; w * x is exact in fp64
+              const double tv = W ? (double)val * (double)w_s[off] : (double)val;
+              const long long T = __double2ll_rn(tv * dscale);
+              tlo = (uint32_t)T;
+              thi = (uint32_t)((unsigned long long)T >> 32);
+            }
+            const uint32_t old = atomicAdd(&acc[li], tlo);
+            const uint32_t hinc = thi + ((old + tlo < old) ? 1u : 0u);
+            if (hinc != 0u) {
+              atomicAdd(&a.hi[v0 + li], hinc);
+              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (++stage == S) { stage = 0; phase ^= 1; }
+
+    if (m.flags & kFlagLast) {
+      // ---------------- epilogue of this item ----------------
+      named_bar_sync(1, kCons);
+      const int64_t cnt = min(q, a.n_dst - (int64_t)v0);
+      const uint32_t nsl = a.bin_nslices[item.j];
+      bool run_apply = true;
+      if (nsl > 1) {
+        for (int64_t i = ctid; i < q; i += kCons) {
+          const uint32_t lo = acc[i];
+          if (lo) atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), (unsigned long long)lo);
+          acc[i] = 0u;
+        }
+        __threadfence();
+        named_bar_sync(1, kCons);
+        if (ctid == 0) {
+          const uint32_t old = atomicAdd(&a.bin_arrive[item.j], 1u);
+          const bool last = old == nsl - 1;
+          if (last) a.bin_arrive[item.j] = 0u;
+          *flag_s = last ? 1u : 0u;
+        }
+        named_bar_sync(1, kCons);
+        run_apply = *flag_s != 0u;
+        if (run_apply) __threadfence();
+      }
+      double dang = 0.0, res = 0.0;
+      if (run_apply) {
+        for (int64_t i = ctid; i < cnt; i += kCons) {
+          const uint32_t v = v0 + (uint32_t)i;
+          uint64_t tot;
+          if (nsl > 1) {
+            tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
+            a.part[v] = 0ull;
+            a.hi[v] = 0u;
+          } else {
+            tot = acc[i];
+            if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
+              tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+              a.hi[v] = 0u;
+            }
+            acc[i] = 0u;
+          }
+          const double sum = (double)(long long)tot * inv_scale;
+          if constexpr (PR) {
+            const double prn = base_pr + a.d * sum;
+            a.pr_new[v] = (float)prn;
+            const uint32_t dg = __ldg(a.outdeg + v);
+            a.spr_new[v] = dg ? (float)(prn / (double)dg) : 0.0f;
+            if (dg == 0) dang += prn;
+            res += fabs(prn - (double)a.pr_old[v]);
+          } else {
+            a.y[v] = (float)sum;
+          }
+        }
+      }
+      for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
+      if constexpr (PR) {
+        for (int o = 16; o; o >>= 1) {
+          dang += __shfl_xor_sync(0xffffffffu, dang, o);
+          res += __shfl_xor_sync(0xffffffffu, res, o);
+        }
+        if (lane == 0) {
+          red_s[cw] = dang;
+          red_s[kConsumerWarps + cw] = res;
+        }
+      }
+      named_bar_sync(1, kCons);
+      if constexpr (PR) {
+        if (ctid == 0) {
+          double sd = 0.0, sr = 0.0;
+          for (int k = 0; k < kConsumerWarps; ++k) {
+            sd += red_s[k];
+            sr += red_s[kConsumerWarps + k];
+          }
+          a.item_red[2 * m.item] = sd;       // zero for non-last slices
+          a.item_red[2 * m.item + 1] = sr;
+        }
+      }
+      for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
+      named_bar_sync(1, kCons);
+    }
+  }
+
+  // ---------------- last CTA: fixed-order reduction, counter reset ----------------
+  named_bar_sync(1, kCons);
+  if (ctid == 0) {
+    __threadfence();
+    const uint32_t done = atomicAdd(&a.counters[1], 1u);
+    *flag_s = (done == gridDim.x - 1) ? 1u : 0u;
+  }
+  named_bar_sync(1, kCons);
+  if (*flag_s) {
+    __threadfence();
+    if constexpr (PR) {
+      if (cw == 0) {
+        // pairwise-free fixed order: lane-strided partial sums, then a fixed shuffle tree
+        double sd = 0.0, sr = 0.0;
+        for (int i = lane; i < a.n_items; i += 32) {
+          sd += __ldcg(&a.item_red[2 * i]);
+          sr += __ldcg(&a.item_red[2 * i + 1]);
+        }
+        for (int o = 16; o; o >>= 1) {
+          sd += __shfl_xor_sync(0xffffffffu, sd, o);
+          sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        }
+        if (lane == 0) {
+          a.red_out[2] = sd;   // D_{t+1}
+          a.red_out[1] = sr;   // residual of iteration t
+        }
+      }
+    }
+    if (ctid == 0) {
+      a.counters[0] = 0u;
+      a.counters[1] = 0u;
+    }
+  }
+}
+
+}  // namespace
+
+int gather_smem_bytes(int b, bool weighted) {
+  const int64_t q = int64_t(1) << b;
+  const int bm_words = (int)((q + 31) / 32) < 4 ? 4 : (int)((q + 31) / 32);
+  const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
+  const int stages = weighted ? Cfg<true>::kStages : Cfg<false>::kStages;
+  const int sbytes = weighted ? Cfg<true>::kStageBytes : Cfg<false>::kStageBytes;
+  return (int)(head + stages * sbytes + stages * sizeof(StageMeta) + 2 * stages * 8 + 2 * kConsumerWarps * 8 + 16);
+}
+
+using GatherFn = void (*)(const GatherArgs);
+
+GatherFn gather_fn(bool weighted, bool pagerank) {
+  return weighted ? (pagerank ? k_gather<true, true> : k_gather<true, false>)
+                  : (pagerank ? k_gather<false, true> : k_gather<false, false>);
+}
+
+int prepare_gather(pcpm_handle* h) {
+  int maxsm = 0;
+  PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  for (int w = 0; w < 2; ++w)
+    for (int p = 0; p < 2; ++p)
+      PCPM_CK(cudaFuncSetAttribute(gather_fn(w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  return PCPM_OK;
+}
+
+int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s) {
+  const int smem = gather_smem_bytes(a.b, weighted);
+  const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
+  gather_fn(weighted, pagerank)<<<grid, kGatherThreads, smem, s>>>(a);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
+  return PCPM_OK;
+}
+
+}  // namespace pcpm

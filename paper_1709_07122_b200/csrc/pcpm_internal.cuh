@@ -1,0 +1,229 @@
+// pcpm_internal.cuh -- shared internals of libpcpm.so (product path only).
+// Handle layout, error plumbing, sm_100a PTX helpers (mbarrier, bulk async
+// copy), and the launch-side declarations of the kernels in build.cu,
+// scatter.cu, gather.cu and pull.cu.  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "pcpm.h"
+
+namespace pcpm {
+
+// ---------------------------------------------------------------- constants
+// Gather tile: kTileIds destination IDs (8 KB) per pipeline stage, decoded by
+// kConsumerWarps warps, each owning one kChunkIds-ID sub-chunk whose update
+// index base comes from chunk_base (the global decode identity).
+constexpr int kTileIds = 2048;
+constexpr int kChunkIds = 128;
+constexpr int kChunksPerTile = kTileIds / kChunkIds;   // 16
+constexpr int kConsumerWarps = kChunksPerTile;         // one sub-chunk per warp
+constexpr int kGatherThreads = 32 * (kConsumerWarps + 1);
+constexpr int kWinCap = kTileIds + 8;                  // update window (floats), 16 B aligned ends
+constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
+constexpr int kScatterThreads = 1024;
+
+struct GatherItem {        // one slice [x0, x1) of destination bin j
+  uint32_t j, x0, x1;
+  uint32_t fx0, fx1;       // #flags in ids[0..x0), ids[0..x1)  (global decode identity)
+  uint32_t pad[3];
+};
+static_assert(sizeof(GatherItem) == 32, "GatherItem is 32 B");
+
+struct ScatterItem {       // source partition p, destination groups [j0, j1)
+  uint32_t p, j0, j1, pad;
+};
+
+// ---------------------------------------------------------------- handle
+struct Graph {             // cached CUDA graph of one pcpm_pagerank configuration
+  cudaGraphExec_t exec = nullptr;
+  int iters = -1;
+  float d = 0.f;
+  float* out = nullptr;
+  int kind = 0;
+  int64_t launches = 0;
+};
+
+}  // namespace pcpm
+
+struct pcpm_handle {
+  int64_t n_src = 0, n_dst = 0, m = 0, m_pad = 0, e_prime = 0;
+  int b = 0;
+  int64_t q = 0, k_src = 0, k_dst = 0, n_dangling = 0;
+  bool weighted = false, compressed = true, has_pull = false;
+  cudaStream_t stream = nullptr;
+  int device = 0, num_sms = 148;
+  double build_ms = 0.0;
+  int fixed_bits = 0;
+  int64_t launches = 0;
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+
+  // layout (device)
+  uint32_t* ids = nullptr;          // [m_pad]
+  float* w = nullptr;               // [m_pad] or null
+  uint32_t* png_src = nullptr;      // [E' (+pad)]
+  uint32_t* png_off = nullptr;      // [k_src*(k_dst+1)]
+  uint32_t* upd_off = nullptr;      // [k_src*k_dst]
+  uint32_t* bin_id_start = nullptr; // [k_dst+1]
+  uint32_t* bin_upd_start = nullptr;// [k_dst+1]
+  uint32_t* chunk_base = nullptr;   // [m_pad/kChunkIds + 1]
+  uint32_t* outdeg = nullptr;       // [n_src]
+  float* upd = nullptr;             // [E' + 8]
+  uint32_t max_in_degree = 0;
+
+  // pull comparison (CSC)
+  uint32_t* in_ptr = nullptr;       // [n_dst+1]
+  uint32_t* in_src = nullptr;       // [m]
+
+  // work lists
+  pcpm::GatherItem* gitems = nullptr;
+  int n_gitems = 0;
+  uint32_t* bin_nslices = nullptr;  // [k_dst]
+  pcpm::ScatterItem* sitems = nullptr;
+  int n_sitems = 0;
+
+  // iteration state
+  float* pr[2] = {nullptr, nullptr};// [n]
+  float* spr = nullptr;             // [n_src (+pad)]
+  float* xbuf = nullptr;            // [n_src (+pad)] staging for host x
+  float* ybuf = nullptr;            // [n_dst]      staging for host y / out
+  uint64_t* part = nullptr;         // [n_dst] split-bin partial sums (kept zero between uses)
+  uint32_t* hi = nullptr;           // [n_dst] fixed-point carry words (kept zero)
+  uint32_t* bin_arrive = nullptr;   // [k_dst]
+  uint32_t* counters = nullptr;     // [4] work counter, done counter (kept zero)
+  double* item_red = nullptr;       // [2*n_gitems] per-item (dangling, residual) partials
+  double* red = nullptr;            // [2*(red_cap)] D_t, res_t
+  int red_cap = 0;
+  int last_iters = 0;
+
+  // options (pcpm_set_option)
+  int opt_use_graph = 1;
+  int opt_scatter_stage = 1;
+
+  pcpm::Graph graph;
+};
+
+namespace pcpm {
+
+// ---------------------------------------------------------------- errors
+void set_error(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define PCPM_CK(call)                                                          \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) return ::pcpm::cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+// allocate device memory owned by the handle
+int dev_alloc(pcpm_handle* h, void** p, size_t bytes);
+template <typename T>
+int dev_alloc_t(pcpm_handle* h, T** p, size_t count) {
+  return dev_alloc(h, reinterpret_cast<void**>(p), count * sizeof(T));
+}
+bool is_device_ptr(const void* p);
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA engine, UBLKCP), completion on mbarrier.
+// dst, src 16 B aligned; bytes a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint32_t lanemask_le() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(r));
+  return r;
+}
+
+// ---------------------------------------------------------------- launchers
+struct GatherArgs {
+  const uint32_t* ids;
+  const float* w;
+  const float* upd;
+  const uint32_t* chunk_base;
+  const GatherItem* items;
+  int n_items;
+  const uint32_t* bin_nslices;
+  uint32_t* counters;      // [0] work, [1] done
+  uint32_t* bin_arrive;
+  uint64_t* part;
+  uint32_t* hi;
+  double* item_red;        // [2*n_items]
+  int b;
+  int64_t n_dst;
+  int fbits;
+  // PageRank epilogue
+  double d, n;
+  const double* red_in;    // D_t at red_in[0]
+  double* red_out;         // D_{t+1} -> red_out[2], residual_t -> red_out[1]  (red_out = &red[2t])
+  const uint32_t* outdeg;
+  const float* pr_old;
+  float* pr_new;
+  float* spr_new;
+  // SpMV epilogue
+  float* y;
+};
+int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s);
+int gather_smem_bytes(int b, bool weighted);
+
+int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
+int prepare_gather(pcpm_handle* h);
+int prepare_scatter(pcpm_handle* h);
+int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, cudaStream_t s);
+int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
+                          float* spr_out, double* red_t, float d, cudaStream_t s);
+int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);
+
+}  // namespace pcpm

@@ -1,0 +1,74 @@
+// pull.cu -- PageRank initialisation (R2: PR_0 = 1/n) and the in-house
+// comparison kernel: naive pull-direction PageRank, Alg. 1,
+// one warp per destination vertex summing SPR over its in-neighbours (CSC) in
+// fp64 registers, with the same apply / dangling rule (R1) as the PCPM path.
+#include "pcpm_internal.cuh"
+
+namespace pcpm {
+namespace {
+
+__global__ void k_pr_init(int64_t n, const uint32_t* __restrict__ outdeg, int64_t n_dangling, float* pr0,
+                          float* spr, double* red, int red_n) {
+  const double inv_n = 1.0 / (double)n;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    pr0[v] = (float)inv_n;
+    const uint32_t dg = outdeg[v];
+    spr[v] = dg ? (float)(inv_n / (double)dg) : 0.0f;
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < red_n; i += blockDim.x) red[i] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) red[0] = (double)n_dangling * inv_n;   // D_0
+  }
+}
+
+__global__ void __launch_bounds__(256) k_pull(int64_t n, const uint32_t* __restrict__ in_ptr,
+                                              const uint32_t* __restrict__ in_src, const float* __restrict__ spr_in,
+                                              const uint32_t* __restrict__ outdeg, const float* __restrict__ pr_old,
+                                              float* pr_new, float* spr_out, const double* red_in, double* red_out,
+                                              double d) {
+  const int lane = threadIdx.x & 31;
+  const double base = (1.0 - d) / (double)n + d * (red_in[0] / (double)n);
+  double dang = 0.0, res = 0.0;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nw) {
+    double s = 0.0;
+    for (uint32_t e = in_ptr[v] + lane; e < in_ptr[v + 1]; e += 32) s += (double)__ldg(spr_in + in_src[e]);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const double prn = base + d * s;
+      pr_new[v] = (float)prn;
+      const uint32_t dg = outdeg[v];
+      spr_out[v] = dg ? (float)(prn / (double)dg) : 0.0f;
+      if (dg == 0) dang += prn;
+      res += fabs(prn - (double)pr_old[v]);
+    }
+  }
+  if (lane == 0) {
+    atomicAdd(&red_out[2], dang);
+    atomicAdd(&red_out[1], res);
+  }
+}
+
+}  // namespace
+
+int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, cudaStream_t s) {
+  int grid = (int)std::min<int64_t>((h->n_src + 255) / 256, h->num_sms * 8);
+  k_pr_init<<<std::max(grid, 1), 256, 0, s>>>(h->n_src, h->outdeg, h->n_dangling, pr0, spr, red, red_n);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
+  return PCPM_OK;
+}
+
+int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new, float* spr_out,
+                          double* red_t, float d, cudaStream_t s) {
+  const int grid = h->num_sms * 8;
+  k_pull<<<grid, 256, 0, s>>>(h->n_dst, h->in_ptr, h->in_src, spr_in, h->outdeg, pr_old, pr_new, spr_out, red_t,
+                              red_t, (double)d);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
+  return PCPM_OK;
+}
+
+}  // namespace pcpm

@@ -1,0 +1,331 @@
+"""Parity of the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+* layout (a0): bit-exact, every array, on fixtures, random graphs and edge cases;
+* scatter (a1): bit-exact given the same fp32 input;
+* PageRank (a1-a4): max relative error <= 1e-5 per vertex and L1 <= 1e-6 after
+  the stated iterations (BASELINE.json north_star), plus bit-reproducibility;
+* SpMV (a5): |y - y_oracle| <= 1e-5 * sum|a x| + deg * 2^-F (R19).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import graphs
+from tests.gpu_util import d2h, to_device
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def pcpm():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1709_07122_b200 import pcpm as p
+    return p
+
+
+def build(p, g, b, flags=0, device=True):
+    if device:
+        rp, col, val = to_device(g)
+        keep = (rp, col, val)
+    else:
+        rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(g.col, dtype=np.uint32)
+        val = None if g.values is None else np.ascontiguousarray(g.values, dtype=np.float32)
+        keep = (rp, col, val)
+    csr = p.make_csr(g.n_src, g.n_dst, rp, col, val)
+    h = p.pcpm_build_ex(csr, b, flags, None)
+    del keep
+    return h
+
+
+def export(p, h):
+    info = p.pcpm_get_info(h)
+    v = p.pcpm_export_layout(h)
+    m, ep, ks, kd = info.nnz, info.e_prime, info.k_src, info.k_dst
+    out = dict(
+        info=info,
+        ids=d2h(v.ids, m, np.uint32),
+        png_src=d2h(v.png_src, ep, np.uint32),
+        png_off=d2h(v.png_off, ks * (kd + 1), np.uint32).reshape(ks, kd + 1),
+        upd_off=d2h(v.upd_off, ks * kd, np.uint32).reshape(ks, kd),
+        bin_id_start=d2h(v.bin_id_start, kd + 1, np.uint32),
+        bin_upd_start=d2h(v.bin_upd_start, kd + 1, np.uint32),
+        chunk_base=d2h(v.chunk_base, (m + 2047) // 2048 * 16 + 1, np.uint32),
+        out_degree=d2h(v.out_degree, info.n_src, np.uint32),
+        w=d2h(v.w, m, np.float32) if v.w else None,
+        view=v,
+    )
+    return out
+
+
+def assert_layout_equal(g, lay_gpu, b, compress=True):
+    if compress:
+        ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, b, val=g.values)
+        ids = ref.ids
+    else:
+        ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, b, val=g.values)
+        ids = None
+    info = lay_gpu["info"]
+    assert info.k_src == ref.k_src and info.k_dst == ref.k_dst
+    if compress:
+        assert info.e_prime == ref.e_prime
+        np.testing.assert_array_equal(lay_gpu["ids"], ids)
+        np.testing.assert_array_equal(lay_gpu["png_src"], ref.png_src)
+        np.testing.assert_array_equal(lay_gpu["png_off"], ref.png_off.astype(np.uint32))
+        np.testing.assert_array_equal(lay_gpu["upd_off"], ref.upd_off.astype(np.uint32))
+        np.testing.assert_array_equal(lay_gpu["bin_upd_start"], ref.bin_upd_start.astype(np.uint32))
+    np.testing.assert_array_equal(lay_gpu["bin_id_start"], ref.bin_id_start.astype(np.uint32))
+    if g.values is not None:
+        np.testing.assert_array_equal(lay_gpu["w"], ref.w)
+    # decode anchors by their plain definition: #flags in ids[0 .. 128 c)
+    flags = (lay_gpu["ids"] >> 31).astype(np.int64)
+    cum = np.concatenate([[0], np.cumsum(flags)])
+    cb = lay_gpu["chunk_base"]
+    for c in range(len(cb)):
+        assert cb[c] == cum[min(128 * c, len(flags))]
+    np.testing.assert_array_equal(lay_gpu["out_degree"], np.diff(g.row_ptr).astype(np.uint32))
+    return ref
+
+
+def g_toy():
+    t = json.load(open(os.path.join(GOLDEN, "g_toy_layout.json")))
+    return graphs.GraphCSR("g_toy", t["n"], t["n"], np.array(t["row_ptr"], dtype=np.int64),
+                           np.array(t["col"], dtype=np.uint32))
+
+
+def star_graph(n_leaves, hub=0, inward=False):
+    n = n_leaves + 1
+    if inward:
+        rp = np.concatenate([[0, 0], np.arange(1, n_leaves + 1)]).astype(np.int64)
+        col = np.zeros(n_leaves, dtype=np.uint32)
+    else:
+        rp = np.concatenate([[0], np.full(n, n_leaves)]).astype(np.int64)
+        col = np.arange(1, n, dtype=np.uint32)
+    return graphs.GraphCSR("star", n, n, rp, col)
+
+
+LAYOUT_CASES = [
+    ("g_toy", lambda: g_toy(), 1),
+    ("c1", lambda: graphs.make_config("c1"), 8),
+    ("rmat12_b4", lambda: graphs.make_graph("rmat", 7, scale=12, permute=True), 4),
+    ("rmat12_b8", lambda: graphs.make_graph("rmat", 7, scale=12, permute=True), 8),
+    ("rmat13_b11", lambda: graphs.make_graph("rmat", 8, scale=13, permute=False), 11),
+    ("er3000_b7", lambda: graphs.make_graph("er", 5, n=3000, m_raw=50000), 7),
+    ("er_ragged_b15", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 15),
+    ("outstar_b10", lambda: star_graph(100000), 10),
+    ("instar_b3", lambda: star_graph(5000, inward=True), 3),
+    ("edgeless", lambda: graphs.GraphCSR("e", 100, 100, np.zeros(101, np.int64), np.zeros(0, np.uint32)), 4),
+    ("self_loop", lambda: graphs.GraphCSR("s", 1, 1, np.array([0, 1], np.int64), np.array([0], np.uint32)), 1),
+]
+
+
+@pytest.mark.parametrize("name,mk,b", LAYOUT_CASES, ids=[c[0] for c in LAYOUT_CASES])
+def test_layout_bit_exact(pcpm, name, mk, b):
+    g = mk()
+    h = build(pcpm, g, b)
+    try:
+        assert_layout_equal(g, export(pcpm, h), b)
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_layout_from_host_pointers_and_weights(pcpm):
+    g = graphs.make_graph("rmat", 9, scale=11, permute=True, values=True, transpose=True)
+    h = build(pcpm, g, 6, device=False)
+    try:
+        lay = export(pcpm, h)
+        assert lay["info"].weighted == 1
+        assert_layout_equal(g, lay, 6)
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_layout_uncompressed(pcpm):
+    g = graphs.make_graph("rmat", 3, scale=11, permute=True)
+    h = build(pcpm, g, 6, flags=pcpm.PCPM_NO_COMPRESS)
+    try:
+        lay = export(pcpm, h)
+        assert lay["info"].e_prime == g.m and lay["info"].compressed == 0
+        ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, 6)
+        np.testing.assert_array_equal(lay["ids"], ref.ids | np.uint32(0x80000000))
+        np.testing.assert_array_equal(lay["bin_id_start"], ref.bin_id_start.astype(np.uint32))
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_bad_csr_rejected(pcpm):
+    rp = np.array([0, 2, 3], dtype=np.int64)
+    for col, code in [(np.array([1, 0, 0], np.uint32), pcpm.PCPM_EBADCSR),    # unsorted row
+                      (np.array([1, 1, 0], np.uint32), pcpm.PCPM_EBADCSR),    # duplicate
+                      (np.array([0, 5, 0], np.uint32), pcpm.PCPM_EBADCSR)]:   # col >= n
+        with pytest.raises(pcpm.PcpmError) as e:
+            pcpm.pcpm_build(pcpm.make_csr(2, 2, rp, col), 1)
+        assert e.value.code == code
+    rp_bad = np.array([0, 3, 2], dtype=np.int64)
+    with pytest.raises(pcpm.PcpmError) as e:
+        pcpm.pcpm_build(pcpm.make_csr(2, 2, rp_bad, np.array([0, 1], np.uint32)), 1)
+    assert e.value.code == pcpm.PCPM_EBADCSR
+
+
+@pytest.mark.parametrize("name,mk,b", LAYOUT_CASES[:7], ids=[c[0] for c in LAYOUT_CASES[:7]])
+def test_scatter_bit_exact(pcpm, name, mk, b):
+    g = mk()
+    h = build(pcpm, g, b)
+    try:
+        x = np.random.default_rng(1).random(g.n_src).astype(np.float32)
+        xd = torch.from_numpy(x).cuda()
+        pcpm.pcpm_scatter(h, xd)
+        torch.cuda.synchronize()
+        v = pcpm.pcpm_export_layout(h)
+        info = pcpm.pcpm_get_info(h)
+        got = d2h(v.upd, info.e_prime, np.float32)
+        ref = oracle.scatter(oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, b), x)
+        np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32))
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def pr_check(got, ref, tag=""):
+    rel = np.abs(got.astype(np.float64) - ref) / ref
+    l1 = np.abs(got.astype(np.float64) - ref).sum()
+    assert rel.max() <= 1e-5, f"{tag} max rel {rel.max():.3e} at {rel.argmax()}"
+    assert l1 <= 1e-6, f"{tag} L1 {l1:.3e}"
+    return rel.max(), l1
+
+
+PR_CASES = [
+    ("g_toy", lambda: g_toy(), 1, 20),
+    ("c1", lambda: graphs.make_config("c1"), 8, 10),
+    ("rmat14_b10", lambda: graphs.make_graph("rmat", 12, scale=14, permute=True), 10, 20),
+    ("rmat15_b15", lambda: graphs.make_graph("rmat", 13, scale=15, permute=False), 15, 20),
+    ("er_ragged_b15", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 15, 20),
+    ("outstar", lambda: star_graph(20000), 12, 7),
+    ("instar", lambda: star_graph(20000, inward=True), 9, 7),
+    ("edgeless", lambda: graphs.GraphCSR("e", 100, 100, np.zeros(101, np.int64), np.zeros(0, np.uint32)), 4, 5),
+    ("cycle", lambda: graphs.GraphCSR("c", 1000, 1000, np.arange(1001, dtype=np.int64),
+                                      ((np.arange(1000) + 1) % 1000).astype(np.uint32)), 5, 20),
+]
+
+
+@pytest.mark.parametrize("name,mk,b,iters", PR_CASES, ids=[c[0] for c in PR_CASES])
+def test_pagerank_parity(pcpm, name, mk, b, iters):
+    g = mk()
+    h = build(pcpm, g, b, flags=pcpm.PCPM_BUILD_PULL)
+    try:
+        ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, iters)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, iters, out)
+        got = out.cpu().numpy()
+        pr_check(got, ref, name)
+        # bit-reproducible (fixed-point accumulation is order independent)
+        out2 = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(h, 0.85, iters, out2)
+        assert torch.equal(out, out2)
+        # host output pointer
+        host = np.zeros(g.n_src, dtype=np.float32)
+        pcpm.pcpm_pagerank(h, 0.85, iters, host)
+        np.testing.assert_array_equal(host, got)
+        # the pull comparison kernel computes the same vector
+        pull = torch.zeros_like(out)
+        pcpm.pcpm_pull_pagerank(h, 0.85, iters, pull)
+        pr_check(pull.cpu().numpy(), ref, name + "/pull")
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_pagerank_residuals_and_dangling_mass(pcpm):
+    g = graphs.make_graph("rmat", 12, scale=13, permute=True)
+    h = build(pcpm, g, 9)
+    try:
+        iters = 6
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, iters, out)
+        red = pcpm.pcpm_get_residuals(h)
+        deg = np.diff(g.row_ptr)
+        prs = [oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, t) for t in range(iters + 1)]
+        for t in range(iters):
+            D = prs[t][deg == 0].sum()
+            assert red[2 * t] == pytest.approx(D, rel=1e-5)
+            res = np.abs(prs[t + 1] - prs[t]).sum()
+            assert red[2 * t + 1] == pytest.approx(res, rel=1e-3, abs=1e-7)
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_pagerank_iters_zero_and_invalid(pcpm):
+    g = graphs.make_config("c1")
+    h = build(pcpm, g, 8)
+    try:
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 0, out)
+        assert torch.all(out == 1.0 / g.n_src)
+        with pytest.raises(pcpm.PcpmError):
+            pcpm.pcpm_pagerank(h, 1.5, 3, out)
+        with pytest.raises(pcpm.PcpmError):
+            pcpm.pcpm_pull_pagerank(h, 0.85, 3, out)   # built without PCPM_BUILD_PULL
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def spmv_check(g, got, x, fbits):
+    ref = oracle.spmv_t(g.n_src, g.n_dst, g.row_ptr, g.col, g.values, x)
+    absval = None if g.values is None else np.abs(g.values)
+    mag = oracle.spmv_t(g.n_src, g.n_dst, g.row_ptr, g.col, absval, np.abs(x))
+    indeg = np.bincount(g.col.astype(np.int64), minlength=g.n_dst)
+    tol = 1e-5 * mag + indeg * 2.0 ** (-fbits) + 1e-30
+    err = np.abs(got.astype(np.float64) - ref)
+    assert np.all(err <= tol), f"worst {np.max(err / tol):.3f}x tol at {np.argmax(err / tol)}"
+
+
+SPMV_CASES = [
+    ("rmat12_w", lambda: graphs.make_graph("rmat", 5, scale=12, permute=True, values=True, transpose=True), 8),
+    ("rmat15_w_b15", lambda: graphs.make_graph("rmat", 5, scale=15, permute=True, values=True, transpose=True), 15),
+    ("rmat12_unweighted", lambda: graphs.make_graph("rmat", 4, scale=12, permute=True), 6),
+]
+
+
+@pytest.mark.parametrize("name,mk,b", SPMV_CASES, ids=[c[0] for c in SPMV_CASES])
+def test_spmv_parity(pcpm, name, mk, b):
+    g = mk()
+    h = build(pcpm, g, b)
+    try:
+        x = graphs.make_x(g.n_src, 5)
+        y = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_spmv(h, torch.from_numpy(x).cuda(), y)
+        fb = pcpm.pcpm_get_info(h).fixed_point_bits
+        spmv_check(g, y.cpu().numpy(), x, fb)
+        yh = np.zeros(g.n_dst, dtype=np.float32)
+        pcpm.pcpm_spmv(h, x, yh)                       # host pointers
+        np.testing.assert_array_equal(yh, y.cpu().numpy())
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_spmv_non_square(pcpm):
+    rng = np.random.default_rng(3)
+    ns, nd = 5000, 1300
+    dens = 0.004
+    rows, cols = np.nonzero(rng.random((ns, nd)) < dens)
+    rp = np.zeros(ns + 1, dtype=np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    vals = rng.uniform(-1, 1, len(cols)).astype(np.float32)
+    g = graphs.GraphCSR("ns", ns, nd, rp, cols.astype(np.uint32), vals)
+    h = build(pcpm, g, 7)
+    try:
+        x = rng.uniform(-1, 1, ns).astype(np.float32)
+        y = np.zeros(nd, dtype=np.float32)
+        pcpm.pcpm_spmv(h, x, y)
+        spmv_check(g, y, x, pcpm.pcpm_get_info(h).fixed_point_bits)
+        with pytest.raises(pcpm.PcpmError) as e:
+            pcpm.pcpm_pagerank(h, 0.85, 2, np.zeros(ns, np.float32))
+        assert e.value.code == pcpm.PCPM_ESTATE
+    finally:
+        pcpm.pcpm_destroy(h)
