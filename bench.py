@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""bench.py -- GTEPS per PageRank iteration and achieved HBM GB/s of the PCPM hot
+path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl pcpm|reference]
+
+A step is one pcpm_pagerank call of the config's iteration count (20 for
+RMAT-26: scatter -> gather+apply per iteration, §5 protocol P:436)
+on the device-resident layout; value = m * iters * K * N / max-over-ranks time
+(GTEPS, the paper's "giga edges / runtime of a single iteration").
+The SpMV config (c5) steps 50 multiplies and reports G-nonzeros/s.
+Multi-GPU runs independent replicas (the single-graph path is not
+sharded in this round), so scaling is weak.
+
+--impl reference times the CPU oracle (oracle/, fp64 C, OpenMP) on the host
+cores on a bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GTEPS per PageRank iteration and achieved HBM GB/s (% of peak) on 1 B200"
+WORKLOADS = {
+    "c1": "c1_rmat10: RMAT scale 10 ef16 seed1 (a,b,c)=(.57,.19,.19) unpermuted, q=2^8, d=0.85, 10 iterations",
+    "c2": "c2_er20: Erdos-Renyi 2^20 vertices 2^24 raw edges seed2, q=2^15, d=0.85, 20 iterations",
+    "c3": "c3_rmat24: RMAT scale 24 ef16 seed3 random labels, q=2^15, d=0.85, 20 iterations",
+    "c4": "c4_rmat26: RMAT scale 26 ef16 seed4 random labels, q=2^15, d=0.85, 20 iterations",
+    "c5": "c5_spmv_rmat25: y=A.x, RMAT scale 25 ef16 seed5 random labels, values/x U[-1,1), q=2^15, 50 multiplies",
+}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out = self.p.communicate(timeout=5)[0]
+        except Exception:
+            self.p.kill()
+            return None
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_graph(key, device):
+    from inputs import graphs
+    return graphs.make_config(key, backend="torch", device=device)
+
+
+def layout_bytes(info, iters_kind="pagerank"):
+    """Algorithmic bytes per launch of each kernel."""
+    n, m, ep, ks, kd = info.n_src, info.nnz, info.e_prime, info.k_src, info.k_dst
+    scatter = 4 * ep + 4 * ep + 4 * n + 4 * ks * (kd + 1) + 4 * ks * kd
+    if iters_kind == "pagerank":
+        gather = 4 * m + 4 * ep + 4 * n * 4      # ids, updates; outdeg + PR_old read, PR + SPR written
+    else:
+        gather = 4 * m + 4 * m + 4 * ep + 4 * info.n_dst   # ids, weights, updates; y written
+    return scatter, gather
+
+
+# ---------------------------------------------------------------------------- PCPM arm
+
+
+def run_pcpm(args, world, rank, local):
+    import torch
+    from paper_1709_07122_b200 import model, pcpm
+
+    key = args.config
+    dev = torch.device("cuda", local)
+    g = make_graph(key, dev)
+    cfg = g.meta
+    op = cfg["op"]
+    iters = args.iters or cfg["iters"]
+    b = cfg["bits"]
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    csr = pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values)
+    flags = pcpm.PCPM_BUILD_PULL if (op == "pagerank" and not args.no_pull) else 0
+    h = pcpm.pcpm_build_ex(csr, b, flags, stream)
+    info = pcpm.pcpm_get_info(h)
+    m, n = info.nnz, info.n_src
+    pcpm.pcpm_set_option(h, "phase_timing", 1)
+    out = torch.zeros(max(g.n_src, g.n_dst), dtype=torch.float32, device=dev)
+
+    if op == "pagerank":
+        def step():
+            pcpm.pcpm_pagerank(h, 0.85, iters, out)
+        units_per_step = m * iters
+    else:
+        from inputs import graphs
+        x = graphs.make_x(g.n_src, cfg["seed"], backend="torch", device=dev)
+
+        def step():
+            for _ in range(iters):
+                pcpm.pcpm_spmv(h, x, out)
+        units_per_step = m * iters
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    launches = pcpm.pcpm_last_launch_count(h) * (iters if op != "pagerank" else 1) * args.steps
+    ms_max = max_over_ranks(ms, world)
+    ms_per_step = ms_max / args.steps
+    value = units_per_step * args.steps * world / (ms_max * 1e-3) / 1e9
+
+    # per-kernel device times of the last step (events recorded inside the graph)
+    pk = peaks()
+    peak = float(pk.get("hbm_gbs", 6650.0))
+    sb, gb = layout_bytes(info, op)
+    kernels = {}
+    if op == "pagerank":
+        ph = pcpm.pcpm_get_phase_times(h)
+        sc = [float(ph[1 + 2 * t]) for t in range(iters)]
+        ga = [float(ph[2 + 2 * t]) for t in range(iters)]
+        kernels["scatter"] = {"ms": statistics.mean(sc), "bytes": sb}
+        kernels["gather_apply"] = {"ms": statistics.mean(ga), "bytes": gb}
+        step_kernel_ms = float(np.sum(ph))
+    else:
+        # SpMV: time one scatter and one gather in isolation with events
+        s_ms, g_ms = spmv_phase_times(pcpm, h, x, out, stream)
+        kernels["scatter"] = {"ms": s_ms, "bytes": sb}
+        kernels["gather"] = {"ms": g_ms, "bytes": gb}
+        step_kernel_ms = None
+    for k, v in kernels.items():
+        v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
+        v["frac"] = v["gbs"] / peak
+    dom = "gather_apply" if op == "pagerank" else "gather"
+    iter_bytes = sb + gb
+    ms_iter = ms_per_step / iters
+    hbm_gbs = iter_bytes / (ms_iter * 1e-3) / 1e9
+    traffic = ncu_traffic(key, dom)
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "ms_per_iter": round(ms_iter, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 values, i64 fixed-point accumulation, f64 apply", "data": "synthetic (seeded RMAT/ER, inputs/)",
+        "hbm_gbs": round(hbm_gbs, 1), "hbm_frac_of_measured": round(hbm_gbs / peak, 4),
+        "hbm_frac_of_8tbs_spec": round(hbm_gbs / 8000.0, 4),
+        "config": {"workload": WORKLOADS[key], "n": n, "m": m, "k": info.k_dst, "q": info.q,
+                   "e_prime": info.e_prime, "r": round(info.r, 4), "iters": iters, "partition_bits": b,
+                   "n_dangling": info.n_dangling, "build_ms": round(info.build_ms, 2),
+                   "gather_items": info.gather_items, "scatter_items": info.scatter_items,
+                   "fixed_point_bits": info.fixed_point_bits,
+                   "l2": "inputs larger than L2 (no flush)" if iter_bytes > 4 * 132e6 else
+                         "working set fits in L2 (no flush; numbers are L2-assisted)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(kernels[dom]["gbs"], 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(kernels[dom]["frac"], 4), "traffic": traffic,
+                     "alg_bytes_per_launch": kernels[dom]["bytes"],
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if not pk.get("_fallback") else "fallback"},
+        "kernels": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                    for k, v in kernels.items()},
+        "model_bytes_per_iter": {
+            "alg_this_build": iter_bytes,
+            "paper_eq5_pcpm": round(model.pcpm_comm(n, m, info.k_dst, info.r if info.r > 0 else 1)),
+            "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
+            "paper_eq4_bvgas": round(model.bvgas_comm(n, m)),
+        },
+        "clocks": clk,
+        "gpu_launches": int(launches),
+    }
+    if op == "pagerank" and not args.no_pull:
+        pull_ms = time_pull(pcpm, h, out, iters, stream)
+        line["pull_comparison"] = {"ms_per_iter": round(pull_ms / iters, 5),
+                                   "gteps": round(m * iters / (pull_ms * 1e-3) / 1e9, 3)}
+    pcpm.pcpm_destroy(h)
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, g, b, iters, op, world)
+    del out
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(g, key, op, iters, budget_s=args.cpu_budget)
+    return line
+
+
+def spmv_phase_times(pcpm, h, x, y, stream):
+    import torch
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    s_t, g_t = [], []
+    for _ in range(5):
+        e[0].record(stream)
+        pcpm.pcpm_scatter(h, x)
+        e[1].record(stream)
+        pcpm.pcpm_spmv(h, x, y)    # scatter + gather
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        s_t.append(e[0].elapsed_time(e[1]))
+        g_t.append(e[1].elapsed_time(e[2]) - e[0].elapsed_time(e[1]))
+    return statistics.median(s_t), statistics.median(g_t)
+
+
+def time_pull(pcpm, h, out, iters, stream):
+    import torch
+    pcpm.pcpm_pull_pagerank(h, 0.85, iters, out)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(2):
+        pcpm.pcpm_pull_pagerank(h, 0.85, iters, out)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 2
+
+
+def e2e(args, g, b, iters, op, world):
+    """Same metric through the public C ABI with HOST buffers: H2D of the CSR,
+    the GPU build, the iterations and the D2H of the result inside the timed region."""
+    import torch
+    from paper_1709_07122_b200 import pcpm
+    rp = torch.empty(g.row_ptr.numel(), dtype=torch.int64, pin_memory=True)
+    col = torch.empty(g.col.numel(), dtype=torch.int32, pin_memory=True)
+    rp.copy_(g.row_ptr)
+    col.copy_(g.col)
+    val = None
+    if g.values is not None:
+        val = torch.empty(g.values.numel(), dtype=torch.float32, pin_memory=True)
+        val.copy_(g.values)
+    res = torch.empty(max(g.n_src, g.n_dst), dtype=torch.float32, pin_memory=True)
+    x = None
+    if op != "pagerank":
+        from inputs import graphs
+        x = torch.from_numpy(graphs.make_x(g.n_src, g.meta["seed"])).pin_memory()
+    csr = pcpm.make_csr(g.n_src, g.n_dst, rp, col, val)
+    m = int(g.row_ptr[-1].item())
+    nsteps = max(1, min(args.steps, 3))
+    times = []
+    for i in range(nsteps + 1):
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        h = pcpm.pcpm_build_ex(csr, b, 0, None)
+        if op == "pagerank":
+            pcpm.pcpm_pagerank(h, 0.85, iters, res)
+        else:
+            for _ in range(iters):
+                pcpm.pcpm_spmv(h, x, res)
+        pcpm.pcpm_destroy(h)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if i > 0:                      # first pass warms the allocator / module
+            times.append(t1 - t0)
+    t = max_over_ranks(statistics.mean(times), world)
+    h2d = rp.numel() * 8 + col.numel() * 4 + (0 if val is None else val.numel() * 4)
+    d2h = res.numel() * 4 if op == "pagerank" else res.numel() * 4 * iters
+    if op != "pagerank":
+        h2d += x.numel() * 4 * iters
+    return {"value": round(m * iters * world / t / 1e9, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "seconds_per_step": round(t, 4), "includes": "H2D CSR + GPU build + iterations + D2H result"}
+
+
+def ncu_traffic(key, kernel):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d[key][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def cpu_baseline(g, key, op, iters, budget_s=20.0):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+    import oracle
+    gn = g.to_numpy()
+    n, m = gn.n_src, gn.m
+    cores = oracle.num_threads()
+    if op == "pagerank":
+        t0 = time.perf_counter()
+        in_ptr, in_src = oracle.transpose(n, gn.row_ptr, gn.col)
+        t_tr = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        oracle.pagerank_pull(n, gn.row_ptr, in_ptr, in_src, 0.85, 1)
+        t1 = time.perf_counter() - t0
+        k = int(max(1, min(iters, budget_s / max(t1, 1e-6))))
+        if k > 1:
+            t0 = time.perf_counter()
+            oracle.pagerank_pull(n, gn.row_ptr, in_ptr, in_src, 0.85, k)
+            t1 = (time.perf_counter() - t0) / k
+        return {"value": round(m / t1 / 1e9, 4), "unit": "GTEPS", "cores": cores, "kind": "oracle",
+                "sample": f"{k} of {iters} iterations of the fp64 pull oracle on the full {key} graph "
+                          f"(its CSC transpose, {t_tr:.1f} s, excluded); {t1 * 1e3:.1f} ms/iteration"}
+    x = None
+    from inputs import graphs
+    x = graphs.make_x(n, gn.meta["seed"])
+    t0 = time.perf_counter()
+    oracle.spmv_t(gn.n_src, gn.n_dst, gn.row_ptr, gn.col, gn.values, x)
+    t1 = time.perf_counter() - t0
+    return {"value": round(m / t1 / 1e9, 4), "unit": "G-nnz/s", "cores": 1, "kind": "oracle",
+            "sample": f"1 of {iters} multiplies of the fp64 oracle SpMV (single-threaded) on the full {key} matrix; "
+                      f"{t1 * 1e3:.1f} ms/multiply"}
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+
+def run_reference(args, world, rank, local):
+    if rank != 0:
+        return None
+    import torch
+    key = args.config
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else "cpu"
+    g = make_graph(key, dev)
+    op = g.meta["op"]
+    iters = args.iters or g.meta["iters"]
+    base = cpu_baseline(g, key, op, iters, budget_s=args.cpu_budget)
+    # steps: one oracle iteration (pagerank) / multiply (spmv) each on the full graph
+    import oracle
+    gn = g.to_numpy()
+    n, m = gn.n_src, gn.m
+    if op == "pagerank":
+        in_ptr, in_src = oracle.transpose(n, gn.row_ptr, gn.col)
+
+        def step():
+            oracle.pagerank_pull(n, gn.row_ptr, in_ptr, in_src, 0.85, 1)
+    else:
+        from inputs import graphs
+        x = graphs.make_x(n, gn.meta["seed"])
+
+        def step():
+            oracle.spmv_t(gn.n_src, gn.n_dst, gn.row_ptr, gn.col, gn.values, x)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = m * args.steps / dt / 1e9
+    unit = "GTEPS" if op == "pagerank" else "G-nnz/s"
+    base["value"] = round(value, 4)
+    base["sample"] = f"each step = 1 of {iters} " + ("iterations" if op == "pagerank" else "multiplies") + \
+                     f" of the fp64 oracle on the full {key} graph"
+    return {"metric": METRIC, "value": round(value, 4), "unit": unit, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RMAT/ER, inputs/)",
+            "config": {"workload": WORKLOADS[key], "n": n, "m": m, "iters": iters},
+            "cpu_baseline": base,
+            "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS) + ["all"])
+    ap.add_argument("--impl", default="pcpm", choices=["pcpm", "reference"])
+    ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pull", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    keys = sorted(WORKLOADS) if args.config == "all" else [args.config]
+    for key in keys:
+        args.config = key
+        if args.impl == "reference":
+            line = run_reference(args, world, rank, local)
+        else:
+            line = run_pcpm(args, world, rank, local)
+        if rank == 0 and line is not None:
+            s = json.dumps(line)
+            print(s, flush=True)
+            if args.out:
+                with open(args.out, "a") as f:
+                    f.write(s + "\n")
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,12 @@ int pcpm_scatter(pcpm_handle* h, const float* x);
 int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value);
 /* Kernel launches issued by the last pcpm_pagerank / pcpm_spmv call (per call). */
 int64_t pcpm_last_launch_count(const pcpm_handle* h);
+/* Per-kernel device times (ms, CUDA events on the handle's stream, recorded
+ * inside the captured graph) of the last pcpm_pagerank / pcpm_pull_pagerank
+ * call when option "phase_timing" is 1: ms[0] = init, then for t = 0..iters-1
+ * ms[1+2t] = scatter_t, ms[2+2t] = gather_t (pull: ms[1+t] = pull_t).
+ * Returns the number of floats written (synchronises the stream). */
+int pcpm_get_phase_times(pcpm_handle* h, float* ms, int cap);
 
 #ifdef __cplusplus
 }

@@ -89,11 +89,6 @@ int pr_fixed_bits(int64_t n) {
   return std::min(60, std::max(30, 26 + ceil_log2((uint64_t)n)));
 }
 
-int spmv_fixed_bits(uint32_t max_in_degree) {
-  // |y| <= in-degree (|w|, |x| <= 1 for the BASELINE inputs); keep 2 bits of headroom.
-  return std::min(52, 61 - ceil_log2((uint64_t)max_in_degree + 1));
-}
-
 GatherArgs base_args(pcpm_handle* h, int fbits) {
   GatherArgs a{};
   a.ids = h->ids;
@@ -115,17 +110,36 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   return a;
 }
 
+int mark(pcpm_handle* h, cudaStream_t s) {
+  if (!h->opt_phase_timing) return PCPM_OK;
+  if ((int)h->events.size() <= h->n_events_used) {
+    cudaEvent_t e;
+    PCPM_CK(cudaEventCreate(&e));
+    h->events.push_back(e);
+  }
+  // inside stream capture an event record must be an external node to be timeable
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  PCPM_CK(cudaStreamIsCapturing(s, &st));
+  const unsigned fl = (st == cudaStreamCaptureStatusActive) ? cudaEventRecordExternal : cudaEventRecordDefault;
+  PCPM_CK(cudaEventRecordWithFlags(h->events[h->n_events_used++], s, fl));
+  return PCPM_OK;
+}
+
 int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
   int rc;
   const int fbits = pr_fixed_bits(h->n_src);
   h->fixed_bits = fbits;
+  h->n_events_used = 0;
+  if ((rc = mark(h, s))) return rc;
   if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, s))) return rc;
+  if ((rc = mark(h, s))) return rc;
   if (iters == 0) {
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
     return PCPM_OK;
   }
   for (int t = 0; t < iters; ++t) {
     if ((rc = launch_scatter(h, h->spr, s))) return rc;          // Alg. 4
+    if ((rc = mark(h, s))) return rc;
     GatherArgs a = base_args(h, fbits);
     a.d = d;
     a.n = (double)h->n_src;
@@ -135,6 +149,7 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
     a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
     a.spr_new = h->spr;
     if ((rc = launch_gather(h, a, false, true, s))) return rc;  // Alg. 5 + apply
+    if ((rc = mark(h, s))) return rc;
   }
   return PCPM_OK;
 }
@@ -142,7 +157,10 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
 int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
   int rc;
   float* sprb[2] = {h->spr, h->xbuf};
+  h->n_events_used = 0;
+  if ((rc = mark(h, s))) return rc;
   if ((rc = launch_pr_init(h, h->pr[0], sprb[0], h->red, h->red_cap, s))) return rc;
+  if ((rc = mark(h, s))) return rc;
   if (iters == 0) {
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
     return PCPM_OK;
@@ -151,6 +169,7 @@ int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s)
     float* pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
     if ((rc = launch_pull_iteration(h, sprb[t & 1], h->pr[t & 1], pr_new, sprb[(t + 1) & 1], h->red + 2 * t, d, s)))
       return rc;
+    if ((rc = mark(h, s))) return rc;
   }
   return PCPM_OK;
 }
@@ -324,7 +343,7 @@ int pcpm_spmv(pcpm_handle* h, const float* x, float* y) {
   h->launches = 0;
   int rc = launch_scatter(h, xd, s);                                       // Alg. 4 on x
   if (rc) return rc;
-  const int fbits = spmv_fixed_bits(h->max_in_degree);
+  const int fbits = 0;   // SpMV accumulates in fp32 (gather.cu, R19)
   h->fixed_bits = fbits;
   GatherArgs a = base_args(h, fbits);
   a.y = yd;
@@ -356,6 +375,7 @@ void pcpm_destroy(pcpm_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   else cudaDeviceSynchronize();
   free_graph(h);
+  for (cudaEvent_t e : h->events) cudaEventDestroy(e);
   for (void* p : h->allocs)
     if (p) cudaFree(p);
   delete h;
@@ -447,6 +467,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     set_error(PCPM_EINVAL, "NULL handle or key");
     return PCPM_EINVAL;
   }
+  if (!strcmp(key, "phase_timing")) {
+    h->opt_phase_timing = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
   if (!strcmp(key, "use_graph")) {
     h->opt_use_graph = (int)value;
     free_graph(h);
@@ -457,5 +482,17 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
 }
 
 int64_t pcpm_last_launch_count(const pcpm_handle* h) { return h ? h->launches : 0; }
+
+int pcpm_get_phase_times(pcpm_handle* h, float* ms, int cap) {
+  if (!h || !ms) {
+    set_error(PCPM_EINVAL, "NULL handle or buffer");
+    return PCPM_EINVAL;
+  }
+  if (!h->opt_phase_timing || h->n_events_used < 2) return 0;
+  PCPM_CK(cudaStreamSynchronize(h->stream));
+  const int n = std::min(cap, h->n_events_used - 1);
+  for (int i = 0; i < n; ++i) PCPM_CK(cudaEventElapsedTime(&ms[i], h->events[i], h->events[i + 1]));
+  return n;
+}
 
 }  // extern "C"

@@ -179,24 +179,21 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           if (x >= m.lo && x < m.hi) {
             const uint32_t li = id & qmask;                      // id &= bitmask (partition-local)
             const float val = win_s[ptr - m.win_base];
-            uint32_t tlo, thi;
             if constexpr (PR) {
               // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
               const unsigned long long T = __float2ull_rn(val * fscale);
-              tlo = (uint32_t)T;
-              thi = (uint32_t)(T >> 32);
+              const uint32_t tlo = (uint32_t)T, thi = (uint32_t)(T >> 32);
+              const uint32_t old = atomicAdd(&acc[li], tlo);
+              const uint32_t hinc = thi + ((old + tlo < old) ? 1u : 0u);
+              if (hinc != 0u) {
+                atomicAdd(&a.hi[v0 + li], hinc);
+                atomicOr(&bitmap[li >> 5], 1u << (li & 31));
+              }
             } else {
-              // SpMV: signed two's-complement fixed point; w * x is exact in fp64
-              const double tv = W ? (double)val * (double)w_s[off] : (double)val;
-              const long long T = __double2ll_rn(tv * dscale);
-              tlo = (uint32_t)T;
-              thi = (uint32_t)((unsigned long long)T >> 32);
-            }
-            const uint32_t old = atomicAdd(&acc[li], tlo);
-            const uint32_t hinc = thi + ((old + tlo < old) ? 1u : 0u);
-            if (hinc != 0u) {
-              atomicAdd(&a.hi[v0 + li], hinc);
-              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
+              // SpMV: signed terms cross zero constantly, which would make a
+              // fixed-point low word wrap on most adds; fp32 accumulation is
+              // within 1e-5 * sum|a x| (R19), so use smem f32 atomics.
+              atomicAdd(reinterpret_cast<float*>(&acc[li]), W ? val * w_s[off] : val);
             }
           }
         }
@@ -215,7 +212,12 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       if (nsl > 1) {
         for (int64_t i = ctid; i < q; i += kCons) {
           const uint32_t lo = acc[i];
-          if (lo) atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), (unsigned long long)lo);
+          if (lo) {
+            if constexpr (PR)
+              atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), (unsigned long long)lo);
+            else
+              atomicAdd(reinterpret_cast<float*>(a.part) + v0 + i, __uint_as_float(lo));
+          }
           acc[i] = 0u;
         }
         __threadfence();
@@ -234,6 +236,19 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       if (run_apply) {
         for (int64_t i = ctid; i < cnt; i += kCons) {
           const uint32_t v = v0 + (uint32_t)i;
+          if constexpr (!PR) {
+            float y;
+            if (nsl > 1) {
+              float* pf = reinterpret_cast<float*>(a.part) + v;
+              y = __ldcg(pf);
+              *pf = 0.0f;
+            } else {
+              y = __uint_as_float(acc[i]);
+              acc[i] = 0u;
+            }
+            a.y[v] = y;
+            continue;
+          }
           uint64_t tot;
           if (nsl > 1) {
             tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);

@@ -103,7 +103,9 @@ struct pcpm_handle {
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
-  int opt_scatter_stage = 1;
+  int opt_phase_timing = 0;
+  std::vector<cudaEvent_t> events;  // phase-timing events (created on demand)
+  int n_events_used = 0;
 
   pcpm::Graph graph;
 };

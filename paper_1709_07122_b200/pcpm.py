@@ -28,7 +28,8 @@ PCPM_KEEP_VALUES = 0x4
 
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
-            "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count"]
+            "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
+            "pcpm_get_phase_times"]
 
 
 class PcpmError(RuntimeError):
@@ -84,6 +85,7 @@ def _load():
         "pcpm_scatter": (I, [P, P]),
         "pcpm_set_option": (I, [P, ctypes.c_char_p, I64]),
         "pcpm_last_launch_count": (I64, [P]),
+        "pcpm_get_phase_times": (I, [P, P, I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -208,3 +210,11 @@ def pcpm_get_residuals(h, cap: int = 4096) -> np.ndarray:
 
 def pcpm_last_launch_count(h) -> int:
     return int(_lib.pcpm_last_launch_count(h))
+
+
+def pcpm_get_phase_times(h, cap: int = 8192) -> np.ndarray:
+    buf = np.zeros(cap, dtype=np.float32)
+    n = _lib.pcpm_get_phase_times(h, _ptr(buf), int(cap))
+    if n < 0:
+        _check(n)
+    return buf[:n]

@@ -279,7 +279,7 @@ def spmv_check(g, got, x, fbits):
     absval = None if g.values is None else np.abs(g.values)
     mag = oracle.spmv_t(g.n_src, g.n_dst, g.row_ptr, g.col, absval, np.abs(x))
     indeg = np.bincount(g.col.astype(np.int64), minlength=g.n_dst)
-    tol = 1e-5 * mag + indeg * 2.0 ** (-fbits) + 1e-30
+    tol = 1e-5 * mag + (indeg * 2.0 ** (-fbits) if fbits > 0 else 0.0) + 1e-30
     err = np.abs(got.astype(np.float64) - ref)
     assert np.all(err <= tol), f"worst {np.max(err / tol):.3f}x tol at {np.argmax(err / tol)}"
 
@@ -302,8 +302,8 @@ def test_spmv_parity(pcpm, name, mk, b):
         fb = pcpm.pcpm_get_info(h).fixed_point_bits
         spmv_check(g, y.cpu().numpy(), x, fb)
         yh = np.zeros(g.n_dst, dtype=np.float32)
-        pcpm.pcpm_spmv(h, x, yh)                       # host pointers
-        np.testing.assert_array_equal(yh, y.cpu().numpy())
+        pcpm.pcpm_spmv(h, x, yh)                       # host pointers (fp32 order may differ: R19)
+        spmv_check(g, yh, x, fb)
     finally:
         pcpm.pcpm_destroy(h)
 
