@@ -129,6 +129,7 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
   int rc;
   const int fbits = pr_fixed_bits(h->n_src);
   h->fixed_bits = fbits;
+  h->last_was_spmv = false;
   h->n_events_used = 0;
   if ((rc = mark(h, s))) return rc;
   if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, s))) return rc;
@@ -341,12 +342,15 @@ int pcpm_spmv(pcpm_handle* h, const float* x, float* y) {
   }
   float* yd = dev_y ? y : h->ybuf;
   h->launches = 0;
-  int rc = launch_scatter(h, xd, s);                                       // Alg. 4 on x
+  int rc = launch_absmax(h, xd, h->n_src, h->xmax, s);                    // fixed-point scale of this x
   if (rc) return rc;
-  const int fbits = 0;   // SpMV accumulates in fp32 (gather.cu, R19)
-  h->fixed_bits = fbits;
-  GatherArgs a = base_args(h, fbits);
+  rc = launch_scatter(h, xd, s);                                           // Alg. 4 on x
+  if (rc) return rc;
+  h->last_was_spmv = true;
+  GatherArgs a = base_args(h, 0);
   a.y = yd;
+  a.xmax = h->xmax;
+  a.wexp = h->weighted ? h->wexp : 0;
   rc = launch_gather(h, a, h->weighted, false, s);                         // Alg. 5 with weights (§3.5)
   if (rc) return rc;
   if (!dev_y) {
@@ -425,6 +429,17 @@ int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
   i.gather_items = h->n_gitems;
   i.scatter_items = h->n_sitems;
   i.fixed_point_bits = h->fixed_bits;
+  if (h->last_was_spmv && h->xmax) {   // same rule as spmv_fbits() in gather.cu
+    float xm = 0.f;
+    if (cudaMemcpy(&xm, h->xmax, 4, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      int ex = 0;
+      if (xm > 0.f) frexpf(xm, &ex);
+      const int F = 30 - (h->weighted ? h->wexp : 0) - ex;
+      i.fixed_point_bits = F < -120 ? -120 : (F > 62 ? 62 : F);
+    } else {
+      cudaGetLastError();
+    }
+  }
   *out = i;
   return PCPM_OK;
 }

@@ -173,17 +173,6 @@ __global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_
   if (threadIdx.x == 0) atomicAdd(n_dangling, (unsigned long long)s);
 }
 
-__global__ void k_indeg_hist(int64_t m, const uint32_t* __restrict__ col, uint32_t* indeg) {
-  GRID_STRIDE(e, m) atomicAdd(&indeg[col[e]], 1u);
-}
-
-__global__ void k_max(int64_t n, const uint32_t* __restrict__ a, uint32_t* out) {
-  uint32_t mx = 0;
-  GRID_STRIDE(i, n) mx = max(mx, a[i]);
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
-}
-
 __global__ void k_item_f(int n_items, GatherItem* items, const uint32_t* __restrict__ chunk_base,
                          const uint32_t* __restrict__ bin_upd_start) {
   GRID_STRIDE(i, n_items) {
@@ -408,17 +397,18 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       TK(cudaGetLastError());
       h->has_pull = true;
     }
-    // ---- max in-degree (fixed-point range of the signed SpMV accumulator)
-    {
-      uint32_t *indeg, *mx;
-      TK(tmp.alloc(&indeg, n_dst));
+    // ---- max|w| (fixed-point range of the signed SpMV accumulator)
+    if (values) {
+      float* mx;
       TK(tmp.alloc(&mx, 1));
-      TK(cudaMemsetAsync(indeg, 0, sizeof(uint32_t) * n_dst, s));
-      TK(cudaMemsetAsync(mx, 0, 4, s));
-      k_indeg_hist<<<grid_for(m), kT, 0, s>>>(m, col, indeg);
-      k_max<<<grid_for(n_dst), kT, 0, s>>>(n_dst, indeg, mx);
-      TK(cudaGetLastError());
-      TK(cudaMemcpyAsync(&h->max_in_degree, mx, 4, cudaMemcpyDeviceToHost, s));
+      float hmx = 0.f;
+      int rc2 = launch_absmax(h, values, m, mx, s);
+      if (rc2) return rc2;
+      TK(cudaMemcpyAsync(&hmx, mx, 4, cudaMemcpyDeviceToHost, s));
+      TK(cudaStreamSynchronize(s));
+      int ex = 0;
+      if (hmx > 0.f) frexpf(hmx, &ex);
+      h->wexp = ex;
     }
   } else {
     h->e_prime = 0;
@@ -541,6 +531,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
   if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
   TK(cudaMemsetAsync(h->part, 0, sizeof(uint64_t) * n_dst, s));
   TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));

@@ -8,19 +8,20 @@
 //  * Persistent CTAs (one per SM, 128 KB accumulator = one destination
 //    partition of q = 2^15 vertices in shared memory).  Work items are slices
 //    of destination bins, largest first, claimed with an atomic counter.
-//  * Warp 0 is the producer: for each 2048-ID tile it issues three bulk async
+//  * Warp 0 is the producer: for each 2048-ID tile it issues bulk async
 //    copies (TMA engine, cp.async.bulk) into a 4-stage ring: the IDs, the
 //    window of update values those IDs reference, and 16 decode anchors.
 //  * 16 consumer warps each decode one 128-ID sub-chunk of the tile.  The
 //    update pointer of Alg. 5 becomes a warp prefix count of MSB flags:
 //    ptr = anchor + popc(ballot(flags) & lanemask_le) - 1  (reading R5's -1
-//    start), with no data-dependent branch.
-//  * Accumulation is 64-bit fixed point (F fractional bits): the low word
-//    lives in shared memory and is updated with native 32-bit integer
-//    ATOMS.ADD; the rare carries go to a global high word (and a smem bitmap
-//    marks them).  Integer sums are exact and order-independent, so results
-//    are bit-reproducible (fp32 atomics fail the
-//    1e-5 bound at the scale-26 hubs and are CAS loops on sm_100a).
+//    start), with no data-dependent branch.  The four 32-ID steps of a
+//    sub-chunk are decoded together so their loads and atomics overlap.
+//  * PageRank accumulates in 64-bit fixed point (F fractional bits): the low
+//    word lives in shared memory and is updated with native 32-bit integer
+//    ATOMS.ADD; the rare carries go to a global high word (a smem bitmap marks
+//    them).  Integer sums are exact and order-independent, so results are
+//    bit-reproducible (fp32 sums fail the 1e-5 bound
+//    at the scale-26 hubs, and fp32 smem atomics are CAS loops on sm_100a).
 //  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
 //    PR'/outdeg; per-item dangling mass and L1 residual, reduced in fixed
 //    order by the last CTA.  Split bins flush their low words to a global
@@ -34,11 +35,12 @@ constexpr uint32_t kFlagLast = 1u, kFlagEmpty = 2u, kFlagStop = 4u;
 
 struct StageMeta {
   int item;
+  uint32_t j;            // destination partition of the item
   uint32_t lo, hi;       // valid ID range of this tile [lo, hi)
   uint32_t tile_base;    // first ID position of the tile
   uint32_t win_base;     // update index of win[0]
   uint32_t flags;
-  uint32_t pad[2];
+  uint32_t pad;
 };
 
 template <bool W>
@@ -54,6 +56,26 @@ struct Cfg {
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ uint64_t ldcg_u64(const uint64_t* p) {
   return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+__device__ int spmv_fbits(float xmax, int wexp) {
+  int ex = 0;
+  if (xmax > 0.0f) frexpf(xmax, &ex);          // xmax <= 2^ex
+  const int F = 30 - wexp - ex;
+  return F < -120 ? -120 : (F > 62 ? 62 : F);
+}
+
+namespace {
+
+__global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
+  float mx = 0.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, fabsf(x[i]));
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
 }
 
 template <bool W, bool PR>
@@ -97,6 +119,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           mbar_wait(&empty[stage], phase ^ 1);
           StageMeta m{};
           m.item = stop ? -1 : (int)it;
+          m.j = stop ? 0u : item.j;
           m.flags = stop ? kFlagStop : (kFlagLast | kFlagEmpty);
           meta[stage] = m;
           mbar_arrive(&full[stage]);
@@ -115,6 +138,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           mbar_wait(&empty[stage], phase ^ 1);
           StageMeta m{};
           m.item = (int)it;
+          m.j = item.j;
           m.lo = lo;
           m.hi = hi;
           m.tile_base = tb;
@@ -140,15 +164,23 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   const int cw = warp - 1;                  // 0..15: sub-chunk owned in every tile
   const int ctid = threadIdx.x - 32;        // 0..511
   constexpr int kCons = 32 * kConsumerWarps;
+  constexpr int kSteps = kChunkIds / 32;    // 4 steps of 32 IDs
   const uint32_t qmask = (uint32_t)(q - 1);
   const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F
-  const double dscale = (double)fscale;
-  const double inv_scale = 1.0 / dscale;
+  const double inv_scale = 1.0 / (double)fscale;
   for (int64_t i = ctid; i < q; i += kCons) acc[i] = 0u;
   for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
   double base_pr = 0.0;
   if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+  // SpMV scale: F = 30 - ceil(log2 max|w|) - ceil(log2 max|x|), so |w x| 2^F <= 2^30
+  double sp_scale = 1.0, sp_inv = 1.0;
+  if constexpr (!PR) {
+    const int F = spmv_fbits(*a.xmax, a.wexp);
+    sp_scale = ldexp(1.0, F);
+    sp_inv = ldexp(1.0, -F);
+  }
   named_bar_sync(1, kCons);
+  const uint32_t lmask = lanemask_le();
 
   int stage = 0;
   uint32_t phase = 0;
@@ -156,8 +188,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
     mbar_wait(&full[stage], phase);
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;
-    const GatherItem item = a.items[m.item];
-    const uint32_t v0 = item.j << a.b;
+    const uint32_t v0 = m.j << a.b;
     if (!(m.flags & kFlagEmpty)) {
       const uint8_t* sb = stage_base + stage * C::kStageBytes;
       const uint32_t* ids_s = reinterpret_cast<const uint32_t*>(sb);
@@ -166,34 +197,69 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
       const uint32_t xs = m.tile_base + cw * kChunkIds;
       if (xs < m.hi && xs + kChunkIds > m.lo) {
-        uint32_t fb = cb_s[cw];               // #flags before xs (global decode identity)
-        const uint32_t lmask = lanemask_le();
+        // decode the sub-chunk's 4 x 32 IDs together (ILP across steps)
+        uint32_t id[kSteps], ptr[kSteps];
+        bool ok[kSteps];
+        float val[kSteps];
+        uint32_t run = cb_s[cw];               // #flags before xs (global decode identity)
 #pragma unroll
-        for (int st = 0; st < kChunkIds / 32; ++st) {
-          const uint32_t off = cw * kChunkIds + st * 32 + lane;
-          const uint32_t x = m.tile_base + off;
-          const uint32_t id = ids_s[off];
-          const uint32_t bal = __ballot_sync(0xffffffffu, id >> 31);
-          const uint32_t ptr = fb + __popc(bal & lmask) - 1;   // Alg. 5: update_ptr += MSB(id)
-          fb += __popc(bal);
-          if (x >= m.lo && x < m.hi) {
-            const uint32_t li = id & qmask;                      // id &= bitmask (partition-local)
-            const float val = win_s[ptr - m.win_base];
-            if constexpr (PR) {
-              // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
-              const unsigned long long T = __float2ull_rn(val * fscale);
-              const uint32_t tlo = (uint32_t)T, thi = (uint32_t)(T >> 32);
-              const uint32_t old = atomicAdd(&acc[li], tlo);
-              const uint32_t hinc = thi + ((old + tlo < old) ? 1u : 0u);
-              if (hinc != 0u) {
-                atomicAdd(&a.hi[v0 + li], hinc);
-                atomicOr(&bitmap[li >> 5], 1u << (li & 31));
-              }
-            } else {
-              // SpMV: signed terms cross zero constantly, which would make a
-              // fixed-point low word wrap on most adds; fp32 accumulation is
-              // within 1e-5 * sum|a x| (R19), so use smem f32 atomics.
-              atomicAdd(reinterpret_cast<float*>(&acc[li]), W ? val * w_s[off] : val);
+        for (int k = 0; k < kSteps; ++k) id[k] = ids_s[cw * kChunkIds + k * 32 + lane];
+#pragma unroll
+        for (int k = 0; k < kSteps; ++k) {
+          const uint32_t bal = __ballot_sync(0xffffffffu, id[k] >> 31);
+          ptr[k] = run + __popc(bal & lmask) - 1;   // Alg. 5: update_ptr += MSB(id)
+          run += __popc(bal);
+          const uint32_t x = xs + k * 32 + lane;
+          ok[k] = x >= m.lo && x < m.hi;
+        }
+#pragma unroll
+        for (int k = 0; k < kSteps; ++k) val[k] = ok[k] ? win_s[ptr[k] - m.win_base] : 0.0f;
+        if constexpr (PR) {
+          // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
+          uint32_t tlo[kSteps], thi[kSteps], old[kSteps];
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) {
+            const unsigned long long T = __float2ull_rn(val[k] * fscale);
+            tlo[k] = (uint32_t)T;
+            thi[k] = (uint32_t)(T >> 32);
+          }
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) old[k] = ok[k] ? atomicAdd(&acc[id[k] & qmask], tlo[k]) : 0u;
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) {
+            const uint32_t hinc = thi[k] + ((old[k] + tlo[k] < old[k]) ? 1u : 0u);
+            if (ok[k] && hinc != 0u) {        // rare: carry out of the low word
+              const uint32_t li = id[k] & qmask;
+              atomicAdd(&a.hi[v0 + li], hinc);
+              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
+            }
+          }
+        } else {
+          // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
+          // word is read as a signed int32, so a running sum that hovers
+          // around zero never wraps; only signed overflow of the low word
+          // (|partial| >= 2^31 units) carries +-1 into the global high word.
+          // w*x is exact in fp64; F keeps |w x| 2^F < 2^31 (R19).
+          uint32_t tlo[kSteps], old[kSteps];
+          int32_t thi[kSteps];
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) {
+            const double tv = W ? (double)val[k] * (double)w_s[cw * kChunkIds + k * 32 + lane] : (double)val[k];
+            const long long T = __double2ll_rn(tv * sp_scale);
+            tlo[k] = (uint32_t)T;
+            thi[k] = (int32_t)(T >> 32) + ((int32_t)tlo[k] < 0 ? 1 : 0);   // T = thi*2^32 + (int32)tlo
+          }
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) old[k] = ok[k] ? atomicAdd(&acc[id[k] & qmask], tlo[k]) : 0u;
+#pragma unroll
+          for (int k = 0; k < kSteps; ++k) {
+            const uint32_t nw = old[k] + tlo[k];
+            const bool ovf = (int32_t)((old[k] ^ nw) & (tlo[k] ^ nw)) < 0;
+            const int32_t hinc = thi[k] + (ovf ? ((int32_t)old[k] < 0 ? -1 : 1) : 0);
+            if (ok[k] && hinc != 0) {
+              const uint32_t li = id[k] & qmask;
+              atomicAdd(&a.hi[v0 + li], (uint32_t)hinc);
+              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
             }
           }
         }
@@ -207,25 +273,24 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       // ---------------- epilogue of this item ----------------
       named_bar_sync(1, kCons);
       const int64_t cnt = min(q, a.n_dst - (int64_t)v0);
-      const uint32_t nsl = a.bin_nslices[item.j];
+      const uint32_t nsl = a.bin_nslices[m.j];
       bool run_apply = true;
       if (nsl > 1) {
         for (int64_t i = ctid; i < q; i += kCons) {
           const uint32_t lo = acc[i];
           if (lo) {
-            if constexpr (PR)
-              atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), (unsigned long long)lo);
-            else
-              atomicAdd(reinterpret_cast<float*>(a.part) + v0 + i, __uint_as_float(lo));
+            // PageRank: unsigned low word; SpMV: balanced (signed) low word, sign-extended
+            const unsigned long long add = PR ? (unsigned long long)lo : (unsigned long long)(long long)(int32_t)lo;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), add);
           }
           acc[i] = 0u;
         }
         __threadfence();
         named_bar_sync(1, kCons);
         if (ctid == 0) {
-          const uint32_t old = atomicAdd(&a.bin_arrive[item.j], 1u);
+          const uint32_t old = atomicAdd(&a.bin_arrive[m.j], 1u);
           const bool last = old == nsl - 1;
-          if (last) a.bin_arrive[item.j] = 0u;
+          if (last) a.bin_arrive[m.j] = 0u;
           *flag_s = last ? 1u : 0u;
         }
         named_bar_sync(1, kCons);
@@ -234,44 +299,78 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       }
       double dang = 0.0, res = 0.0;
       if (run_apply) {
-        for (int64_t i = ctid; i < cnt; i += kCons) {
-          const uint32_t v = v0 + (uint32_t)i;
-          if constexpr (!PR) {
-            float y;
+        if constexpr (PR) {
+          // total of local vertex i (exact u64 fixed point); resets the state it reads
+          auto total = [&](int64_t i) -> uint64_t {
+            const uint32_t v = v0 + (uint32_t)i;
+            uint64_t tot;
             if (nsl > 1) {
-              float* pf = reinterpret_cast<float*>(a.part) + v;
-              y = __ldcg(pf);
-              *pf = 0.0f;
+              tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
+              a.part[v] = 0ull;
+              a.hi[v] = 0u;
             } else {
-              y = __uint_as_float(acc[i]);
+              tot = acc[i];
+              if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
+                tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+                a.hi[v] = 0u;
+              }
               acc[i] = 0u;
             }
-            a.y[v] = y;
-            continue;
-          }
-          uint64_t tot;
-          if (nsl > 1) {
-            tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
-            a.part[v] = 0ull;
-            a.hi[v] = 0u;
-          } else {
-            tot = acc[i];
-            if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
-              tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
-              a.hi[v] = 0u;
+            return tot;
+          };
+          const bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
+                           aligned16(a.spr_new + v0) && aligned16(a.outdeg + v0);
+          if (vec) {
+            const uint4* dg4 = reinterpret_cast<const uint4*>(a.outdeg + v0);
+            const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
+            float4* pn4 = reinterpret_cast<float4*>(a.pr_new + v0);
+            float4* sp4 = reinterpret_cast<float4*>(a.spr_new + v0);
+#pragma unroll 2
+            for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
+              const uint4 dg = __ldg(dg4 + i4);
+              const float4 po = __ldg(po4 + i4);
+              const uint32_t dgv[4] = {dg.x, dg.y, dg.z, dg.w};
+              const float pov[4] = {po.x, po.y, po.z, po.w};
+              float pn[4], sp[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
+                pn[c] = (float)prn;
+                sp[c] = dgv[c] ? (float)(prn / (double)dgv[c]) : 0.0f;
+                dang += dgv[c] ? 0.0 : prn;
+                res += fabs(prn - (double)pov[c]);
+              }
+              pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
+              sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
             }
-            acc[i] = 0u;
-          }
-          const double sum = (double)(long long)tot * inv_scale;
-          if constexpr (PR) {
-            const double prn = base_pr + a.d * sum;
-            a.pr_new[v] = (float)prn;
-            const uint32_t dg = __ldg(a.outdeg + v);
-            a.spr_new[v] = dg ? (float)(prn / (double)dg) : 0.0f;
-            if (dg == 0) dang += prn;
-            res += fabs(prn - (double)a.pr_old[v]);
           } else {
-            a.y[v] = (float)sum;
+            for (int64_t i = ctid; i < cnt; i += kCons) {
+              const uint32_t v = v0 + (uint32_t)i;
+              const double prn = base_pr + a.d * ((double)(long long)total(i) * inv_scale);
+              a.pr_new[v] = (float)prn;
+              const uint32_t dg = __ldg(a.outdeg + v);
+              a.spr_new[v] = dg ? (float)(prn / (double)dg) : 0.0f;
+              if (dg == 0) dang += prn;
+              res += fabs(prn - (double)a.pr_old[v]);
+            }
+          }
+        } else {
+          for (int64_t i = ctid; i < cnt; i += kCons) {
+            const uint32_t v = v0 + (uint32_t)i;
+            long long tot;
+            if (nsl > 1) {
+              tot = (long long)ldcg_u64(&a.part[v]) + (long long)((uint64_t)ldcg_u32(&a.hi[v]) << 32);
+              a.part[v] = 0ull;
+              a.hi[v] = 0u;
+            } else {
+              tot = (long long)(int32_t)acc[i];
+              if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
+                tot += (long long)((uint64_t)ldcg_u32(&a.hi[v]) << 32);
+                a.hi[v] = 0u;
+              }
+              acc[i] = 0u;
+            }
+            a.y[v] = (float)((double)tot * sp_inv);
           }
         }
       }
@@ -315,7 +414,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
     __threadfence();
     if constexpr (PR) {
       if (cw == 0) {
-        // pairwise-free fixed order: lane-strided partial sums, then a fixed shuffle tree
+        // fixed order: lane-strided partial sums, then a fixed shuffle tree
         double sd = 0.0, sr = 0.0;
         for (int i = lane; i < a.n_items; i += 32) {
           sd += __ldcg(&a.item_red[2 * i]);
@@ -362,6 +461,15 @@ int prepare_gather(pcpm_handle* h) {
   for (int w = 0; w < 2; ++w)
     for (int p = 0; p < 2; ++p)
       PCPM_CK(cudaFuncSetAttribute(gather_fn(w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  return PCPM_OK;
+}
+
+int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s) {
+  PCPM_CK(cudaMemsetAsync(out, 0, sizeof(float), s));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, h->num_sms * 4));
+  k_absmax<<<grid, 256, 0, s>>>(n, x, out);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
   return PCPM_OK;
 }
 

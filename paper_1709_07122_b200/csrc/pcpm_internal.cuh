@@ -74,7 +74,9 @@ struct pcpm_handle {
   uint32_t* chunk_base = nullptr;   // [m_pad/kChunkIds + 1]
   uint32_t* outdeg = nullptr;       // [n_src]
   float* upd = nullptr;             // [E' + 8]
-  uint32_t max_in_degree = 0;
+  int wexp = 0;                     // max|w| <= 2^wexp (SpMV fixed-point scale)
+  float* xmax = nullptr;            // [1] device max|x| of the last pcpm_spmv
+  bool last_was_spmv = false;
 
   // pull comparison (CSC)
   uint32_t* in_ptr = nullptr;       // [n_dst+1]
@@ -216,7 +218,11 @@ struct GatherArgs {
   float* spr_new;
   // SpMV epilogue
   float* y;
+  const float* xmax;       // device max|x| of this call (fixed-point scale)
+  int wexp;                // max|w| <= 2^wexp
 };
+__device__ int spmv_fbits(float xmax, int wexp);
+int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s);
 int gather_smem_bytes(int b, bool weighted);
 

@@ -20,8 +20,10 @@ k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __res
           int64_t k_dst, const uint32_t* __restrict__ png_src, const uint32_t* __restrict__ png_off,
           const uint32_t* __restrict__ upd_off, float* __restrict__ upd) {
   extern __shared__ float4 smem_f4[];
+  __shared__ uint32_t next_group;
+  constexpr int kUnroll = 4;
   float* xs = reinterpret_cast<float*>(smem_f4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t q = int64_t(1) << b;
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const ScatterItem item = items[it];
@@ -37,14 +39,27 @@ k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __res
     } else {
       for (int64_t i = threadIdx.x; i < len; i += blockDim.x) xs[i] = __ldg(src + i);
     }
+    if (threadIdx.x == 0) next_group = 0;
     __syncthreads();
     const uint32_t* off = png_off + (int64_t)item.p * (k_dst + 1);
     const uint32_t* uo = upd_off + (int64_t)item.p * k_dst;
     const uint32_t ubase = (uint32_t)base;
-    for (uint32_t j = item.j0 + warp; j < item.j1; j += nwarps) {
-      const uint32_t s = __ldg(off + j), e = __ldg(off + j + 1);
+    for (;;) {
+      // groups (p, j) are claimed dynamically: their sizes vary by orders of magnitude
+      uint32_t g = 0;
+      if (lane == 0) g = atomicAdd(&next_group, 1u);
+      const uint32_t j = item.j0 + __shfl_sync(0xffffffffu, g, 0);
+      if (j >= item.j1) break;
+      const uint32_t s = __ldg(off + j), len = __ldg(off + j + 1) - s;
       const uint32_t dst = __ldg(uo + j);
-      for (uint32_t t = lane; t < e - s; t += 32) upd[dst + t] = xs[__ldg(png_src + s + t) - ubase];
+      for (uint32_t t = lane; t < len; t += 32 * kUnroll) {
+        uint32_t src[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) src[k] = (t + 32 * k < len) ? __ldg(png_src + s + t + 32 * k) : ubase;
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k)
+          if (t + 32 * k < len) upd[dst + t + 32 * k] = xs[src[k] - ubase];
+      }
     }
     __syncthreads();
   }
