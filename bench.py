@@ -131,14 +131,18 @@ def make_graph(key, device):
     return graphs.make_config(key, backend="torch", device=device)
 
 
-def layout_bytes(info, iters_kind="pagerank"):
-    """Algorithmic bytes per launch of each kernel."""
+def layout_bytes(info, iters_kind="pagerank", wide=False):
+    """Algorithmic bytes per launch of each kernel.
+
+    d_i = 2 (compact layout: 2-byte IDs and PNG sources) or 4 (PCPM_WIDE_IDS), d_v = 4.
+    """
     n, m, ep, ks, kd = info.n_src, info.nnz, info.e_prime, info.k_src, info.k_dst
-    scatter = 4 * ep + 4 * ep + 4 * n + 4 * ks * (kd + 1) + 4 * ks * kd
+    di = 4 if wide else 2
+    scatter = di * ep + 4 * ep + 4 * n + 4 * ks * (kd + 1) + 4 * ks * kd
     if iters_kind == "pagerank":
-        gather = 4 * m + 4 * ep + 4 * n * 4      # ids, updates; outdeg + PR_old read, PR + SPR written
+        gather = di * m + 4 * ep + 4 * n * 4      # ids, updates; outdeg + PR_old read, PR + SPR written
     else:
-        gather = 4 * m + 4 * m + 4 * ep + 4 * info.n_dst   # ids, weights, updates; y written
+        gather = di * m + 4 * m + 4 * ep + 4 * info.n_dst   # ids, weights, updates; y written
     return scatter, gather
 
 
@@ -160,6 +164,8 @@ def run_pcpm(args, world, rank, local):
     stream = torch.cuda.current_stream()
     csr = pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values)
     flags = pcpm.PCPM_BUILD_PULL if (op == "pagerank" and not args.no_pull) else 0
+    if args.wide:
+        flags |= pcpm.PCPM_WIDE_IDS
     h = pcpm.pcpm_build_ex(csr, b, flags, stream)
     info = pcpm.pcpm_get_info(h)
     m, n = info.nnz, info.n_src
@@ -206,7 +212,7 @@ def run_pcpm(args, world, rank, local):
     # per-kernel device times of the last step (events recorded inside the graph)
     pk = peaks()
     peak = float(pk.get("hbm_gbs", 6650.0))
-    sb, gb = layout_bytes(info, op)
+    sb, gb = layout_bytes(info, op, args.wide)
     kernels = {}
     if op == "pagerank":
         ph = pcpm.pcpm_get_phase_times(h)
@@ -253,7 +259,9 @@ def run_pcpm(args, world, rank, local):
                     for k, v in kernels.items()},
         "model_bytes_per_iter": {
             "alg_this_build": iter_bytes,
+            "layout": "wide (d_i=4)" if args.wide else "compact (d_i=2)",
             "paper_eq5_pcpm": round(model.pcpm_comm(n, m, info.k_dst, info.r if info.r > 0 else 1)),
+            "paper_eq5_pcpm_d_i_2": round(model.pcpm_comm(n, m, info.k_dst, info.r if info.r > 0 else 1, d_i=2)),
             "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
             "paper_eq4_bvgas": round(model.bvgas_comm(n, m)),
         },
@@ -329,7 +337,7 @@ def e2e(args, g, b, iters, op, world):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
-        h = pcpm.pcpm_build_ex(csr, b, 0, None)
+        h = pcpm.pcpm_build_ex(csr, b, pcpm.PCPM_WIDE_IDS if args.wide else 0, None)
         if op == "pagerank":
             pcpm.pcpm_pagerank(h, 0.85, iters, res)
         else:
@@ -453,6 +461,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     keys = sorted(WORKLOADS) if args.config == "all" else [args.config]

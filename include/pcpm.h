@@ -49,6 +49,11 @@ extern "C" {
                                   the BVGAS-like traffic baseline of P:342-345, measured with our layout */
 #define PCPM_BUILD_PULL 0x2u   /* also build the in-adjacency (CSC) for pcpm_pull_pagerank */
 #define PCPM_KEEP_VALUES 0x4u  /* keep weight bins even if values == NULL (all ones) */
+#define PCPM_WIDE_IDS 0x8u     /* iterate on the paper's 4-byte layout (global 31-bit IDs + MSB flag in
+                                  destID bins, 4-byte PNG sources) instead of the default
+                                  compact one (2-byte partition-local IDs: 15-bit offset + MSB flag,
+                                  2-byte PNG sources; the "smallest number of bits" of P:589).  Both
+                                  encode the same bins; the compact one moves half the index bytes. */
 
 /* A CSR matrix M with n_src rows and n_dst columns: row u lists the columns
  * v with M[u][v] != 0, i.e. the out-neighbours of u (push form).
@@ -81,7 +86,9 @@ typedef struct {
   int32_t fixed_point_bits; /* F of the last pcpm_pagerank / pcpm_spmv call */
 } pcpm_info;
 
-/* Device pointers to the built layout, for bit-exact tests (read-only). */
+/* Device pointers to the built layout, for bit-exact tests (read-only).
+ * The compact arrays (ids16, png_src16) always exist; the 4-byte arrays
+ * (ids, png_src) only for handles built with PCPM_WIDE_IDS (else NULL). */
 typedef struct {
   const uint32_t* ids;           /* [nnz] destID bins concatenated in j order; v | flag<<31 */
   const float* w;                /* [nnz] weights aligned with ids, or NULL */
@@ -96,6 +103,9 @@ typedef struct {
   const uint32_t* out_degree;    /* [n_src] |N_o(u)| */
   float* upd;                    /* [E'] update bins of the last scatter (scratch) */
   int64_t chunk_ids;             /* IDs per chunk_base entry (128) */
+  const uint16_t* ids16;         /* [nnz] compact destID bins: (v & (q-1)) | flag<<15 */
+  const uint16_t* png_src16;     /* [E'] compact PNG sources: u & (q-1) (u is in partition p) */
+  int32_t wide;                  /* 1 when the kernels iterate on the 4-byte arrays */
 } pcpm_layout_view;
 
 /* Build the PCPM layout on the GPU (§3.1-3.3): validation,

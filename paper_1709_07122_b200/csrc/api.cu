@@ -91,7 +91,7 @@ int pr_fixed_bits(int64_t n) {
 
 GatherArgs base_args(pcpm_handle* h, int fbits) {
   GatherArgs a{};
-  a.ids = h->ids;
+  a.ids = h->wide ? static_cast<const void*>(h->ids) : static_cast<const void*>(h->ids16);
   a.w = h->w;
   a.upd = h->upd;
   a.chunk_base = h->chunk_base;
@@ -461,6 +461,9 @@ int pcpm_export_layout(pcpm_handle* h, pcpm_layout_view* out) {
   v.out_degree = h->outdeg;
   v.upd = h->upd;
   v.chunk_ids = kChunkIds;
+  v.ids16 = h->ids16;
+  v.png_src16 = h->png16;
+  v.wide = h->wide ? 1 : 0;
   *out = v;
   return PCPM_OK;
 }

@@ -97,13 +97,21 @@ __global__ void k_boundaries(int64_t m, const uint32_t* __restrict__ sorted_keys
   }
 }
 
+// ids[x] = v | flag << 31 (4-byte form), ids16[x] = (v & (q-1)) | flag << 15 (compact form)
 __global__ void k_gather_ids(int64_t m, const uint32_t* __restrict__ perm, const uint32_t* __restrict__ enc,
-                             const float* __restrict__ values, uint32_t* ids, float* w) {
+                             const float* __restrict__ values, uint32_t qmask, uint32_t* ids, uint16_t* ids16,
+                             float* w) {
   GRID_STRIDE(x, m) {
     uint32_t e = perm[x];
-    ids[x] = enc[e];
+    const uint32_t id = enc[e];
+    ids[x] = id;
+    ids16[x] = (uint16_t)((id & qmask) | ((id >> 31) << 15));
     if (w) w[x] = values ? values[e] : 1.0f;
   }
+}
+
+__global__ void k_png16(int64_t ep, const uint32_t* __restrict__ png, uint32_t qmask, uint16_t* png16) {
+  GRID_STRIDE(i, ep) png16[i] = (uint16_t)(png[i] & qmask);
 }
 
 __global__ void k_png_keys(int64_t ep, const uint32_t* __restrict__ sel, const uint32_t* __restrict__ rowid,
@@ -243,8 +251,9 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   h->m = m;
   h->compressed = !(flags & PCPM_NO_COMPRESS);
   h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
-  h->m_pad = ((m + kTileIds - 1) / kTileIds) * kTileIds;
-  if (h->m_pad == 0) h->m_pad = kTileIds;
+  h->wide = (flags & PCPM_WIDE_IDS) != 0;
+  h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
+  if (h->m_pad == 0) h->m_pad = kTileAlign;
 
   Temp tmp;
   // ---- inputs on the device
@@ -285,7 +294,15 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 
   // ---- layout arrays owned by the handle
   int rc;
-  if ((rc = dev_alloc_t(h, &h->ids, h->m_pad))) return rc;
+  uint32_t* ids32 = nullptr;           // 4-byte IDs: handle-owned for wide handles, else scratch
+  if (h->wide) {
+    if ((rc = dev_alloc_t(h, &h->ids, h->m_pad))) return rc;
+    ids32 = h->ids;
+  } else {
+    TK(tmp.alloc(&ids32, h->m_pad));
+  }
+  if ((rc = dev_alloc_t(h, &h->ids16, h->m_pad))) return rc;
+  TK(cudaMemsetAsync(h->ids16, 0, sizeof(uint16_t) * h->m_pad, s));
   if (h->weighted && (rc = dev_alloc_t(h, &h->w, h->m_pad))) return rc;
   if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1)))) return rc;
   if ((rc = dev_alloc_t(h, &h->upd_off, k_src * k_dst))) return rc;
@@ -294,7 +311,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   const int64_t nchunks = h->m_pad / kChunkIds;
   if ((rc = dev_alloc_t(h, &h->chunk_base, nchunks + 1))) return rc;
   if ((rc = dev_alloc_t(h, &h->outdeg, n_src))) return rc;
-  TK(cudaMemsetAsync(h->ids, 0, sizeof(uint32_t) * h->m_pad, s));
+  TK(cudaMemsetAsync(ids32, 0, sizeof(uint32_t) * h->m_pad, s));
   if (h->w) TK(cudaMemsetAsync(h->w, 0, sizeof(float) * h->m_pad, s));
 
   // ---- out-degrees and dangling count
@@ -350,7 +367,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(radix_sort_pairs(tmp, keyj, keyj_s, iota, perm, m, bits_for((uint64_t)std::max<int64_t>(k_dst - 1, 0)), s));
     k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keyj_s, k_dst, h->bin_id_start);
     TK(cudaGetLastError());
-    k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, h->ids, h->w);
+    k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, (uint32_t)(q - 1), ids32, h->ids16, h->w);
     TK(cudaGetLastError());
 
     // ---- PNG: flagged edges, stable sort by (p, j)
@@ -368,17 +385,26 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(cudaMemcpyAsync(&ep, d_nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     TK(cudaStreamSynchronize(s));
     h->e_prime = ep;
-    if ((rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+    uint32_t* png32 = nullptr;
+    if (h->wide) {
+      if ((rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+      png32 = h->png_src;
+    } else {
+      TK(tmp.alloc(&png32, ep + 8));
+    }
+    if ((rc = dev_alloc_t(h, &h->png16, ep + 16))) return rc;
     if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
     TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+    TK(cudaMemsetAsync(h->png16, 0, sizeof(uint16_t) * (ep + 16), s));
     uint32_t *pk, *pv, *pk_s;
     TK(tmp.alloc(&pk, ep));
     TK(tmp.alloc(&pv, ep));
     TK(tmp.alloc(&pk_s, ep));
     k_png_keys<<<grid_for(ep), kT, 0, s>>>(ep, sel, rowid, col, b, k_dst, pk, pv);
     TK(cudaGetLastError());
-    TK(radix_sort_pairs(tmp, pk, pk_s, pv, h->png_src, ep, bits_for((uint64_t)(k_src * k_dst - 1)), s));
+    TK(radix_sort_pairs(tmp, pk, pk_s, pv, png32, ep, bits_for((uint64_t)(k_src * k_dst - 1)), s));
     k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk_s, k_src * k_dst, G);
+    k_png16<<<grid_for(ep), kT, 0, s>>>(ep, png32, (uint32_t)(q - 1), h->png16);
     TK(cudaGetLastError());
 
     // ---- pull comparison: CSC (in-adjacency), sources ascending per destination
@@ -412,7 +438,8 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     }
   } else {
     h->e_prime = 0;
-    if ((rc = dev_alloc_t(h, &h->png_src, 8))) return rc;
+    if (h->wide && (rc = dev_alloc_t(h, &h->png_src, 8))) return rc;
+    if ((rc = dev_alloc_t(h, &h->png16, 16))) return rc;
     if ((rc = dev_alloc_t(h, &h->upd, 8))) return rc;
     TK(cudaMemsetAsync(h->upd, 0, 32, s));
     TK(cudaMemsetAsync(G, 0, sizeof(uint32_t) * (k_src * k_dst + 1), s));
@@ -445,7 +472,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   {
     uint32_t* cnt;
     TK(tmp.alloc(&cnt, nchunks + 1));
-    k_chunk_counts<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, h->ids, cnt);
+    k_chunk_counts<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, ids32, cnt);
     TK(cudaGetLastError());
     size_t bytes = 0;
     TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, h->chunk_base, nchunks + 1, s));
@@ -469,14 +496,14 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   // paper's dynamic scheduling).
   std::vector<GatherItem> gi;
   std::vector<uint32_t> nsl(k_dst, 0);
-  int64_t slice = std::max<int64_t>(4 * kTileIds, ((m / (2 * h->num_sms)) / kTileIds + 1) * kTileIds);
+  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (2 * h->num_sms)) / kTileAlign + 1) * kTileAlign);
   for (int64_t j = 0; j < k_dst; ++j) {
     int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
     int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
     int64_t per = (sz + nslc - 1) / nslc;
     std::vector<int64_t> cuts{s0};
     for (int64_t i = 1; i < nslc; ++i) {
-      int64_t c = ((s0 + i * per + kTileIds - 1) / kTileIds) * kTileIds;
+      int64_t c = ((s0 + i * per + kTileAlign - 1) / kTileAlign) * kTileAlign;
       if (c > cuts.back() && c < s1) cuts.push_back(c);
     }
     cuts.push_back(s1);
@@ -506,7 +533,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     int64_t acc = 0, j0 = 0;
     for (int64_t j = 0; j < k_dst; ++j) {
       acc += hG[p * k_dst + j + 1] - hG[p * k_dst + j];
-      if (acc >= target) {
+      if (acc >= target || j + 1 - j0 >= kScatterMaxGroups) {   // item offsets fit in smem
         si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)(j + 1), (uint32_t)acc});
         acc = 0;
         j0 = j + 1;

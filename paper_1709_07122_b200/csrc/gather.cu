@@ -8,24 +8,30 @@
 //  * Persistent CTAs (one per SM, 128 KB accumulator = one destination
 //    partition of q = 2^15 vertices in shared memory).  Work items are slices
 //    of destination bins, largest first, claimed with an atomic counter.
-//  * Warp 0 is the producer: for each 2048-ID tile it issues bulk async
-//    copies (TMA engine, cp.async.bulk) into a 4-stage ring: the IDs, the
-//    window of update values those IDs reference, and 16 decode anchors.
-//  * 16 consumer warps each decode one 128-ID sub-chunk of the tile.  The
-//    update pointer of Alg. 5 becomes a warp prefix count of MSB flags:
-//    ptr = anchor + popc(ballot(flags) & lanemask_le) - 1  (reading R5's -1
-//    start), with no data-dependent branch.  The four 32-ID steps of a
-//    sub-chunk are decoded together so their loads and atomics overlap.
+//  * Warp 0 is the producer: for each tile it issues bulk async copies (TMA
+//    engine, cp.async.bulk) into a 4-stage ring: the IDs (4096 2-byte IDs in
+//    the compact layout), the window of update values they reference, and
+//    the decode anchors.
+//  * 16 consumer warps each decode one sub-chunk of the tile, 8 (or 4)
+//    consecutive IDs per lane from one 16-byte load.  The update pointer of
+//    Alg. 5 becomes a warp prefix count of MSB flags:
+//    ptr = anchor + (flags in lower lanes, by ballot/popc) + (own flags so far) - 1
+//    (reading R5's -1 start), with no data-dependent branch; all loads and
+//    atomics of a sub-chunk are independent, so they overlap.
 //  * PageRank accumulates in 64-bit fixed point (F fractional bits): the low
 //    word lives in shared memory and is updated with native 32-bit integer
-//    ATOMS.ADD; the rare carries go to a global high word (a smem bitmap marks
-//    them).  Integer sums are exact and order-independent, so results are
-//    bit-reproducible (fp32 sums fail the 1e-5 bound
-//    at the scale-26 hubs, and fp32 smem atomics are CAS loops on sm_100a).
+//    ATOMS.ADD; the rare carries go to a global high word (a coarse smem bitmap
+//    marks groups of 32 vertices that have one).  Integer sums are exact and
+//    order-independent, so results are bit-reproducible (DESIGN.md
+//    "accumulator": fp32 sums fail the 1e-5 bound at the scale-26 hubs, and
+//    fp32 smem atomics are CAS loops on sm_100a).  SpMV uses the signed
+//    ("balanced") variant of the same accumulator.
 //  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
 //    PR'/outdeg; per-item dangling mass and L1 residual, reduced in fixed
 //    order by the last CTA.  Split bins flush their low words to a global
 //    u64 partial and the last-arriving slice runs the epilogue.
+#include <type_traits>
+
 #include "pcpm_internal.cuh"
 
 namespace pcpm {
@@ -43,14 +49,22 @@ struct StageMeta {
   uint32_t pad;
 };
 
-template <bool W>
+template <typename IdT, bool W>
 struct Cfg {
-  static constexpr int kStages = W ? 3 : 4;
-  static constexpr int kIdsBytes = kTileIds * 4;
+  static constexpr bool kCompact = sizeof(IdT) == 2;
+  static constexpr int kTile = (kCompact && !W) ? 2 * kTileIds : kTileIds;
+  static constexpr int kStages = (!kCompact && W) ? 3 : 4;
+  static constexpr int kSub = kTile / kConsumerWarps;      // IDs per warp per tile
+  static constexpr int kPer = kSub / 32;                   // IDs per lane (one vector load)
+  static constexpr int kIdsBytes = kTile * (int)sizeof(IdT);
+  static constexpr int kWinCap = kTile + 8;                // >= #flags + 1, 16 B aligned ends
   static constexpr int kWinBytes = kWinCap * 4;
-  static constexpr int kWBytes = W ? kTileIds * 4 : 0;
-  static constexpr int kCbBytes = kChunksPerTile * 4;
+  static constexpr int kWBytes = W ? kTile * 4 : 0;
+  static constexpr int kCbBytes = (kTile / kChunkIds) * 4;
   static constexpr int kStageBytes = kIdsBytes + kWinBytes + kWBytes + kCbBytes;
+  static constexpr int kFlagShift = kCompact ? 15 : 31;
+  static_assert(kTileAlign % kTile == 0, "slices are cut at tile multiples");
+  static_assert(kStageBytes % 16 == 0, "bulk copies need 16 B alignment");
 };
 
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
@@ -58,6 +72,38 @@ __device__ __forceinline__ uint64_t ldcg_u64(const uint64_t* p) {
   return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t r;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+  return r;
+}
+
+// kPer consecutive IDs of this lane from one vector load
+template <typename IdT, int P>
+__device__ __forceinline__ void load_ids(const IdT* p, uint32_t (&id)[P]) {
+  if constexpr (sizeof(IdT) == 2 && P == 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      id[2 * c] = w[c] & 0xFFFFu;
+      id[2 * c + 1] = w[c] >> 16;
+    }
+  } else if constexpr (sizeof(IdT) == 2 && P == 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    id[0] = v.x & 0xFFFFu;
+    id[1] = v.x >> 16;
+    id[2] = v.y & 0xFFFFu;
+    id[3] = v.y >> 16;
+  } else {
+    static_assert(sizeof(IdT) == 4 && P == 4, "layout");
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    id[0] = v.x;
+    id[1] = v.y;
+    id[2] = v.z;
+    id[3] = v.w;
+  }
+}
 
 }  // namespace
 
@@ -78,21 +124,23 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
 }
 
-template <bool W, bool PR>
+template <typename IdT, bool W, bool PR>
 __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a) {
-  using C = Cfg<W>;
+  using C = Cfg<IdT, W>;
   constexpr int S = C::kStages;
+  constexpr int P = C::kPer;
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t q = int64_t(1) << a.b;
   uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // q words (128 B rounded)
-  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;                           // q/32 words (>= 4)
-  const int bm_words = (int)((q + 31) / 32) < 4 ? 4 : (int)((q + 31) / 32);
+  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;                           // 1 bit per 32 vertices
+  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + ((bm_words + 31) / 32) * 32);
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
   uint64_t* empty = full + S;
   double* red_s = reinterpret_cast<double*>(empty + S);                    // 2*kConsumerWarps
   uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * kConsumerWarps);
+  const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -127,10 +175,10 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           if (stop) break;
           continue;
         }
-        const uint32_t t0 = item.x0 / kTileIds, t1 = (item.x1 - 1) / kTileIds;
+        const uint32_t t0 = item.x0 / C::kTile, t1 = (item.x1 - 1) / C::kTile;
         for (uint32_t t = t0; t <= t1; ++t) {
-          const uint32_t tb = t * kTileIds;
-          const uint32_t lo = max(tb, item.x0), hi = min(tb + kTileIds, item.x1);
+          const uint32_t tb = t * C::kTile;
+          const uint32_t lo = max(tb, item.x0), hi = min(tb + C::kTile, item.x1);
           const uint32_t flo = (lo == item.x0) ? item.fx0 : __ldg(a.chunk_base + lo / kChunkIds);
           const uint32_t fhi = (hi == item.x1) ? item.fx1 : __ldg(a.chunk_base + hi / kChunkIds);
           const uint32_t wlo = flo > 0 ? flo - 1 : 0;
@@ -148,7 +196,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           uint8_t* sb = stage_base + stage * C::kStageBytes;
           const uint32_t win_bytes = (ahi - alo) * 4;
           mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
-          bulk_g2s(sb, a.ids + tb, C::kIdsBytes, &full[stage], pol);
+          bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
           bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
           bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
                    &full[stage], pol);
@@ -164,9 +212,8 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   const int cw = warp - 1;                  // 0..15: sub-chunk owned in every tile
   const int ctid = threadIdx.x - 32;        // 0..511
   constexpr int kCons = 32 * kConsumerWarps;
-  constexpr int kSteps = kChunkIds / 32;    // 4 steps of 32 IDs
   const uint32_t qmask = (uint32_t)(q - 1);
-  const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F
+  const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F (PageRank)
   const double inv_scale = 1.0 / (double)fscale;
   for (int64_t i = ctid; i < q; i += kCons) acc[i] = 0u;
   for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
@@ -180,7 +227,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
     sp_inv = ldexp(1.0, -F);
   }
   named_bar_sync(1, kCons);
-  const uint32_t lmask = lanemask_le();
+  const uint32_t ltmask = lanemask_lt();
 
   int stage = 0;
   uint32_t phase = 0;
@@ -191,78 +238,103 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
     const uint32_t v0 = m.j << a.b;
     if (!(m.flags & kFlagEmpty)) {
       const uint8_t* sb = stage_base + stage * C::kStageBytes;
-      const uint32_t* ids_s = reinterpret_cast<const uint32_t*>(sb);
+      const IdT* ids_s = reinterpret_cast<const IdT*>(sb);
       const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
       const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
       const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
-      const uint32_t xs = m.tile_base + cw * kChunkIds;
-      if (xs < m.hi && xs + kChunkIds > m.lo) {
-        // decode the sub-chunk's 4 x 32 IDs together (ILP across steps)
-        uint32_t id[kSteps], ptr[kSteps];
-        bool ok[kSteps];
-        float val[kSteps];
-        uint32_t run = cb_s[cw];               // #flags before xs (global decode identity)
+      const uint32_t xs = m.tile_base + cw * C::kSub;        // first ID position of this warp's sub-chunk
+      if (xs < m.hi && xs + C::kSub > m.lo) {
+        const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
+        auto body = [&](auto WHOLE) {
+          constexpr bool kWhole = decltype(WHOLE)::value;
+          uint32_t id[P];
+          load_ids<IdT, P>(ids_s + cw * C::kSub + P * lane, id);
+          // prefix count of MSB flags (global decode identity)
+          uint32_t before = 0, total = 0;
 #pragma unroll
-        for (int k = 0; k < kSteps; ++k) id[k] = ids_s[cw * kChunkIds + k * 32 + lane];
-#pragma unroll
-        for (int k = 0; k < kSteps; ++k) {
-          const uint32_t bal = __ballot_sync(0xffffffffu, id[k] >> 31);
-          ptr[k] = run + __popc(bal & lmask) - 1;   // Alg. 5: update_ptr += MSB(id)
-          run += __popc(bal);
-          const uint32_t x = xs + k * 32 + lane;
-          ok[k] = x >= m.lo && x < m.hi;
-        }
-#pragma unroll
-        for (int k = 0; k < kSteps; ++k) val[k] = ok[k] ? win_s[ptr[k] - m.win_base] : 0.0f;
-        if constexpr (PR) {
-          // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
-          uint32_t tlo[kSteps], thi[kSteps], old[kSteps];
-#pragma unroll
-          for (int k = 0; k < kSteps; ++k) {
-            const unsigned long long T = __float2ull_rn(val[k] * fscale);
-            tlo[k] = (uint32_t)T;
-            thi[k] = (uint32_t)(T >> 32);
+          for (int c = 0; c < P; ++c) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (id[c] >> C::kFlagShift) & 1u);
+            before += __popc(bal & ltmask);
+            total += __popc(bal);
           }
+          const uint32_t base = cb_s[(cw * C::kSub) / kChunkIds] + before - 1 - m.win_base;
+          uint32_t own = 0;
+          float val[P];
+          bool ok[P];
 #pragma unroll
-          for (int k = 0; k < kSteps; ++k) old[k] = ok[k] ? atomicAdd(&acc[id[k] & qmask], tlo[k]) : 0u;
+          for (int c = 0; c < P; ++c) {
+            own += (id[c] >> C::kFlagShift) & 1u;               // Alg. 5: update_ptr += MSB(id)
+            const uint32_t x = xs + P * lane + c;
+            ok[c] = kWhole || (x >= m.lo && x < m.hi);
+            val[c] = ok[c] ? win_s[base + own] : 0.0f;
+          }
+          (void)total;
+          if constexpr (PR) {
+            // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
+            uint32_t tlo[P], thi[P], old[P];
 #pragma unroll
-          for (int k = 0; k < kSteps; ++k) {
-            const uint32_t hinc = thi[k] + ((old[k] + tlo[k] < old[k]) ? 1u : 0u);
-            if (ok[k] && hinc != 0u) {        // rare: carry out of the low word
-              const uint32_t li = id[k] & qmask;
-              atomicAdd(&a.hi[v0 + li], hinc);
-              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
+            for (int c = 0; c < P; ++c) {
+              const unsigned long long T = __float2ull_rn(val[c] * fscale);
+              tlo[c] = (uint32_t)T;
+              thi[c] = (uint32_t)(T >> 32);
+            }
+#pragma unroll
+            for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+            uint32_t any = 0;
+            uint32_t hinc[P];
+#pragma unroll
+            for (int c = 0; c < P; ++c) {
+              hinc[c] = ok[c] ? thi[c] + ((old[c] + tlo[c] < old[c]) ? 1u : 0u) : 0u;
+              any |= hinc[c];
+            }
+            if (any) {                                   // rare: carry out of a low word
+#pragma unroll
+              for (int c = 0; c < P; ++c)
+                if (hinc[c]) {
+                  const uint32_t li = id[c] & qmask;
+                  atomicAdd(&a.hi[v0 + li], hinc[c]);
+                  atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+                }
+            }
+          } else {
+            // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
+            // word is read as a signed int32, so a running sum that hovers
+            // around zero never wraps; only signed overflow of the low word
+            // (|partial| >= 2^31 units) carries +-1 into the global high word.
+            // w*x is exact in fp64; F keeps |w x| 2^F <= 2^30 (R19).
+            uint32_t tlo[P], old[P];
+            int32_t thi[P];
+#pragma unroll
+            for (int c = 0; c < P; ++c) {
+              const double tv = W ? (double)val[c] * (double)w_s[cw * C::kSub + P * lane + c] : (double)val[c];
+              const long long T = __double2ll_rn(tv * sp_scale);
+              tlo[c] = (uint32_t)T;
+              thi[c] = (int32_t)(T >> 32) + ((int32_t)tlo[c] < 0 ? 1 : 0);   // T = thi*2^32 + (int32)tlo
+            }
+#pragma unroll
+            for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+            uint32_t any = 0;
+            int32_t hinc[P];
+#pragma unroll
+            for (int c = 0; c < P; ++c) {
+              const uint32_t nw = old[c] + tlo[c];
+              const bool ovf = (int32_t)((old[c] ^ nw) & (tlo[c] ^ nw)) < 0;
+              hinc[c] = ok[c] ? thi[c] + (ovf ? ((int32_t)old[c] < 0 ? -1 : 1) : 0) : 0;
+              any |= (uint32_t)hinc[c];
+            }
+            if (any) {
+#pragma unroll
+              for (int c = 0; c < P; ++c)
+                if (hinc[c]) {
+                  const uint32_t li = id[c] & qmask;
+                  atomicAdd(&a.hi[v0 + li], (uint32_t)hinc[c]);
+                  atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+                }
             }
           }
-        } else {
-          // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
-          // word is read as a signed int32, so a running sum that hovers
-          // around zero never wraps; only signed overflow of the low word
-          // (|partial| >= 2^31 units) carries +-1 into the global high word.
-          // w*x is exact in fp64; F keeps |w x| 2^F < 2^31 (R19).
-          uint32_t tlo[kSteps], old[kSteps];
-          int32_t thi[kSteps];
-#pragma unroll
-          for (int k = 0; k < kSteps; ++k) {
-            const double tv = W ? (double)val[k] * (double)w_s[cw * kChunkIds + k * 32 + lane] : (double)val[k];
-            const long long T = __double2ll_rn(tv * sp_scale);
-            tlo[k] = (uint32_t)T;
-            thi[k] = (int32_t)(T >> 32) + ((int32_t)tlo[k] < 0 ? 1 : 0);   // T = thi*2^32 + (int32)tlo
-          }
-#pragma unroll
-          for (int k = 0; k < kSteps; ++k) old[k] = ok[k] ? atomicAdd(&acc[id[k] & qmask], tlo[k]) : 0u;
-#pragma unroll
-          for (int k = 0; k < kSteps; ++k) {
-            const uint32_t nw = old[k] + tlo[k];
-            const bool ovf = (int32_t)((old[k] ^ nw) & (tlo[k] ^ nw)) < 0;
-            const int32_t hinc = thi[k] + (ovf ? ((int32_t)old[k] < 0 ? -1 : 1) : 0);
-            if (ok[k] && hinc != 0) {
-              const uint32_t li = id[k] & qmask;
-              atomicAdd(&a.hi[v0 + li], (uint32_t)hinc);
-              atomicOr(&bitmap[li >> 5], 1u << (li & 31));
-            }
-          }
-        }
+        };
+        if (whole) body(std::true_type{});
+        else body(std::false_type{});
       }
     }
     __syncwarp();
@@ -297,27 +369,27 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
         run_apply = *flag_s != 0u;
         if (run_apply) __threadfence();
       }
+      // exact 64-bit total of local vertex i; resets the state it reads
+      auto total = [&](int64_t i) -> uint64_t {
+        const uint32_t v = v0 + (uint32_t)i;
+        uint64_t tot;
+        if (nsl > 1) {
+          tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
+          a.part[v] = 0ull;
+          a.hi[v] = 0u;
+        } else {
+          tot = PR ? (uint64_t)acc[i] : (uint64_t)(long long)(int32_t)acc[i];
+          if ((bitmap[i >> 10] >> ((i >> 5) & 31)) & 1u) {
+            tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+            a.hi[v] = 0u;
+          }
+          acc[i] = 0u;
+        }
+        return tot;
+      };
       double dang = 0.0, res = 0.0;
       if (run_apply) {
         if constexpr (PR) {
-          // total of local vertex i (exact u64 fixed point); resets the state it reads
-          auto total = [&](int64_t i) -> uint64_t {
-            const uint32_t v = v0 + (uint32_t)i;
-            uint64_t tot;
-            if (nsl > 1) {
-              tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
-              a.part[v] = 0ull;
-              a.hi[v] = 0u;
-            } else {
-              tot = acc[i];
-              if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
-                tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
-                a.hi[v] = 0u;
-              }
-              acc[i] = 0u;
-            }
-            return tot;
-          };
           const bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
                            aligned16(a.spr_new + v0) && aligned16(a.outdeg + v0);
           if (vec) {
@@ -355,23 +427,8 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
             }
           }
         } else {
-          for (int64_t i = ctid; i < cnt; i += kCons) {
-            const uint32_t v = v0 + (uint32_t)i;
-            long long tot;
-            if (nsl > 1) {
-              tot = (long long)ldcg_u64(&a.part[v]) + (long long)((uint64_t)ldcg_u32(&a.hi[v]) << 32);
-              a.part[v] = 0ull;
-              a.hi[v] = 0u;
-            } else {
-              tot = (long long)(int32_t)acc[i];
-              if ((bitmap[i >> 5] >> (i & 31)) & 1u) {
-                tot += (long long)((uint64_t)ldcg_u32(&a.hi[v]) << 32);
-                a.hi[v] = 0u;
-              }
-              acc[i] = 0u;
-            }
-            a.y[v] = (float)((double)tot * sp_inv);
-          }
+          for (int64_t i = ctid; i < cnt; i += kCons)
+            a.y[v0 + (uint32_t)i] = (float)((double)(long long)total(i) * sp_inv);
         }
       }
       for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
@@ -437,30 +494,45 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   }
 }
 
-}  // namespace
-
-int gather_smem_bytes(int b, bool weighted) {
+template <typename IdT, bool W>
+int smem_bytes_for(int b) {
+  using C = Cfg<IdT, W>;
   const int64_t q = int64_t(1) << b;
-  const int bm_words = (int)((q + 31) / 32) < 4 ? 4 : (int)((q + 31) / 32);
+  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
-  const int stages = weighted ? Cfg<true>::kStages : Cfg<false>::kStages;
-  const int sbytes = weighted ? Cfg<true>::kStageBytes : Cfg<false>::kStageBytes;
-  return (int)(head + stages * sbytes + stages * sizeof(StageMeta) + 2 * stages * 8 + 2 * kConsumerWarps * 8 + 16);
+  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
+               2 * kConsumerWarps * 8 + 16);
 }
 
 using GatherFn = void (*)(const GatherArgs);
 
-GatherFn gather_fn(bool weighted, bool pagerank) {
-  return weighted ? (pagerank ? k_gather<true, true> : k_gather<true, false>)
-                  : (pagerank ? k_gather<false, true> : k_gather<false, false>);
+GatherFn gather_fn(bool wide, bool weighted, bool pagerank) {
+  if (wide)
+    return weighted ? (pagerank ? k_gather<uint32_t, true, true> : k_gather<uint32_t, true, false>)
+                    : (pagerank ? k_gather<uint32_t, false, true> : k_gather<uint32_t, false, false>);
+  return weighted ? (pagerank ? k_gather<uint16_t, true, true> : k_gather<uint16_t, true, false>)
+                  : (pagerank ? k_gather<uint16_t, false, true> : k_gather<uint16_t, false, false>);
+}
+
+}  // namespace
+
+int gather_smem_bytes(int b, bool wide, bool weighted) {
+  if (wide) return weighted ? smem_bytes_for<uint32_t, true>(b) : smem_bytes_for<uint32_t, false>(b);
+  return weighted ? smem_bytes_for<uint16_t, true>(b) : smem_bytes_for<uint16_t, false>(b);
 }
 
 int prepare_gather(pcpm_handle* h) {
   int maxsm = 0;
   PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-  for (int w = 0; w < 2; ++w)
-    for (int p = 0; p < 2; ++p)
-      PCPM_CK(cudaFuncSetAttribute(gather_fn(w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  for (int wd = 0; wd < 2; ++wd)
+    for (int w = 0; w < 2; ++w)
+      for (int p = 0; p < 2; ++p) {
+        if (gather_smem_bytes(kMaxBits, wd, w) > maxsm) {
+          set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit");
+          return PCPM_ECUDA;
+        }
+        PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+      }
   return PCPM_OK;
 }
 
@@ -474,9 +546,9 @@ int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStr
 }
 
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s) {
-  const int smem = gather_smem_bytes(a.b, weighted);
+  const int smem = gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
-  gather_fn(weighted, pagerank)<<<grid, kGatherThreads, smem, s>>>(a);
+  gather_fn(h->wide, weighted, pagerank)<<<grid, kGatherThreads, smem, s>>>(a);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return PCPM_OK;

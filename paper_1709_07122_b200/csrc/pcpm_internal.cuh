@@ -15,17 +15,18 @@
 namespace pcpm {
 
 // ---------------------------------------------------------------- constants
-// Gather tile: kTileIds destination IDs (8 KB) per pipeline stage, decoded by
-// kConsumerWarps warps, each owning one kChunkIds-ID sub-chunk whose update
-// index base comes from chunk_base (the global decode identity).
+// Gather tile: kTileIds destination IDs per pipeline stage (the compact
+// PageRank kernel uses 2x that), decoded by kConsumerWarps warps, each owning
+// one sub-chunk whose update-index base comes from chunk_base (the global
+// decode identity).  Bin slices are cut at kTileAlign multiples.
 constexpr int kTileIds = 2048;
-constexpr int kChunkIds = 128;
-constexpr int kChunksPerTile = kTileIds / kChunkIds;   // 16
-constexpr int kConsumerWarps = kChunksPerTile;         // one sub-chunk per warp
+constexpr int kTileAlign = 4096;
+constexpr int kChunkIds = 128;                         // chunk_base granularity
+constexpr int kConsumerWarps = 16;
 constexpr int kGatherThreads = 32 * (kConsumerWarps + 1);
-constexpr int kWinCap = kTileIds + 8;                  // update window (floats), 16 B aligned ends
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
 constexpr int kScatterThreads = 1024;
+constexpr int kScatterMaxGroups = 4096;                // j-range of one scatter item (smem offsets)
 
 struct GatherItem {        // one slice [x0, x1) of destination bin j
   uint32_t j, x0, x1;
@@ -64,9 +65,12 @@ struct pcpm_handle {
   std::vector<void*> allocs;
 
   // layout (device)
-  uint32_t* ids = nullptr;          // [m_pad]
+  bool wide = false;                // iterate on the 4-byte arrays (PCPM_WIDE_IDS)
+  uint32_t* ids = nullptr;          // [m_pad] 4-byte IDs (wide handles only)
+  uint16_t* ids16 = nullptr;        // [m_pad] compact IDs: local | flag << 15
   float* w = nullptr;               // [m_pad] or null
-  uint32_t* png_src = nullptr;      // [E' (+pad)]
+  uint32_t* png_src = nullptr;      // [E' (+pad)] 4-byte PNG sources (wide handles only)
+  uint16_t* png16 = nullptr;        // [E' (+pad)] compact PNG sources: u & (q-1)
   uint32_t* png_off = nullptr;      // [k_src*(k_dst+1)]
   uint32_t* upd_off = nullptr;      // [k_src*k_dst]
   uint32_t* bin_id_start = nullptr; // [k_dst+1]
@@ -193,7 +197,7 @@ __device__ __forceinline__ uint32_t lanemask_le() {
 
 // ---------------------------------------------------------------- launchers
 struct GatherArgs {
-  const uint32_t* ids;
+  const void* ids;         // uint16_t* (compact) or uint32_t* (wide)
   const float* w;
   const float* upd;
   const uint32_t* chunk_base;
@@ -224,7 +228,7 @@ struct GatherArgs {
 __device__ int spmv_fbits(float xmax, int wexp);
 int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s);
-int gather_smem_bytes(int b, bool weighted);
+int gather_smem_bytes(int b, bool wide, bool weighted);
 
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
 int prepare_gather(pcpm_handle* h);

@@ -25,6 +25,7 @@ PCPM_ESTATE = -6
 PCPM_NO_COMPRESS = 0x1
 PCPM_BUILD_PULL = 0x2
 PCPM_KEEP_VALUES = 0x4
+PCPM_WIDE_IDS = 0x8
 
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
@@ -60,7 +61,8 @@ class pcpm_layout_view(ctypes.Structure):
     _fields_ = [("ids", ctypes.c_void_p), ("w", ctypes.c_void_p), ("png_src", ctypes.c_void_p),
                 ("png_off", ctypes.c_void_p), ("upd_off", ctypes.c_void_p), ("bin_id_start", ctypes.c_void_p),
                 ("bin_upd_start", ctypes.c_void_p), ("chunk_base", ctypes.c_void_p),
-                ("out_degree", ctypes.c_void_p), ("upd", ctypes.c_void_p), ("chunk_ids", ctypes.c_int64)]
+                ("out_degree", ctypes.c_void_p), ("upd", ctypes.c_void_p), ("chunk_ids", ctypes.c_int64),
+                ("ids16", ctypes.c_void_p), ("png_src16", ctypes.c_void_p), ("wide", ctypes.c_int32)]
 
 
 def _load():

@@ -51,8 +51,10 @@ def export(p, h):
     m, ep, ks, kd = info.nnz, info.e_prime, info.k_src, info.k_dst
     out = dict(
         info=info,
-        ids=d2h(v.ids, m, np.uint32),
-        png_src=d2h(v.png_src, ep, np.uint32),
+        ids=d2h(v.ids, m, np.uint32) if v.ids else None,
+        png_src=d2h(v.png_src, ep, np.uint32) if v.png_src else None,
+        ids16=d2h(v.ids16, m, np.uint16),
+        png_src16=d2h(v.png_src16, ep, np.uint16),
         png_off=d2h(v.png_off, ks * (kd + 1), np.uint32).reshape(ks, kd + 1),
         upd_off=d2h(v.upd_off, ks * kd, np.uint32).reshape(ks, kd),
         bin_id_start=d2h(v.bin_id_start, kd + 1, np.uint32),
@@ -74,10 +76,16 @@ def assert_layout_equal(g, lay_gpu, b, compress=True):
         ids = None
     info = lay_gpu["info"]
     assert info.k_src == ref.k_src and info.k_dst == ref.k_dst
+    qmask = np.uint32((1 << b) - 1)
     if compress:
         assert info.e_prime == ref.e_prime
-        np.testing.assert_array_equal(lay_gpu["ids"], ids)
-        np.testing.assert_array_equal(lay_gpu["png_src"], ref.png_src)
+        if lay_gpu["ids"] is not None:                       # 4-byte layout (PCPM_WIDE_IDS)
+            np.testing.assert_array_equal(lay_gpu["ids"], ids)
+            np.testing.assert_array_equal(lay_gpu["png_src"], ref.png_src)
+        # compact layout = the same bins re-encoded: (v & (q-1)) | flag << 15, u & (q-1)
+        want16 = ((ids & qmask) | ((ids >> np.uint32(31)) << np.uint32(15))).astype(np.uint16)
+        np.testing.assert_array_equal(lay_gpu["ids16"], want16)
+        np.testing.assert_array_equal(lay_gpu["png_src16"], (ref.png_src & qmask).astype(np.uint16))
         np.testing.assert_array_equal(lay_gpu["png_off"], ref.png_off.astype(np.uint32))
         np.testing.assert_array_equal(lay_gpu["upd_off"], ref.upd_off.astype(np.uint32))
         np.testing.assert_array_equal(lay_gpu["bin_upd_start"], ref.bin_upd_start.astype(np.uint32))
@@ -85,7 +93,7 @@ def assert_layout_equal(g, lay_gpu, b, compress=True):
     if g.values is not None:
         np.testing.assert_array_equal(lay_gpu["w"], ref.w)
     # decode anchors by their plain definition: #flags in ids[0 .. 128 c)
-    flags = (lay_gpu["ids"] >> 31).astype(np.int64)
+    flags = (lay_gpu["ids16"] >> 15).astype(np.int64)
     cum = np.concatenate([[0], np.cumsum(flags)])
     cb = lay_gpu["chunk_base"]
     for c in range(len(cb)):
@@ -149,13 +157,31 @@ def test_layout_from_host_pointers_and_weights(pcpm):
 
 def test_layout_uncompressed(pcpm):
     g = graphs.make_graph("rmat", 3, scale=11, permute=True)
-    h = build(pcpm, g, 6, flags=pcpm.PCPM_NO_COMPRESS)
+    h = build(pcpm, g, 6, flags=pcpm.PCPM_NO_COMPRESS | pcpm.PCPM_WIDE_IDS)
     try:
         lay = export(pcpm, h)
         assert lay["info"].e_prime == g.m and lay["info"].compressed == 0
         ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, 6)
         np.testing.assert_array_equal(lay["ids"], ref.ids | np.uint32(0x80000000))
+        np.testing.assert_array_equal(lay["ids16"] >> 15, np.ones(g.m, np.uint16))
         np.testing.assert_array_equal(lay["bin_id_start"], ref.bin_id_start.astype(np.uint32))
+        # the uncompressed layout computes the same PageRank (every ID carries its own update)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 10, out)
+        pr_check(out.cpu().numpy(), oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 10), "nocompress")
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+@pytest.mark.parametrize("name,mk,b", [LAYOUT_CASES[i] for i in (1, 3, 6, 7, 9)],
+                         ids=[LAYOUT_CASES[i][0] for i in (1, 3, 6, 7, 9)])
+def test_layout_bit_exact_wide(pcpm, name, mk, b):
+    g = mk()
+    h = build(pcpm, g, b, flags=pcpm.PCPM_WIDE_IDS)
+    try:
+        lay = export(pcpm, h)
+        assert lay["view"].wide == 1 and lay["ids"] is not None
+        assert_layout_equal(g, lay, b)
     finally:
         pcpm.pcpm_destroy(h)
 
@@ -214,10 +240,11 @@ PR_CASES = [
 ]
 
 
+@pytest.mark.parametrize("wide", [False, True], ids=["compact", "wide"])
 @pytest.mark.parametrize("name,mk,b,iters", PR_CASES, ids=[c[0] for c in PR_CASES])
-def test_pagerank_parity(pcpm, name, mk, b, iters):
+def test_pagerank_parity(pcpm, name, mk, b, iters, wide):
     g = mk()
-    h = build(pcpm, g, b, flags=pcpm.PCPM_BUILD_PULL)
+    h = build(pcpm, g, b, flags=pcpm.PCPM_BUILD_PULL | (pcpm.PCPM_WIDE_IDS if wide else 0))
     try:
         ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, iters)
         out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
@@ -293,10 +320,11 @@ SPMV_CASES = [
 ]
 
 
+@pytest.mark.parametrize("wide", [False, True], ids=["compact", "wide"])
 @pytest.mark.parametrize("name,mk,b", SPMV_CASES, ids=[c[0] for c in SPMV_CASES])
-def test_spmv_parity(pcpm, name, mk, b):
+def test_spmv_parity(pcpm, name, mk, b, wide):
     g = mk()
-    h = build(pcpm, g, b)
+    h = build(pcpm, g, b, flags=pcpm.PCPM_WIDE_IDS if wide else 0)
     try:
         x = graphs.make_x(g.n_src, 5)
         y = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
