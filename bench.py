@@ -204,6 +204,7 @@ def run_pcpm(args, world, rank, local):
     barrier(world)
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
+    info = pcpm.pcpm_get_info(h)          # F of the calls just timed
     launches = pcpm.pcpm_last_launch_count(h) * (iters if op != "pagerank" else 1) * args.steps
     ms_max = max_over_ranks(ms, world)
     ms_per_step = ms_max / args.steps
