@@ -36,6 +36,8 @@ WORKLOADS = {
     "c2": "c2_er20: Erdos-Renyi 2^20 vertices 2^24 raw edges seed2, q=2^15, d=0.85, 20 iterations",
     "c3": "c3_rmat24: RMAT scale 24 ef16 seed3 random labels, q=2^15, d=0.85, 20 iterations",
     "c4": "c4_rmat26: RMAT scale 26 ef16 seed4 random labels, q=2^15, d=0.85, 20 iterations",
+    "c4bfs": "c4_rmat26_bfs: c4's graph relabelled in BFS order from the highest-out-degree vertex (R16), "
+             "q=2^15, d=0.85, 20 iterations",
     "c5": "c5_spmv_rmat25: y=A.x, RMAT scale 25 ef16 seed5 random labels, values/x U[-1,1), q=2^15, 50 multiplies",
 }
 

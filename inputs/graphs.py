@@ -211,6 +211,9 @@ CONFIGS = {
                probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=20, op="pagerank"),
     "c4": dict(name="c4_rmat26", kind="rmat", scale=26, edge_factor=16, seed=4,
                probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=20, op="pagerank"),
+    # configs[3] run twice: C4's graph relabelled by BFS order (reading R16)
+    "c4bfs": dict(name="c4_rmat26_bfs", kind="rmat", scale=26, edge_factor=16, seed=4,
+                  probs=(0.57, 0.19, 0.19), permute=True, bfs=True, bits=15, iters=20, op="pagerank"),
     "c5": dict(name="c5_spmv_rmat25", kind="rmat", scale=25, edge_factor=16, seed=5,
                probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=50, op="spmv"),
 }
@@ -259,8 +262,60 @@ def make_x(n: int, seed: int, backend: str = "np", device=None):
     return unit_values_torch(seed, S_X, torch.arange(n, dtype=torch.int64, device=device))
 
 
+_BFS_LIB = None
+
+
+def _bfs_lib():
+    """inputs/bfs_order.c compiled with gcc on first use (input generation, not the method)."""
+    global _BFS_LIB
+    if _BFS_LIB is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, lib = os.path.join(here, "bfs_order.c"), os.path.join(here, "libinputs.so")
+        if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+            tmp = lib + f".tmp{os.getpid()}"
+            subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-o", tmp, src])
+            os.replace(tmp, lib)
+        _BFS_LIB = ctypes.CDLL(lib)
+        P = ctypes.c_void_p
+        _BFS_LIB.inputs_bfs_order.argtypes = [ctypes.c_int64, P, P, P]
+        _BFS_LIB.inputs_bfs_order.restype = ctypes.c_int
+    return _BFS_LIB
+
+
+def bfs_order(n: int, row_ptr: np.ndarray, col: np.ndarray) -> np.ndarray:
+    """new_id[v] for the BFS locality labelling of reading R16 (host, O(n + m))."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    cl = np.ascontiguousarray(col, dtype=np.uint32)
+    out = np.empty(n, dtype=np.int64)
+    rc = _bfs_lib().inputs_bfs_order(n, rp.ctypes.data, cl.ctypes.data, out.ctypes.data)
+    if rc != 0:
+        raise MemoryError("bfs_order")
+    return out
+
+
+def relabel(g: GraphCSR, new_id, name: str = "") -> GraphCSR:
+    """CSR of the same graph with vertex v renamed new_id[v] (rows re-sorted)."""
+    n = g.n_src
+    if g.backend == "np":
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(g.row_ptr))
+        keys = (new_id[rows] << 32) | new_id[g.col.astype(np.int64)]
+        del rows
+    else:
+        import torch
+        nid = torch.as_tensor(new_id, device=g.row_ptr.device)
+        rows = torch.repeat_interleave(torch.arange(n, dtype=torch.int64, device=nid.device),
+                                       g.row_ptr[1:] - g.row_ptr[:-1])
+        keys = (nid[rows] << 32) | nid[g.col.to(torch.int64) & 0xFFFFFFFF]
+        del rows, nid
+    row_ptr, col, _ = edges_to_csr(keys, n, n, g.backend)
+    return GraphCSR(name or g.name, n, n, row_ptr, col, None, dict(g.meta))
+
+
 def make_config(key: str, backend: str = "np", device=None) -> GraphCSR:
-    """Build BASELINE.json config ``key`` ('c1'..'c5')."""
+    """Build BASELINE.json config ``key`` ('c1'..'c5', 'c4bfs')."""
     cfg = CONFIGS[key]
     if cfg["kind"] == "rmat":
         g = make_graph("rmat", cfg["seed"], scale=cfg["scale"], edge_factor=cfg["edge_factor"],
@@ -269,5 +324,10 @@ def make_config(key: str, backend: str = "np", device=None) -> GraphCSR:
     else:
         g = make_graph("er", cfg["seed"], n=cfg["n"], m_raw=cfg["m_raw"], permute=cfg["permute"],
                        backend=backend, device=device, name=cfg["name"])
+    if cfg.get("bfs"):
+        h = g.to_numpy()
+        new_id = bfs_order(g.n_src, h.row_ptr, h.col)
+        del h
+        g = relabel(g, new_id, cfg["name"])
     g.meta.update(cfg)
     return g

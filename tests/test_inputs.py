@@ -46,3 +46,58 @@ def test_values_exact_in_unit_interval():
     v = graphs.make_x(100000, 5)
     assert v.dtype == np.float32 and v.min() >= -1 and v.max() < 1
     assert abs(float(v.mean())) < 0.01
+
+
+def _bfs_python(n, row_ptr, col):
+    """Reading R16 written out with Python lists (small graphs only)."""
+    deg = [int(row_ptr[u + 1] - row_ptr[u]) for u in range(n)]
+    order = sorted(range(n), key=lambda u: (-deg[u], u))
+    new = [-1] * n
+    nxt = 0
+    for s in order:
+        if new[s] >= 0:
+            continue
+        new[s] = nxt
+        nxt += 1
+        q = [s]
+        while q:
+            u = q.pop(0)
+            for v in col[row_ptr[u]:row_ptr[u + 1]]:
+                if new[v] < 0:
+                    new[v] = nxt
+                    nxt += 1
+                    q.append(int(v))
+    return new
+
+
+def test_bfs_order_matches_python_bfs_and_relabels_isomorphically():
+    import numpy as np
+    from inputs import graphs
+    for seed, scale in ((1, 8), (2, 10)):
+        g = graphs.make_graph("rmat", seed, scale=scale, permute=True)
+        nid = graphs.bfs_order(g.n_src, g.row_ptr, g.col)
+        assert nid.tolist() == _bfs_python(g.n_src, g.row_ptr, g.col)
+        assert sorted(nid.tolist()) == list(range(g.n_src))
+        h = graphs.relabel(g, nid)
+        assert h.m == g.m
+        rows = np.repeat(np.arange(g.n_src), np.diff(g.row_ptr))
+        old = set(zip(nid[rows].tolist(), nid[g.col.astype(np.int64)].tolist()))
+        rows2 = np.repeat(np.arange(h.n_src), np.diff(h.row_ptr))
+        assert old == set(zip(rows2.tolist(), h.col.astype(np.int64).tolist()))
+    # the start vertex (max out-degree) gets label 0
+    deg = np.diff(g.row_ptr)
+    assert nid[int(np.argmax(deg))] == 0
+
+
+def test_relabel_torch_equals_numpy():
+    import numpy as np
+    import torch
+    from inputs import graphs
+    g = graphs.make_graph("rmat", 3, scale=9, permute=True)
+    nid = graphs.bfs_order(g.n_src, g.row_ptr, g.col)
+    a = graphs.relabel(g, nid)
+    gt = graphs.GraphCSR("t", g.n_src, g.n_dst, torch.from_numpy(g.row_ptr),
+                         torch.from_numpy(g.col.view(np.int32)), None, {})
+    b = graphs.relabel(gt, torch.from_numpy(nid)).to_numpy()
+    np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
+    np.testing.assert_array_equal(a.col, b.col)
