@@ -172,6 +172,9 @@ def run_pcpm(args, world, rank, local):
     info = pcpm.pcpm_get_info(h)
     m, n = info.nnz, info.n_src
     pcpm.pcpm_set_option(h, "phase_timing", 1)
+    for kv in args.opt:                   # kernel-variant A/B experiments
+        k, v = kv.split("=")
+        pcpm.pcpm_set_option(h, k, int(v))
     out = torch.zeros(max(g.n_src, g.n_dst), dtype=torch.float32, device=dev)
 
     if op == "pagerank":
@@ -268,6 +271,7 @@ def run_pcpm(args, world, rank, local):
             "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
             "paper_eq4_bvgas": round(model.bvgas_comm(n, m)),
         },
+        "options": args.opt,
         "clocks": clk,
         "gpu_launches": int(launches),
     }
@@ -464,6 +468,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--opt", action="append", default=[], help="pcpm_set_option key=value (A/B experiments)")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)

@@ -107,6 +107,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.n_dst = h->n_dst;
   a.fbits = fbits;
   a.outdeg = h->outdeg;
+  a.epi_pf = h->opt_epi_pf;
   return a;
 }
 
@@ -492,6 +493,29 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
   }
   if (!strcmp(key, "use_graph")) {
     h->opt_use_graph = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "scatter_variant")) {
+    if (value < 0 || value > 1) {
+      set_error(PCPM_EINVAL, "scatter_variant must be 0 (TMA stream) or 1 (warp per group)");
+      return PCPM_EINVAL;
+    }
+    h->opt_scatter_variant = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "scatter_prefetch")) {
+    if (value < 0 || value > 64) {
+      set_error(PCPM_EINVAL, "scatter_prefetch must be in [0, 64]");
+      return PCPM_EINVAL;
+    }
+    h->opt_scatter_pf = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "epilogue_prefetch")) {
+    h->opt_epi_pf = value ? 1 : 0;
     free_graph(h);
     return PCPM_OK;
   }

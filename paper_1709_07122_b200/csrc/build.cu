@@ -304,8 +304,8 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->ids16, h->m_pad))) return rc;
   TK(cudaMemsetAsync(h->ids16, 0, sizeof(uint16_t) * h->m_pad, s));
   if (h->weighted && (rc = dev_alloc_t(h, &h->w, h->m_pad))) return rc;
-  if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1)))) return rc;
-  if ((rc = dev_alloc_t(h, &h->upd_off, k_src * k_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1) + 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->upd_off, k_src * k_dst + 4))) return rc;
   if ((rc = dev_alloc_t(h, &h->bin_id_start, k_dst + 1))) return rc;
   if ((rc = dev_alloc_t(h, &h->bin_upd_start, k_dst + 1))) return rc;
   const int64_t nchunks = h->m_pad / kChunkIds;

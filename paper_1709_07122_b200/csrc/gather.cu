@@ -153,57 +153,103 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   __syncthreads();
 
   if (warp == 0) {
-    // ================= producer =================
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (;;) {
-        const uint32_t it = atomicAdd(&a.counters[0], 1u);
-        const bool stop = it >= (uint32_t)a.n_items;
-        GatherItem item;
-        if (!stop) item = a.items[it];
-        if (stop || item.x0 == item.x1) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          StageMeta m{};
-          m.item = stop ? -1 : (int)it;
-          m.j = stop ? 0u : item.j;
-          m.flags = stop ? kFlagStop : (kFlagLast | kFlagEmpty);
-          meta[stage] = m;
-          mbar_arrive(&full[stage]);
-          if (++stage == S) { stage = 0; phase ^= 1; }
-          if (stop) break;
-          continue;
+    // ================= producer (whole warp; lane 0 issues) =================
+    // The window of tile t is fixed by two decode anchors (chunk_base at the
+    // tile's ends).  Lanes load the anchors of 32 tiles at once, so the issue
+    // loop carries no dependent global load per tile.
+    const uint64_t pol = policy_evict_first();
+    int stage = 0;
+    uint32_t phase = 0;
+    auto claim = [&]() -> uint32_t {
+      uint32_t v = 0;
+      if (lane == 0) v = atomicAdd(&a.counters[0], 1u);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    auto push_meta = [&](const StageMeta& m) {      // a stage without data (empty item / stop)
+      if (lane == 0) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        meta[stage] = m;
+        mbar_arrive(&full[stage]);
+      }
+      __syncwarp();
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    };
+    uint32_t it = claim();
+    GatherItem item{};
+    if (it < (uint32_t)a.n_items) item = a.items[it];
+    for (;;) {
+      if (it >= (uint32_t)a.n_items) {
+        StageMeta m{};
+        m.item = -1;
+        m.flags = kFlagStop;
+        push_meta(m);
+        break;
+      }
+      // claim the next item now so its descriptor load overlaps this item's issue loop
+      const uint32_t it_next = claim();
+      GatherItem item_next{};
+      if (it_next < (uint32_t)a.n_items) item_next = a.items[it_next];
+      if (item.x0 == item.x1) {
+        StageMeta m{};
+        m.item = (int)it;
+        m.j = item.j;
+        m.flags = kFlagLast | kFlagEmpty;
+        push_meta(m);
+      } else {
+        if constexpr (PR) {
+          if (a.epi_pf && lane == 0) {   // the apply's vertex arrays of partition j, L2-resident by the epilogue
+            const int64_t v0 = (int64_t)item.j << a.b;
+            const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
+            if (vb) {
+              bulk_prefetch_l2(a.outdeg + v0, vb);
+              bulk_prefetch_l2(a.pr_old + v0, vb);
+            }
+          }
         }
         const uint32_t t0 = item.x0 / C::kTile, t1 = (item.x1 - 1) / C::kTile;
-        for (uint32_t t = t0; t <= t1; ++t) {
-          const uint32_t tb = t * C::kTile;
-          const uint32_t lo = max(tb, item.x0), hi = min(tb + C::kTile, item.x1);
-          const uint32_t flo = (lo == item.x0) ? item.fx0 : __ldg(a.chunk_base + lo / kChunkIds);
-          const uint32_t fhi = (hi == item.x1) ? item.fx1 : __ldg(a.chunk_base + hi / kChunkIds);
-          const uint32_t wlo = flo > 0 ? flo - 1 : 0;
-          const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
-          mbar_wait(&empty[stage], phase ^ 1);
-          StageMeta m{};
-          m.item = (int)it;
-          m.j = item.j;
-          m.lo = lo;
-          m.hi = hi;
-          m.tile_base = tb;
-          m.win_base = alo;
-          m.flags = (t == t1) ? kFlagLast : 0u;
-          meta[stage] = m;
-          uint8_t* sb = stage_base + stage * C::kStageBytes;
-          const uint32_t win_bytes = (ahi - alo) * 4;
-          mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
-          bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
-          bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
-          bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
-                   &full[stage], pol);
-          if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
-          if (++stage == S) { stage = 0; phase ^= 1; }
+        for (uint32_t tb0 = t0; tb0 <= t1; tb0 += 32) {
+          const uint32_t tl = tb0 + lane;
+          uint32_t fa = 0, fb = 0;                 // #flags before the tile's first / after its last ID
+          if (tl <= t1) {
+            const uint32_t tb = tl * C::kTile;
+            fa = (tl == t0) ? item.fx0 : __ldg(a.chunk_base + tb / kChunkIds);
+            fb = (tl == t1) ? item.fx1 : __ldg(a.chunk_base + (tb + C::kTile) / kChunkIds);
+          }
+          const uint32_t nb = min(32u, t1 - tb0 + 1);
+          for (uint32_t k = 0; k < nb; ++k) {
+            const uint32_t flo = __shfl_sync(0xffffffffu, fa, k);
+            const uint32_t fhi = __shfl_sync(0xffffffffu, fb, k);
+            if (lane == 0) {
+              const uint32_t t = tb0 + k;
+              const uint32_t tb = t * C::kTile;
+              const uint32_t wlo = flo > 0 ? flo - 1 : 0;   // the first ID may continue the previous run
+              const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
+              mbar_wait(&empty[stage], phase ^ 1);
+              StageMeta m{};
+              m.item = (int)it;
+              m.j = item.j;
+              m.lo = max(tb, item.x0);
+              m.hi = min(tb + C::kTile, item.x1);
+              m.tile_base = tb;
+              m.win_base = alo;
+              m.flags = (t == t1) ? kFlagLast : 0u;
+              meta[stage] = m;
+              uint8_t* sb = stage_base + stage * C::kStageBytes;
+              const uint32_t win_bytes = (ahi - alo) * 4;
+              mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
+              bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
+              bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
+              bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
+                       &full[stage], pol);
+              if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
+            }
+            __syncwarp();
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
         }
       }
+      it = it_next;
+      item = item_next;
     }
     return;
   }

@@ -26,7 +26,7 @@ constexpr int kConsumerWarps = 16;
 constexpr int kGatherThreads = 32 * (kConsumerWarps + 1);
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
 constexpr int kScatterThreads = 1024;
-constexpr int kScatterMaxGroups = 4096;                // j-range of one scatter item (smem offsets)
+constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
 
 struct GatherItem {        // one slice [x0, x1) of destination bin j
   uint32_t j, x0, x1;
@@ -109,6 +109,10 @@ struct pcpm_handle {
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
+  int opt_gather_pf = 8;            // gather: tiles prefetched into L2 ahead of the smem ring
+  int opt_epi_pf = 0;
+  int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
+  int opt_scatter_pf = 4;           // scatter: PNG stages prefetched into L2 ahead of the ring               // gather: prefetch the apply's vertex arrays into L2 at item claim
   int opt_phase_timing = 0;
   std::vector<cudaEvent_t> events;  // phase-timing events (created on demand)
   int n_events_used = 0;
@@ -176,6 +180,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// bulk prefetch of [src, src + bytes) into L2 (TMA engine; no smem, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -224,6 +232,7 @@ struct GatherArgs {
   float* y;
   const float* xmax;       // device max|x| of this call (fixed-point scale)
   int wexp;                // max|w| <= 2^wexp
+  int epi_pf;              // prefetch outdeg / pr_old of the item's partition into L2
 };
 __device__ int spmv_fbits(float xmax, int wexp);
 int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);

@@ -2,29 +2,263 @@
 //
 //   for p in P:  for p' in P:  for u in N_i^p(p'):  insert SPR[u] into update_bins[p']
 //
-// One CTA per work item (source partition p, destination groups [j0, j1)).
-// The CTA stages the partition's source values x[p q .. p q + q) in shared
-// memory (coalesced 128-bit loads; 128 KB at q = 2^15 -- the "cache the vertex
-// data of p" of P:137) together with the item's rows of png_off / upd_off.
-// Warps then claim whole (p, j) groups dynamically and stream them: coalesced
-// reads of the PNG sources (2-byte partition-local in the compact layout),
-// random reads of the staged slice, and coalesced writes to the group's
-// disjoint range upd[upd_off[p][j] ...] (fixed, disjoint write
-// locations -- no atomics).  Eight independent loads per lane are kept in
-// flight.  A pure copy: the update bins are bit-identical to the oracle's
-// scatter for the same x.
+// Work items are (source partition p, destination groups [j0, j1)); their PNG
+// entries png[png_off[p][j0] .. png_off[p][j1]) are contiguous (groups are
+// stored in (p, j) order), and group (p, j) writes the disjoint range
+// upd[upd_off[p][j] ...] (fixed, disjoint write locations -- no atomics).
+// A pure copy: the update bins are bit-identical to the oracle's scatter for
+// the same x.
+//
+// k_scatter_tma (default):
+//  * Persistent CTAs claim items (largest first) from an atomic counter.
+//  * Warp 0 is a TMA producer.  Per item it bulk-copies the partition's source
+//    values x[p q .. p q + q) (128 KB at q = 2^15 -- "cache the vertex data of
+//    p") and the item's rows of png_off / upd_off into shared memory,
+//    then streams the item's PNG entries through a 3-stage ring of 16 KB
+//    bulk copies, with an L2 prefetch running further ahead.
+//  * 16 consumer warps take 512-entry sub-ranges of each stage.  Lane l
+//    handles entries e = base + l + 32 i: consecutive lanes read consecutive
+//    PNG entries from smem and write consecutive update slots of the group
+//    containing e (dst = upd_off[g] + e - png_off[g]), so global stores are
+//    coalesced; the group index is advanced per lane as e crosses group
+//    boundaries.
+//
+// k_scatter_warp (option "scatter_variant" = 1, the round-1 design kept for
+// A/B): warps claim whole groups and read the PNG straight from global memory.
 #include "pcpm_internal.cuh"
 
 namespace pcpm {
 namespace {
 
+// ------------------------------------------------------------------ TMA variant
+constexpr int kScW = 16;                           // consumer warps
+constexpr int kScThreads = 32 * (kScW + 1);
+constexpr int kScStages = 3;
+constexpr int kScStageBytes = 16384;               // PNG bytes per stage
+constexpr int kScOffCap = kScatterMaxGroups + 8;   // offsets of one item (+ alignment slack)
+
+struct ScItemMeta {
+  uint32_t p, j0, ng;
+  uint32_t stop;
+  uint32_t off_shift;    // png_off row starts at off_s[off_shift]
+  uint32_t uo_shift;     // upd_off row starts at uo_s[uo_shift]
+  uint32_t pad[2];
+};
+struct ScStageMeta {
+  uint32_t base;         // PNG position of stage element 0 (16 B aligned)
+  uint32_t lo, hi;       // valid PNG positions [lo, hi)
+  uint32_t last;         // last stage of the item
+};
+
+struct ScatterArgs {
+  const ScatterItem* items;
+  int n_items;
+  const float* x;
+  int64_t n_src;
+  int b;
+  int64_t k_dst;
+  const void* png;
+  const uint32_t* png_off;
+  const uint32_t* upd_off;
+  float* upd;
+  uint32_t* counters;    // [2] item counter, [3] done counter (kept zero)
+  int pf_stages;         // L2 prefetch distance in stages
+};
+
+template <typename SrcT>
+__global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs a) {
+  constexpr int kChunk = kScStageBytes / (int)sizeof(SrcT);   // PNG entries per stage
+  constexpr int kSub = kChunk / kScW;                           // entries per consumer warp
+  constexpr uint32_t kAlignE = 16 / sizeof(SrcT);               // entries per 16 B
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t q = int64_t(1) << a.b;
+  float* xs = reinterpret_cast<float*>(smem);                                        // q floats
+  uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + ((q * 4 + 127) & ~int64_t(127)));
+  uint32_t* uo_s = off_s + kScOffCap;
+  uint8_t* ring = reinterpret_cast<uint8_t*>(uo_s + kScOffCap);
+  ScStageMeta* smeta = reinterpret_cast<ScStageMeta*>(ring + kScStages * kScStageBytes);
+  ScItemMeta* imeta = reinterpret_cast<ScItemMeta*>(smeta + kScStages);
+  uint64_t* full = reinterpret_cast<uint64_t*>(imeta + 1);
+  uint64_t* empty = full + kScStages;
+  uint64_t* ifull = empty + kScStages;
+  uint64_t* iempty = ifull + 1;
+  uint32_t* flag_s = reinterpret_cast<uint32_t*>(iempty + 1);
+  const SrcT* png = reinterpret_cast<const SrcT*>(a.png);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kScStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kScW);
+    }
+    mbar_init(ifull, 1);
+    mbar_init(iempty, kScW);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= producer =================
+    if (lane == 0) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0, iphase = 0;
+      for (;;) {
+        const uint32_t it = atomicAdd(&a.counters[2], 1u);
+        const bool stop = it >= (uint32_t)a.n_items;
+        ScatterItem item{};
+        uint32_t s0 = 0, s1 = 0;
+        if (!stop) {
+          item = a.items[it];
+          s0 = __ldg(a.png_off + (int64_t)item.p * (a.k_dst + 1) + item.j0);
+          s1 = __ldg(a.png_off + (int64_t)item.p * (a.k_dst + 1) + item.j1);
+          if (s0 == s1) continue;                                   // nothing to write
+          // warm L2 with the item's first stages and its source slice while the
+          // consumers finish the previous item
+          const int64_t xb = (int64_t)item.p << a.b;
+          const uint32_t xpb = (uint32_t)((min(q, a.n_src - xb) * 4) & ~int64_t(15));
+          if (xpb) bulk_prefetch_l2(a.x + xb, xpb);
+          const uint32_t ab = s0 & ~(kAlignE - 1);
+          for (int c = kScStages; c < kScStages + a.pf_stages; ++c) {
+            const uint32_t cb = ab + (uint32_t)c * kChunk;
+            if (cb >= s1) break;
+            bulk_prefetch_l2(png + cb, kScStageBytes);
+          }
+        }
+        uint32_t cb = 0;
+        // issue a stage of the item's PNG entries through the ring
+        auto issue = [&](uint32_t c) {
+          if (a.pf_stages) {
+            const uint32_t pb = c + (uint32_t)a.pf_stages * kChunk;
+            if (pb < s1) bulk_prefetch_l2(png + pb, kScStageBytes);
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          ScStageMeta sm;
+          sm.base = c;
+          sm.lo = max(c, s0);
+          sm.hi = min(c + (uint32_t)kChunk, s1);
+          sm.last = (c + (uint32_t)kChunk >= s1) ? 1u : 0u;
+          smeta[stage] = sm;
+          const uint32_t bytes = (((sm.hi - c) * (uint32_t)sizeof(SrcT)) + 15) & ~15u;   // png is padded
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(ring + stage * kScStageBytes, png + c, bytes, &full[stage], pol_stream);
+          if (++stage == kScStages) { stage = 0; phase ^= 1; }
+        };
+        if (!stop) {
+          // the first ring stages of this item do not depend on the source slice:
+          // issue them while the consumers finish the previous item
+          cb = s0 & ~(kAlignE - 1);
+          for (int c = 0; c < kScStages && cb < s1; ++c, cb += kChunk) issue(cb);
+        }
+        mbar_wait(iempty, iphase ^ 1);                              // consumers done with the last item
+        iphase ^= 1;
+        ScItemMeta im{};
+        if (stop) {
+          im.stop = 1;
+          *imeta = im;
+          mbar_arrive(ifull);
+          break;
+        }
+        const int64_t xbase = (int64_t)item.p << a.b;
+        const int64_t len = min(q, a.n_src - xbase);
+        const uint32_t xbytes = (uint32_t)(((len * 4) + 15) & ~int64_t(15));      // x is padded (launch_scatter)
+        const int64_t orow = (int64_t)item.p * (a.k_dst + 1) + item.j0;
+        const int64_t urow = (int64_t)item.p * a.k_dst + item.j0;
+        const uint32_t ng = item.j1 - item.j0;
+        const int64_t oal = orow & ~int64_t(3), ual = urow & ~int64_t(3);
+        const uint32_t obytes = (uint32_t)(((orow + ng + 1 - oal) * 4 + 15) & ~int64_t(15));   // offsets padded
+        const uint32_t ubytes = (uint32_t)(((urow + ng - ual) * 4 + 15) & ~int64_t(15));
+        im.p = item.p;
+        im.j0 = item.j0;
+        im.ng = ng;
+        im.off_shift = (uint32_t)(orow - oal);
+        im.uo_shift = (uint32_t)(urow - ual);
+        *imeta = im;
+        mbar_arrive_expect_tx(ifull, xbytes + obytes + ubytes);
+        bulk_g2s(xs, a.x + xbase, xbytes, ifull, pol_keep);
+        bulk_g2s(off_s, a.png_off + oal, obytes, ifull, pol_keep);
+        bulk_g2s(uo_s, a.upd_off + ual, ubytes, ifull, pol_keep);
+        for (; cb < s1; cb += kChunk) issue(cb);
+      }
+    }
+  } else {
+    // ================= consumers =================
+    const int cw = warp - 1;
+    int stage = 0;
+    uint32_t phase = 0, iphase = 0;
+    const uint32_t ubase_wide = 0;
+    (void)ubase_wide;
+    for (;;) {
+      mbar_wait(ifull, iphase);
+      iphase ^= 1;
+      const ScItemMeta im = *imeta;
+      if (im.stop) break;
+      const uint32_t* offs = off_s + im.off_shift;    // offs[g] = png_off[p][j0 + g], g in [0, ng]
+      const uint32_t* uos = uo_s + im.uo_shift;       // uos[g] = upd_off[p][j0 + g]
+      const uint32_t ubase = sizeof(SrcT) == 2 ? 0u : (im.p << a.b);   // wide sources are global IDs
+      for (;;) {
+        mbar_wait(&full[stage], phase);
+        const ScStageMeta sm = smeta[stage];
+        const SrcT* ps = reinterpret_cast<const SrcT*>(ring + stage * kScStageBytes);
+        const uint32_t wb = sm.base + (uint32_t)(cw * kSub);
+        const uint32_t wlo = max(wb, sm.lo), whi = min(wb + (uint32_t)kSub, sm.hi);
+        if (wlo < whi) {
+          // group of the warp's first entry: largest g with offs[g] <= wlo (broadcast search)
+          uint32_t lo = 0, hi = im.ng;                 // offs[lo] <= wlo < offs[hi]
+          while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (offs[mid] <= wlo) lo = mid; else hi = mid;
+          }
+          uint32_t g = lo;
+          uint32_t gend = offs[g + 1];
+#pragma unroll 4
+          for (uint32_t e = wlo + lane; e < whi; e += 32) {
+            while (e >= gend) {                          // cross (possibly empty) groups
+              ++g;
+              gend = offs[g + 1];
+            }
+            const uint32_t u = (uint32_t)ps[e - sm.base] - ubase;
+            a.upd[uos[g] + (e - offs[g])] = xs[u];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == kScStages) { stage = 0; phase ^= 1; }
+        if (sm.last) break;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(iempty);
+    }
+  }
+
+  // last CTA resets the work counters (graph replays start from zero)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t done = atomicAdd(&a.counters[3], 1u);
+    if (done == gridDim.x - 1) {
+      a.counters[2] = 0u;
+      a.counters[3] = 0u;
+    }
+  }
+  (void)flag_s;
+}
+
+int scatter_tma_smem_bytes(int b) {
+  const int64_t q = int64_t(1) << b;
+  return (int)(((q * 4 + 127) & ~int64_t(127)) + 2 * kScOffCap * 4 + kScStages * kScStageBytes +
+               kScStages * sizeof(ScStageMeta) + sizeof(ScItemMeta) + (2 * kScStages + 2) * 8 + 16);
+}
+
+// ------------------------------------------------------------------ warp-per-group variant
 constexpr int kUnroll = 8;
 
 template <typename SrcT>
 __global__ void __launch_bounds__(kScatterThreads, 1)
-k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __restrict__ x, int64_t n_src, int b,
-          int64_t k_dst, const SrcT* __restrict__ png, const uint32_t* __restrict__ png_off,
-          const uint32_t* __restrict__ upd_off, float* __restrict__ upd) {
+k_scatter_warp(const ScatterItem* __restrict__ items, int n_items, const float* __restrict__ x, int64_t n_src,
+               int b, int64_t k_dst, const SrcT* __restrict__ png, const uint32_t* __restrict__ png_off,
+               const uint32_t* __restrict__ upd_off, float* __restrict__ upd) {
   extern __shared__ float4 smem_f4[];
   __shared__ uint32_t next_group;
   const int64_t q = int64_t(1) << b;
@@ -37,7 +271,6 @@ k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __res
     const int64_t base = (int64_t)item.p << b;
     const int64_t len = min(q, n_src - base);
     const uint32_t ng = item.j1 - item.j0;
-    // stage x[base, base + len) -- 16 B vectors when aligned
     const float* src = x + base;
     if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
       const int64_t n4 = len >> 2;
@@ -55,7 +288,6 @@ k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __res
     __syncthreads();
     const uint32_t ubase = sizeof(SrcT) == 2 ? 0u : (uint32_t)base;   // compact sources are local
     for (;;) {
-      // groups (p, j) are claimed dynamically: their sizes vary by orders of magnitude
       uint32_t g = 0;
       if (lane == 0) g = atomicAdd(&next_group, 1u);
       g = __shfl_sync(0xffffffffu, g, 0);
@@ -76,7 +308,7 @@ k_scatter(const ScatterItem* __restrict__ items, int n_items, const float* __res
   }
 }
 
-int scatter_smem_bytes(int b) {
+int scatter_warp_smem_bytes(int b) {
   const int64_t q = int64_t(1) << b;
   return (int)(((q + 3) & ~int64_t(3)) * 4 + (2 * kScatterMaxGroups + 8) * 4);
 }
@@ -84,23 +316,59 @@ int scatter_smem_bytes(int b) {
 }  // namespace
 
 int prepare_scatter(pcpm_handle* h) {
-  PCPM_CK(cudaFuncSetAttribute(k_scatter<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               scatter_smem_bytes(kMaxBits)));
-  PCPM_CK(cudaFuncSetAttribute(k_scatter<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               scatter_smem_bytes(kMaxBits)));
+  (void)h;
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_warp_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_warp_smem_bytes(kMaxBits)));
   return PCPM_OK;
 }
 
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
   if (h->n_sitems == 0) return PCPM_OK;
-  const int smem = scatter_smem_bytes(h->b);
   const int grid = std::min(h->n_sitems, h->num_sms);
-  if (h->wide)
-    k_scatter<uint32_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b, h->k_dst,
-                                                            h->png_src, h->png_off, h->upd_off, h->upd);
-  else
-    k_scatter<uint16_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b, h->k_dst,
-                                                            h->png16, h->png_off, h->upd_off, h->upd);
+  if (h->opt_scatter_variant == 1 || h->b < 2) {   // the bulk-copy variant needs 16 B aligned slices
+    const int smem = scatter_warp_smem_bytes(h->b);
+    if (h->wide)
+      k_scatter_warp<uint32_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b,
+                                                                   h->k_dst, h->png_src, h->png_off, h->upd_off,
+                                                                   h->upd);
+    else
+      k_scatter_warp<uint16_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b,
+                                                                   h->k_dst, h->png16, h->png_off, h->upd_off,
+                                                                   h->upd);
+  } else {
+    // the bulk copy of a source slice reads whole 16 B words: x must be 16 B aligned
+    // and readable up to round16(n_src); internal vectors are padded, user vectors
+    // that are not go through the padded staging buffer
+    if ((reinterpret_cast<uintptr_t>(x) & 15) != 0 ||
+        ((h->n_src & 3) != 0 && x != h->spr && x != h->xbuf)) {
+      PCPM_CK(cudaMemcpyAsync(h->xbuf, x, sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
+      x = h->xbuf;
+    }
+    ScatterArgs a{};
+    a.items = h->sitems;
+    a.n_items = h->n_sitems;
+    a.x = x;
+    a.n_src = h->n_src;
+    a.b = h->b;
+    a.k_dst = h->k_dst;
+    a.png = h->wide ? static_cast<const void*>(h->png_src) : static_cast<const void*>(h->png16);
+    a.png_off = h->png_off;
+    a.upd_off = h->upd_off;
+    a.upd = h->upd;
+    a.counters = h->counters;
+    a.pf_stages = h->opt_scatter_pf;
+    const int smem = scatter_tma_smem_bytes(h->b);
+    if (h->wide)
+      k_scatter_tma<uint32_t><<<grid, kScThreads, smem, s>>>(a);
+    else
+      k_scatter_tma<uint16_t><<<grid, kScThreads, smem, s>>>(a);
+  }
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return PCPM_OK;
