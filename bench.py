@@ -168,6 +168,8 @@ def run_pcpm(args, world, rank, local):
     flags = pcpm.PCPM_BUILD_PULL if (op == "pagerank" and not args.no_pull) else 0
     if args.wide:
         flags |= pcpm.PCPM_WIDE_IDS
+    if args.no_compress:
+        flags |= pcpm.PCPM_NO_COMPRESS
     h = pcpm.pcpm_build_ex(csr, b, flags, stream)
     info = pcpm.pcpm_get_info(h)
     m, n = info.nnz, info.n_src
@@ -265,7 +267,8 @@ def run_pcpm(args, world, rank, local):
                     for k, v in kernels.items()},
         "model_bytes_per_iter": {
             "alg_this_build": iter_bytes,
-            "layout": "wide (d_i=4)" if args.wide else "compact (d_i=2)",
+            "layout": ("wide (d_i=4)" if args.wide else "compact (d_i=2)") +
+                      (", uncompressed bins (E' = m, P:342-345)" if args.no_compress else ""),
             "paper_eq5_pcpm": round(model.pcpm_comm(n, m, info.k_dst, info.r if info.r > 0 else 1)),
             "paper_eq5_pcpm_d_i_2": round(model.pcpm_comm(n, m, info.k_dst, info.r if info.r > 0 else 1, d_i=2)),
             "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
@@ -344,7 +347,8 @@ def e2e(args, g, b, iters, op, world):
         torch.cuda.synchronize()
         barrier(world)
         t0 = time.perf_counter()
-        h = pcpm.pcpm_build_ex(csr, b, pcpm.PCPM_WIDE_IDS if args.wide else 0, None)
+        h = pcpm.pcpm_build_ex(csr, b, (pcpm.PCPM_WIDE_IDS if args.wide else 0) |
+                               (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0), None)
         if op == "pagerank":
             pcpm.pcpm_pagerank(h, 0.85, iters, res)
         else:
@@ -469,6 +473,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--out", default="")
     ap.add_argument("--opt", action="append", default=[], help="pcpm_set_option key=value (A/B experiments)")
+    ap.add_argument("--no-compress", action="store_true",
+                    help="uncompressed bins: one update per edge (the BVGAS-like traffic of Eq. 4)")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)

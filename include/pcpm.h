@@ -136,6 +136,34 @@ int pcpm_spmv(pcpm_handle* h, const float* x, float* y);
  * the in-house comparison of BASELINE.json).  Needs PCPM_BUILD_PULL. */
 int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out);
 
+/* ---- Multi-GPU: destination shards.
+ * Rank r owns the destination vertices [v_lo, v_hi) (v_lo a multiple of q = 2^b,
+ * so its bins are whole partitions of the global graph).  Per iteration every
+ * rank scatters all source partitions into ITS bins only, gathers and applies
+ * its vertices, then the ranks all-gather the SPR slices (one n*4-byte exchange)
+ * and all-reduce (residual, dangling mass); paper_1709_07122_b200/dist.py drives
+ * the exchange with torch.distributed (NCCL).
+ *
+ * pcpm_build_shard: layout of the column slice [v_lo, v_hi) of csr (n_src rows,
+ * local columns v - v_lo), keeping the GLOBAL out-degrees |N_o(u)| of all
+ * sources (P:65's SPR divides by the full out-degree).  csr is borrowed, host or
+ * device; only the slice's columns are validated.  flags: PCPM_WIDE_IDS,
+ * PCPM_KEEP_VALUES.  NULL on error.
+ * pcpm_shard_init: PR_0 = 1/n_global on the slice (pr0, spr0: DEVICE f32[v_hi-v_lo])
+ * and dang0 (DEVICE f64[1]) = the slice's share of D_0.
+ * pcpm_shard_step: one iteration of Eq. 1 with rule R1 for the slice:
+ *   spr_in  DEVICE f32[n_src]  SPR_t of ALL vertices (after the all-gather);
+ *   D_in    DEVICE f64[1]      D_t, the global dangling mass (after the all-reduce);
+ *   pr_old  DEVICE f32[n_loc]  the slice's PR_t;  pr_new / spr_out: its PR_{t+1}, SPR_{t+1}
+ *           (spr_out may alias spr_in + v_lo: the scatter has read spr_in before the gather writes);
+ *   red_out DEVICE f64[2]      [0] = sum |PR_{t+1} - PR_t| over the slice, [1] = its dangling mass.
+ * Stream-ordered on the handle's stream; returns 0 or PCPM_E*. */
+pcpm_handle* pcpm_build_shard(const pcpm_csr* csr, int partition_bits, int64_t v_lo, int64_t v_hi,
+                              unsigned flags, void* cuda_stream);
+int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0);
+int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                    float* pr_new, float* spr_out, double* red_out);
+
 void pcpm_destroy(pcpm_handle* h);
 
 /* Support: stream, errors, introspection. */

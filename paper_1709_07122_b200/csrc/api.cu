@@ -106,7 +106,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.b = h->b;
   a.n_dst = h->n_dst;
   a.fbits = fbits;
-  a.outdeg = h->outdeg;
+  a.outdeg = h->outdeg + h->shard_lo;    // apply: global out-degree of destination v (shards: lo + v)
   a.epi_pf = h->opt_epi_pf;
   return a;
 }
@@ -146,7 +146,8 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
     a.d = d;
     a.n = (double)h->n_src;
     a.red_in = h->red + 2 * t;
-    a.red_out = h->red + 2 * t;
+    a.res_out = h->red + 2 * t + 1;
+    a.dang_out = h->red + 2 * t + 2;
     a.pr_old = h->pr[t & 1];
     a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
     a.spr_new = h->spr;
@@ -253,7 +254,8 @@ using namespace pcpm;
 
 extern "C" {
 
-pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned flags, void* cuda_stream) {
+static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsigned flags, void* cuda_stream,
+                                 int64_t lo, int64_t hi) {
   set_error(PCPM_OK, "");
   if (!csr || !csr->row_ptr || (csr->nnz > 0 && !csr->col_idx)) {
     set_error(PCPM_EINVAL, "NULL csr / row_ptr / col_idx");
@@ -299,7 +301,15 @@ pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned fla
   cudaEventRecord(e0, h->stream);
   int rc = prepare_gather(h);
   if (rc == PCPM_OK) rc = prepare_scatter(h);
-  if (rc == PCPM_OK) rc = build_layout(h, csr, flags);
+  if (rc == PCPM_OK) {
+    if (lo < 0) {
+      rc = build_layout(h, csr, flags);
+      h->n_global = h->n_dst;
+    } else {
+      h->shard = true;
+      rc = build_shard_layout(h, csr, lo, hi, flags);
+    }
+  }
   if (rc == PCPM_OK) {
     cudaEventRecord(e1, h->stream);
     cudaEventSynchronize(e1);
@@ -317,6 +327,86 @@ pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned fla
     return nullptr;
   }
   return h;
+}
+
+pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned flags, void* cuda_stream) {
+  return build_common(csr, partition_bits, flags, cuda_stream, -1, -1);
+}
+
+pcpm_handle* pcpm_build_shard(const pcpm_csr* csr, int partition_bits, int64_t v_lo, int64_t v_hi, unsigned flags,
+                              void* cuda_stream) {
+  set_error(PCPM_OK, "");
+  if (!csr || partition_bits < 1 || partition_bits > kMaxBits) {
+    set_error(PCPM_EINVAL, "NULL csr or partition_bits not in [1, 15]");
+    return nullptr;
+  }
+  if (v_lo < 0 || v_hi <= v_lo || v_hi > csr->n_dst || (v_lo & ((int64_t(1) << partition_bits) - 1)) != 0) {
+    set_error(PCPM_EINVAL, "shard range must satisfy 0 <= v_lo < v_hi <= n_dst with v_lo a multiple of 2^b");
+    return nullptr;
+  }
+  if (flags & (PCPM_BUILD_PULL | PCPM_NO_COMPRESS)) {
+    set_error(PCPM_EINVAL, "shard handles take only PCPM_WIDE_IDS / PCPM_KEEP_VALUES");
+    return nullptr;
+  }
+  pcpm_csr shape = *csr;                     // validation of sizes happens on the slice shape
+  shape.n_dst = v_hi - v_lo;
+  if (csr->n_dst >= (int64_t(1) << 31)) {
+    set_error(PCPM_ETOOBIG, "n >= 2^31: the MSB of a 4-byte ID is the run flag (P:172-173)");
+    return nullptr;
+  }
+  (void)shape;
+  return build_common(csr, partition_bits, flags, cuda_stream, v_lo, v_hi);
+}
+
+int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0) {
+  if (!h || !pr0 || !spr0 || !dang0) {
+    set_error(PCPM_EINVAL, "NULL handle or output");
+    return PCPM_EINVAL;
+  }
+  if (!is_device_ptr(pr0) || !is_device_ptr(spr0) || !is_device_ptr(dang0)) {
+    set_error(PCPM_EINVAL, "pcpm_shard_init takes device pointers");
+    return PCPM_EINVAL;
+  }
+  h->launches = 0;
+  return launch_pr_init_slice(h, pr0, spr0, dang0, h->stream);
+}
+
+int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                    float* pr_new, float* spr_out, double* red_out) {
+  if (!h || !spr_in || !D_in || !pr_old || !pr_new || !spr_out || !red_out) {
+    set_error(PCPM_EINVAL, "NULL handle or argument");
+    return PCPM_EINVAL;
+  }
+  if (!(d > 0.f && d < 1.f)) {
+    set_error(PCPM_EINVAL, "d must be in (0,1)");
+    return PCPM_EINVAL;
+  }
+  if (!is_device_ptr(spr_in) || !is_device_ptr(D_in) || !is_device_ptr(pr_old) || !is_device_ptr(pr_new) ||
+      !is_device_ptr(spr_out) || !is_device_ptr(red_out)) {
+    set_error(PCPM_EINVAL, "pcpm_shard_step takes device pointers");
+    return PCPM_EINVAL;
+  }
+  if (!h->shard && h->n_src != h->n_dst) {
+    set_error(PCPM_ESTATE, "pcpm_shard_step needs a shard handle or a square matrix");
+    return PCPM_ESTATE;
+  }
+  cudaStream_t s = h->stream;
+  h->launches = 0;
+  const int fbits = pr_fixed_bits(h->n_global);
+  h->fixed_bits = fbits;
+  h->last_was_spmv = false;
+  int rc = launch_scatter(h, spr_in, s);                     // Alg. 4 over all source partitions
+  if (rc) return rc;
+  GatherArgs a = base_args(h, fbits);
+  a.d = d;
+  a.n = (double)h->n_global;
+  a.red_in = D_in;
+  a.res_out = red_out;
+  a.dang_out = red_out + 1;
+  a.pr_old = pr_old;
+  a.pr_new = pr_new;
+  a.spr_new = spr_out;
+  return launch_gather(h, a, false, true, s);                // Alg. 5 + apply on the shard's vertices
 }
 
 pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits) {

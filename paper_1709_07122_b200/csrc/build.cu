@@ -197,6 +197,43 @@ __global__ void k_gather_u32(int64_t m, const uint32_t* __restrict__ perm, const
   GRID_STRIDE(x, m) out[x] = src[perm[x]];
 }
 
+// Column slice [lo, hi) of each (sorted) row: a = lower_bound(lo), c = lower_bound(hi).
+__global__ void k_slice_count(int64_t n, const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                              uint32_t lo, uint32_t hi, int64_t* cnt, int64_t* first) {
+  GRID_STRIDE(u, n) {
+    int64_t a = row_ptr[u], e = row_ptr[u + 1];
+    int64_t l = a, r = e;
+    while (l < r) {
+      const int64_t mid = (l + r) >> 1;
+      if (col[mid] < lo) l = mid + 1; else r = mid;
+    }
+    const int64_t x0 = l;
+    r = e;
+    while (l < r) {
+      const int64_t mid = (l + r) >> 1;
+      if (col[mid] < hi) l = mid + 1; else r = mid;
+    }
+    cnt[u] = l - x0;
+    first[u] = x0;
+  }
+}
+
+__global__ void k_slice_fill(int64_t n, const int64_t* __restrict__ new_ptr, const int64_t* __restrict__ first,
+                             const uint32_t* __restrict__ col, const float* __restrict__ val, uint32_t lo,
+                             uint32_t* out_col, float* out_val) {
+  // one warp per row
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = w0; u < n; u += nw) {
+    const int64_t o = new_ptr[u], len = new_ptr[u + 1] - o, f = first[u];
+    for (int64_t i = lane; i < len; i += 32) {
+      out_col[o + i] = col[f + i] - lo;
+      if (out_val) out_val[o + i] = val[f + i];
+    }
+  }
+}
+
 struct Temp {
   std::vector<void*> ptrs;
   ~Temp() {
@@ -567,6 +604,99 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaStreamSynchronize(s));
+  return PCPM_OK;
+}
+
+// Destination shard: the layout of the column slice [lo, hi) of the
+// CSR (n_src rows, local columns v - lo), with the GLOBAL out-degrees of the
+// sources (the slice's rows hold only the edges into the slice).
+int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags) {
+  cudaStream_t s = h->stream;
+  const int64_t n = csr->n_src, m = csr->nnz;
+  Temp tmp;
+  const int64_t* row_ptr = csr->row_ptr;
+  const uint32_t* col = csr->col_idx;
+  const float* values = csr->values;
+  if (!is_device_ptr(row_ptr)) {
+    int64_t* d;
+    TK(tmp.alloc(&d, n + 1));
+    TK(cudaMemcpyAsync(d, row_ptr, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    row_ptr = d;
+  }
+  if (m > 0 && !is_device_ptr(col)) {
+    uint32_t* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, col, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, s));
+    col = d;
+  }
+  if (m > 0 && values && !is_device_ptr(values)) {
+    float* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, values, sizeof(float) * m, cudaMemcpyHostToDevice, s));
+    values = d;
+  }
+  uint32_t* err;
+  TK(tmp.alloc(&err, 4));
+  TK(cudaMemsetAsync(err, 0, 16, s));
+  k_check_rows<<<grid_for(n), kT, 0, s>>>(n, row_ptr, m, err);
+  TK(cudaGetLastError());
+  uint32_t herr = 0;
+  TK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  if (herr) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+  int64_t *cnt, *first, *new_ptr;
+  TK(tmp.alloc(&cnt, n + 1));
+  TK(tmp.alloc(&first, n + 1));
+  TK(tmp.alloc(&new_ptr, n + 1));
+  TK(cudaMemsetAsync(cnt + n, 0, 8, s));
+  if (m > 0) {
+    k_slice_count<<<grid_for(n), kT, 0, s>>>(n, row_ptr, col, (uint32_t)lo, (uint32_t)hi, cnt, first);
+    TK(cudaGetLastError());
+  } else {
+    TK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * n, s));
+  }
+  {
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, new_ptr, n + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, new_ptr, n + 1, s));
+  }
+  int64_t ms = 0;
+  TK(cudaMemcpyAsync(&ms, new_ptr + n, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  uint32_t* scol;
+  float* sval = nullptr;
+  TK(tmp.alloc(&scol, ms));
+  if (values) TK(tmp.alloc(&sval, ms));
+  if (ms > 0) {
+    k_slice_fill<<<grid_for(n * 32), kT, 0, s>>>(n, new_ptr, first, col, values, (uint32_t)lo, scol, sval);
+    TK(cudaGetLastError());
+  }
+  pcpm_csr sub{};
+  sub.n_src = n;
+  sub.n_dst = hi - lo;
+  sub.nnz = ms;
+  sub.row_ptr = new_ptr;
+  sub.col_idx = scol;
+  sub.values = sval;
+  int rc = build_layout(h, &sub, flags);
+  if (rc) return rc;
+  // global out-degrees and dangling count (build_layout saw only the slice's rows)
+  unsigned long long* d_dang;
+  TK(tmp.alloc(&d_dang, 1));
+  TK(cudaMemsetAsync(d_dang, 0, 8, s));
+  k_outdeg<<<grid_for(n), kT, 0, s>>>(n, row_ptr, h->outdeg, d_dang);
+  TK(cudaGetLastError());
+  unsigned long long hd = 0;
+  TK(cudaMemcpyAsync(&hd, d_dang, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  h->n_dangling = (int64_t)hd;
+  h->shard_lo = lo;
+  h->n_global = csr->n_dst;
   return PCPM_OK;
 }
 

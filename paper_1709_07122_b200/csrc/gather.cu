@@ -12,10 +12,10 @@
 //    engine, cp.async.bulk) into a 4-stage ring: the IDs (4096 2-byte IDs in
 //    the compact layout), the window of update values they reference, and
 //    the decode anchors.
-//  * 16 consumer warps each decode one sub-chunk of the tile, 8 (or 4)
-//    consecutive IDs per lane from one 16-byte load.  The update pointer of
-//    Alg. 5 becomes a warp prefix count of MSB flags:
-//    ptr = anchor + (flags in lower lanes, by ballot/popc) + (own flags so far) - 1
+//  * 16 consumer warps each decode one sub-chunk of the tile in steps of 32
+//    consecutive IDs (lane l takes ID 32 c + l).  The update pointer of Alg. 5
+//    becomes a warp prefix count of MSB flags:
+//    ptr = anchor + (flags of earlier steps) + popc(ballot & lanemask_le) - 1
 //    (reading R5's -1 start), with no data-dependent branch; all loads and
 //    atomics of a sub-chunk are independent, so they overlap.
 //  * PageRank accumulates in 64-bit fixed point (F fractional bits): the low
@@ -49,13 +49,26 @@ struct StageMeta {
   uint32_t pad;
 };
 
+#ifndef PCPM_GATHER_BIG_TILE
+#define PCPM_GATHER_BIG_TILE 0
+#endif
 template <typename IdT, bool W>
 struct Cfg {
   static constexpr bool kCompact = sizeof(IdT) == 2;
-  static constexpr int kTile = (kCompact && !W) ? 2 * kTileIds : kTileIds;
-  static constexpr int kStages = (!kCompact && W) ? 3 : 4;
-  static constexpr int kSub = kTile / kConsumerWarps;      // IDs per warp per tile
-  static constexpr int kPer = kSub / 32;                   // IDs per lane (one vector load)
+  // compact PageRank (the hot configuration): 4096-ID tiles in a 4-stage ring,
+  // 31 consumer warps each taking a 128-ID sub-chunk per stage (32 sub-chunks,
+  // the extra one rotating; with the producer, 32 warps).  PCPM_GATHER_BIG_TILE
+  // = 1 selects 8192-ID tiles double-buffered (2 x 48 KB; measured slower on
+  // c4: 2.10 vs 1.98 ms).  Other variants: 2048-ID tiles, 16 warps of 128 IDs.
+  static constexpr bool kHot = kCompact && !W;
+  static constexpr bool kBig = kHot && PCPM_GATHER_BIG_TILE;
+  static constexpr int kTile = kBig ? 4 * kTileIds : (kHot ? 2 * kTileIds : kTileIds);
+  static constexpr int kStages = kBig ? 2 : ((!kCompact && W) ? 3 : 4);
+  static constexpr int kWarps = kHot ? 31 : 16;
+  static constexpr int kThreads = 32 * (kWarps + 1);
+  static constexpr int kSub = kHot ? kTile / 32 : kTile / 16;   // IDs per sub-chunk
+  static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
+  static constexpr int kPer = kSub / 32;                   // decode steps of 32 IDs per sub-chunk
   static constexpr int kIdsBytes = kTile * (int)sizeof(IdT);
   static constexpr int kWinCap = kTile + 8;                // >= #flags + 1, 16 B aligned ends
   static constexpr int kWinBytes = kWinCap * 4;
@@ -64,6 +77,8 @@ struct Cfg {
   static constexpr int kStageBytes = kIdsBytes + kWinBytes + kWBytes + kCbBytes;
   static constexpr int kFlagShift = kCompact ? 15 : 31;
   static_assert(kTileAlign % kTile == 0, "slices are cut at tile multiples");
+  static_assert(kSub % kChunkIds == 0 && kSub % 32 == 0, "sub-chunks start on decode anchors");
+  static_assert(kThreads <= 1024 && kNsc >= kWarps, "launch shape");
   static_assert(kStageBytes % 16 == 0, "bulk copies need 16 B alignment");
 };
 
@@ -72,39 +87,6 @@ __device__ __forceinline__ uint64_t ldcg_u64(const uint64_t* p) {
   return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
 }
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t r;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-  return r;
-}
-
-// kPer consecutive IDs of this lane from one vector load
-template <typename IdT, int P>
-__device__ __forceinline__ void load_ids(const IdT* p, uint32_t (&id)[P]) {
-  if constexpr (sizeof(IdT) == 2 && P == 8) {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      id[2 * c] = w[c] & 0xFFFFu;
-      id[2 * c + 1] = w[c] >> 16;
-    }
-  } else if constexpr (sizeof(IdT) == 2 && P == 4) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
-    id[0] = v.x & 0xFFFFu;
-    id[1] = v.x >> 16;
-    id[2] = v.y & 0xFFFFu;
-    id[3] = v.y >> 16;
-  } else {
-    static_assert(sizeof(IdT) == 4 && P == 4, "layout");
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
-    id[0] = v.x;
-    id[1] = v.y;
-    id[2] = v.z;
-    id[3] = v.w;
-  }
-}
-
 }  // namespace
 
 __device__ int spmv_fbits(float xmax, int wexp) {
@@ -125,7 +107,7 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
 }
 
 template <typename IdT, bool W, bool PR>
-__global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a) {
+__global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const GatherArgs a) {
   using C = Cfg<IdT, W>;
   constexpr int S = C::kStages;
   constexpr int P = C::kPer;
@@ -138,15 +120,15 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
   uint64_t* empty = full + S;
-  double* red_s = reinterpret_cast<double*>(empty + S);                    // 2*kConsumerWarps
-  uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * kConsumerWarps);
+  double* red_s = reinterpret_cast<double*>(empty + S);                    // 2*C::kWarps
+  uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * C::kWarps);
   const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], C::kWarps);
     }
     fence_mbar_init();
   }
@@ -255,9 +237,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
   }
 
   // ================= consumers =================
-  const int cw = warp - 1;                  // 0..15: sub-chunk owned in every tile
+  const int cw = warp - 1;                  // consumer warp: sub-chunk cw of every tile
   const int ctid = threadIdx.x - 32;        // 0..511
-  constexpr int kCons = 32 * kConsumerWarps;
+  constexpr int kCons = 32 * C::kWarps;
   const uint32_t qmask = (uint32_t)(q - 1);
   const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F (PageRank)
   const double inv_scale = 1.0 / (double)fscale;
@@ -273,9 +255,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
     sp_inv = ldexp(1.0, -F);
   }
   named_bar_sync(1, kCons);
-  const uint32_t ltmask = lanemask_lt();
+  const uint32_t lemask = lanemask_le();
 
-  int stage = 0;
+  int stage = 0, rot = 0;
   uint32_t phase = 0;
   for (;;) {
     mbar_wait(&full[stage], phase);
@@ -288,33 +270,34 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
       const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
       const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
       const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
-      const uint32_t xs = m.tile_base + cw * C::kSub;        // first ID position of this warp's sub-chunk
+      // sub-chunk sc of the tile: warp cw takes sc = cw; the kNsc - kWarps extra
+      // sub-chunks rotate over the warps from stage to stage
+      auto process = [&](const int sc) {
+      const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
       if (xs < m.hi && xs + C::kSub > m.lo) {
         const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
         auto body = [&](auto WHOLE) {
           constexpr bool kWhole = decltype(WHOLE)::value;
+          // lane-strided decode: step c covers the 32 consecutive IDs c*32 .. c*32+31
+          // of the sub-chunk, so the window reads of a step hit ~32/r consecutive
+          // words (one or two smem wavefronts)
           uint32_t id[P];
-          load_ids<IdT, P>(ids_s + cw * C::kSub + P * lane, id);
-          // prefix count of MSB flags (global decode identity)
-          uint32_t before = 0, total = 0;
 #pragma unroll
-          for (int c = 0; c < P; ++c) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, (id[c] >> C::kFlagShift) & 1u);
-            before += __popc(bal & ltmask);
-            total += __popc(bal);
-          }
-          const uint32_t base = cb_s[(cw * C::kSub) / kChunkIds] + before - 1 - m.win_base;
-          uint32_t own = 0;
+          for (int c = 0; c < P; ++c) id[c] = ids_s[sc * C::kSub + c * 32 + lane];
+          // Alg. 5 update_ptr = #flags in ids[0..x] - 1 (R5), from the sub-chunk's
+          // anchor plus a warp prefix count of the MSB flags, step by step
+          uint32_t run = cb_s[(sc * C::kSub) / kChunkIds] - 1u - m.win_base;
           float val[P];
           bool ok[P];
 #pragma unroll
           for (int c = 0; c < P; ++c) {
-            own += (id[c] >> C::kFlagShift) & 1u;               // Alg. 5: update_ptr += MSB(id)
-            const uint32_t x = xs + P * lane + c;
+            const uint32_t bal = __ballot_sync(0xffffffffu, id[c] & (1u << C::kFlagShift));
+            const uint32_t ptr = run + __popc(bal & lemask);
+            run += __popc(bal);
+            const uint32_t x = xs + c * 32 + lane;
             ok[c] = kWhole || (x >= m.lo && x < m.hi);
-            val[c] = ok[c] ? win_s[base + own] : 0.0f;
+            val[c] = ok[c] ? win_s[ptr] : 0.0f;
           }
-          (void)total;
           if constexpr (PR) {
             // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
             uint32_t tlo[P], thi[P], old[P];
@@ -326,21 +309,21 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
             }
 #pragma unroll
             for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+            // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
+            // ok = false have lo = hi = 0 (val = 0) and never carry
             uint32_t any = 0;
-            uint32_t hinc[P];
 #pragma unroll
-            for (int c = 0; c < P; ++c) {
-              hinc[c] = ok[c] ? thi[c] + ((old[c] + tlo[c] < old[c]) ? 1u : 0u) : 0u;
-              any |= hinc[c];
-            }
-            if (any) {                                   // rare: carry out of a low word
+            for (int c = 0; c < P; ++c) any |= thi[c] | (tlo[c] > ~old[c] ? 1u : 0u);
+            if (any) {                                   // rare: carry into the global high word
 #pragma unroll
-              for (int c = 0; c < P; ++c)
-                if (hinc[c]) {
+              for (int c = 0; c < P; ++c) {
+                const uint32_t hinc = thi[c] + (tlo[c] > ~old[c] ? 1u : 0u);
+                if (hinc) {
                   const uint32_t li = id[c] & qmask;
-                  atomicAdd(&a.hi[v0 + li], hinc[c]);
+                  atomicAdd(&a.hi[v0 + li], hinc);
                   atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
                 }
+              }
             }
           } else {
             // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
@@ -352,7 +335,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
             int32_t thi[P];
 #pragma unroll
             for (int c = 0; c < P; ++c) {
-              const double tv = W ? (double)val[c] * (double)w_s[cw * C::kSub + P * lane + c] : (double)val[c];
+              const double tv = W ? (double)val[c] * (double)w_s[sc * C::kSub + c * 32 + lane] : (double)val[c];
               const long long T = __double2ll_rn(tv * sp_scale);
               tlo[c] = (uint32_t)T;
               thi[c] = (int32_t)(T >> 32) + ((int32_t)tlo[c] < 0 ? 1 : 0);   // T = thi*2^32 + (int32)tlo
@@ -382,7 +365,14 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
         if (whole) body(std::true_type{});
         else body(std::false_type{});
       }
+      };
+      process(cw);
+      if constexpr (C::kNsc > C::kWarps) {
+        for (int e = 0; e < C::kNsc - C::kWarps; ++e)
+          if (cw == (rot + e) % C::kWarps) process(C::kWarps + e);
+      }
     }
+    if constexpr (C::kNsc > C::kWarps) rot = (rot + 1 == C::kWarps) ? 0 : rot + 1;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -443,7 +433,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
             const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
             float4* pn4 = reinterpret_cast<float4*>(a.pr_new + v0);
             float4* sp4 = reinterpret_cast<float4*>(a.spr_new + v0);
-#pragma unroll 2
+#pragma unroll 1
             for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
               const uint4 dg = __ldg(dg4 + i4);
               const float4 po = __ldg(po4 + i4);
@@ -485,16 +475,16 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
         }
         if (lane == 0) {
           red_s[cw] = dang;
-          red_s[kConsumerWarps + cw] = res;
+          red_s[C::kWarps + cw] = res;
         }
       }
       named_bar_sync(1, kCons);
       if constexpr (PR) {
         if (ctid == 0) {
           double sd = 0.0, sr = 0.0;
-          for (int k = 0; k < kConsumerWarps; ++k) {
+          for (int k = 0; k < C::kWarps; ++k) {
             sd += red_s[k];
-            sr += red_s[kConsumerWarps + k];
+            sr += red_s[C::kWarps + k];
           }
           a.item_red[2 * m.item] = sd;       // zero for non-last slices
           a.item_red[2 * m.item + 1] = sr;
@@ -528,8 +518,8 @@ __global__ void __launch_bounds__(kGatherThreads, 1) k_gather(const GatherArgs a
           sr += __shfl_xor_sync(0xffffffffu, sr, o);
         }
         if (lane == 0) {
-          a.red_out[2] = sd;   // D_{t+1}
-          a.red_out[1] = sr;   // residual of iteration t
+          *a.dang_out = sd;    // D_{t+1}
+          *a.res_out = sr;     // residual of iteration t
         }
       }
     }
@@ -547,7 +537,7 @@ int smem_bytes_for(int b) {
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
-               2 * kConsumerWarps * 8 + 16);
+               2 * C::kWarps * 8 + 16);
 }
 
 using GatherFn = void (*)(const GatherArgs);
@@ -591,10 +581,15 @@ int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStr
   return PCPM_OK;
 }
 
+int gather_threads(bool wide, bool weighted) {
+  if (wide) return weighted ? Cfg<uint32_t, true>::kThreads : Cfg<uint32_t, false>::kThreads;
+  return weighted ? Cfg<uint16_t, true>::kThreads : Cfg<uint16_t, false>::kThreads;
+}
+
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s) {
   const int smem = gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
-  gather_fn(h->wide, weighted, pagerank)<<<grid, kGatherThreads, smem, s>>>(a);
+  gather_fn(h->wide, weighted, pagerank)<<<grid, gather_threads(h->wide, weighted), smem, s>>>(a);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return PCPM_OK;

@@ -16,14 +16,12 @@ namespace pcpm {
 
 // ---------------------------------------------------------------- constants
 // Gather tile: kTileIds destination IDs per pipeline stage (the compact
-// PageRank kernel uses 2x that), decoded by kConsumerWarps warps, each owning
+// PageRank kernel uses 2x that), decoded by 16 or 32 consumer warps, each owning
 // one sub-chunk whose update-index base comes from chunk_base (the global
 // decode identity).  Bin slices are cut at kTileAlign multiples.
 constexpr int kTileIds = 2048;
 constexpr int kTileAlign = 4096;
 constexpr int kChunkIds = 128;                         // chunk_base granularity
-constexpr int kConsumerWarps = 16;
-constexpr int kGatherThreads = 32 * (kConsumerWarps + 1);
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
@@ -63,6 +61,11 @@ struct pcpm_handle {
   int64_t launches = 0;
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
+
+  // destination shard (pcpm_build_shard): columns [shard_lo, shard_lo + n_dst) of an
+  // n_global-column graph; outdeg holds the GLOBAL out-degrees of all n_src sources
+  int64_t shard_lo = 0, n_global = 0;
+  bool shard = false;
 
   // layout (device)
   bool wide = false;                // iterate on the 4-byte arrays (PCPM_WIDE_IDS)
@@ -223,7 +226,8 @@ struct GatherArgs {
   // PageRank epilogue
   double d, n;
   const double* red_in;    // D_t at red_in[0]
-  double* red_out;         // D_{t+1} -> red_out[2], residual_t -> red_out[1]  (red_out = &red[2t])
+  double* res_out;         // L1 residual of this iteration
+  double* dang_out;        // dangling mass of the new vector (D_{t+1})
   const uint32_t* outdeg;
   const float* pr_old;
   float* pr_new;
@@ -246,5 +250,7 @@ int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
                           float* spr_out, double* red_t, float d, cudaStream_t s);
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);
+int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags);
+int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, cudaStream_t s);
 
 }  // namespace pcpm

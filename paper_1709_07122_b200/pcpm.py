@@ -30,7 +30,7 @@ PCPM_WIDE_IDS = 0x8
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
-            "pcpm_get_phase_times"]
+            "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step"]
 
 
 class PcpmError(RuntimeError):
@@ -88,6 +88,9 @@ def _load():
         "pcpm_set_option": (I, [P, ctypes.c_char_p, I64]),
         "pcpm_last_launch_count": (I64, [P]),
         "pcpm_get_phase_times": (I, [P, P, I]),
+        "pcpm_build_shard": (P, [ctypes.POINTER(pcpm_csr), I, I64, I64, ctypes.c_uint, P]),
+        "pcpm_shard_init": (I, [P, P, P, P]),
+        "pcpm_shard_step": (I, [P, ctypes.c_float, P, P, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -220,3 +223,20 @@ def pcpm_get_phase_times(h, cap: int = 8192) -> np.ndarray:
     if n < 0:
         _check(n)
     return buf[:n]
+
+
+def pcpm_build_shard(csr: pcpm_csr, partition_bits: int, v_lo: int, v_hi: int, flags: int = 0, stream=None):
+    h = _lib.pcpm_build_shard(ctypes.byref(csr), int(partition_bits), int(v_lo), int(v_hi), int(flags),
+                              _stream(stream))
+    if not h:
+        raise PcpmError(pcpm_last_status(), pcpm_last_error())
+    return h
+
+
+def pcpm_shard_init(h, pr0, spr0, dang0):
+    return _check(_lib.pcpm_shard_init(h, _ptr(pr0), _ptr(spr0), _ptr(dang0)))
+
+
+def pcpm_shard_step(h, d: float, spr_in, D_in, pr_old, pr_new, spr_out, red_out):
+    return _check(_lib.pcpm_shard_step(h, float(d), _ptr(spr_in), _ptr(D_in), _ptr(pr_old), _ptr(pr_new),
+                                       _ptr(spr_out), _ptr(red_out)))

@@ -68,8 +68,10 @@ def test_fullsize_pagerank(pcpm, key):
     deg = np.diff(gn.row_ptr)
     assert red[2 * (iters - 1)] == pytest.approx(
         oracle.pagerank_pull(n, gn.row_ptr, in_ptr, in_src, d, iters - 1)[deg == 0].sum(), rel=1e-5)
+    # contraction, down to the floor set by storing PR in fp32 between iterations
+    # (each stored value rounds by <= 2^-24 relative, so sum |rounding| <= 2^-24)
     res = red[1::2][:iters]
-    assert np.all(res[1:] <= d * res[:-1] * (1 + 1e-3) + 1e-9), res
+    assert np.all(res[1:] <= d * res[:-1] * (1 + 1e-3) + 2.0 ** -22), res
 
 
 def test_fullsize_spmv(pcpm):
