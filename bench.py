@@ -292,6 +292,105 @@ def run_pcpm(args, world, rank, local):
     return line
 
 
+def run_sharded(args, world, rank, local):
+    """PageRank of ONE graph over N GPUs: destination shards + NCCL all-gather.
+
+    Strong scaling: every step is the whole graph's `iters` iterations; value =
+    m * iters * K / (max-over-ranks device time)."""
+    import torch
+    from paper_1709_07122_b200 import dist as pdist
+
+    key = args.config
+    dev = torch.device("cuda", local)
+    g = make_graph(key, dev)
+    iters = args.iters or g.meta["iters"]
+    b = g.meta["bits"]
+    n, m = g.n_src, g.m
+    stream = torch.cuda.current_stream()
+    sh = pdist.ShardedPageRank(n, g.row_ptr, g.col, b, device=dev, stream=stream, timing=True)
+    info = sh.info()
+    rp_h = col_h = None
+    if not args.no_e2e:
+        rp_h = torch.empty(g.row_ptr.numel(), dtype=torch.int64, pin_memory=True)
+        col_h = torch.empty(g.col.numel(), dtype=torch.int32, pin_memory=True)
+        rp_h.copy_(g.row_ptr)
+        col_h.copy_(g.col)
+    del g
+    torch.cuda.empty_cache()
+
+    def step():
+        sh.run(0.85, iters)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    comp, comm = sh.phase_ms()                       # last step
+    ms_max = max_over_ranks(ms, world)
+    comp_max = max_over_ranks(comp, world)
+    comm_max = max_over_ranks(comm, world)
+    ms_per_step = ms_max / args.steps
+    value = m * iters * args.steps / (ms_max * 1e-3) / 1e9
+    pk = peaks()
+    peak = float(pk.get("hbm_gbs", 6650.0))
+    sb, gb = layout_bytes(info, "pagerank", args.wide) if info is not None else (0, 0)
+    shard_gbs = (sb + gb) / (comp / iters * 1e-3) / 1e9 if comp > 0 else 0.0
+    sh.close()
+    e2e_line = None
+    if rp_h is not None:
+        # end to end through the public API: host CSR -> shard build (H2D inside) -> iterations -> D2H of the slice
+        times = []
+        for i in range(max(1, min(args.steps, 3)) + 1):
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            s2 = pdist.ShardedPageRank(n, rp_h, col_h, b, device=dev, stream=stream)
+            pr_host = s2.run(0.85, iters).cpu()
+            s2.close()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            if i > 0:
+                times.append(t1 - t0)
+            del s2
+        t = max_over_ranks(statistics.mean(times), world)
+        e2e_line = {"value": round(m * iters / t / 1e9, 3), "unit": "GTEPS",
+                    "h2d_bytes_per_step": int(rp_h.numel() * 8 + col_h.numel() * 4),
+                    "d2h_bytes_per_step": int(pr_host.numel() * 4), "seconds_per_step": round(t, 4),
+                    "includes": "H2D CSR + GPU shard build + iterations (with exchanges) + D2H of the PR slice"}
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "ms_per_iter": round(ms_per_step / iters, 5),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 values, i64 fixed-point accumulation, f64 apply", "data": "synthetic (seeded RMAT/ER, inputs/)",
+        "config": {"workload": WORKLOADS[key], "n": n, "m": m, "iters": iters, "partition_bits": b,
+                   "l2": "inputs larger than L2 (no flush)",
+                   "parallelism": f"destination shards x{world}, NCCL all-gather of SPR + all-reduce of (res, D)"},
+        "phases_ms_per_step_max_over_ranks": {"shard_compute": round(comp_max, 4), "exchange": round(comm_max, 4)},
+        "roofline": {"bound": "hbm", "kernel": "scatter+gather_apply (rank 0 shard)", "achieved": round(shard_gbs, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(shard_gbs / peak, 4), "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if not pk.get("_fallback") else "fallback"},
+        "clocks": clk,
+        "gpu_launches": 2 * iters * args.steps + 2 * args.steps,
+        "e2e": e2e_line,
+    }
+    return line
+
+
 def spmv_phase_times(pcpm, h, x, y, stream):
     import torch
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -459,6 +558,11 @@ def run_reference(args, world, rank, local):
             "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def graphs_op(key):
+    from inputs import graphs
+    return graphs.CONFIGS[key]["op"]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -475,6 +579,9 @@ def main():
     ap.add_argument("--opt", action="append", default=[], help="pcpm_set_option key=value (A/B experiments)")
     ap.add_argument("--no-compress", action="store_true",
                     help="uncompressed bins: one update per edge (the BVGAS-like traffic of Eq. 4)")
+    ap.add_argument("--sharded", action="store_true", help="use the destination-sharded path even at N=1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: run N independent replicas instead of one destination-sharded graph")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
@@ -483,6 +590,8 @@ def main():
         args.config = key
         if args.impl == "reference":
             line = run_reference(args, world, rank, local)
+        elif (world > 1 or args.sharded) and not args.replicas and graphs_op(key) == "pagerank":
+            line = run_sharded(args, world, rank, local)
         else:
             line = run_pcpm(args, world, rank, local)
         if rank == 0 and line is not None:

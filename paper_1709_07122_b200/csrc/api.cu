@@ -106,7 +106,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.b = h->b;
   a.n_dst = h->n_dst;
   a.fbits = fbits;
-  a.outdeg = h->outdeg + h->shard_lo;    // apply: global out-degree of destination v (shards: lo + v)
+  a.inv_deg = h->inv_deg + h->shard_lo;  // apply: 1 / global out-degree of destination v (shards: lo + v)
   a.epi_pf = h->opt_epi_pf;
   return a;
 }
@@ -594,6 +594,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     h->opt_scatter_variant = (int)value;
     free_graph(h);
     return PCPM_OK;
+  }
+  if (!strcmp(key, "scatter_lpt")) {
+    h->opt_scatter_lpt = value ? 1 : 0;
+    free_graph(h);
+    return order_scatter_items(h, h->stream);
   }
   if (!strcmp(key, "scatter_prefetch")) {
     if (value < 0 || value > 64) {

@@ -124,6 +124,14 @@ __global__ void k_png_keys(int64_t ep, const uint32_t* __restrict__ sel, const u
   }
 }
 
+// grp_at[c] = flat group (p*k_dst + j) of PNG entry kPngChunk*c (the sorted group keys)
+__global__ void k_grp_at(int64_t ep, const uint32_t* __restrict__ keys_sorted, int64_t n, uint32_t* grp_at) {
+  GRID_STRIDE(c, n) {
+    const int64_t x = c * kPngChunk;
+    grp_at[c] = keys_sorted[x < ep ? x : ep - 1];
+  }
+}
+
 // png_off[p][j] = G[p*k_dst + j] for j <= k_dst
 __global__ void k_png_off(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, uint32_t* png_off) {
   GRID_STRIDE(i, k_src * (k_dst + 1)) {
@@ -165,7 +173,8 @@ __global__ void k_chunk_counts(int64_t nchunks, const uint32_t* __restrict__ ids
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[nchunks] = 0;
 }
 
-__global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* outdeg,
+// |N_o(u)| and its fp32 reciprocal (0 for dangling u; the apply multiplies by it)
+__global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* outdeg, float* inv_deg,
                          unsigned long long* n_dangling) {
   __shared__ unsigned int s;
   if (threadIdx.x == 0) s = 0;
@@ -174,6 +183,7 @@ __global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_
   GRID_STRIDE(u, n) {
     uint32_t dg = static_cast<uint32_t>(row_ptr[u + 1] - row_ptr[u]);
     outdeg[u] = dg;
+    inv_deg[u] = dg ? 1.0f / (float)dg : 0.0f;
     local += dg == 0;
   }
   atomicAdd(&s, local);
@@ -348,6 +358,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   const int64_t nchunks = h->m_pad / kChunkIds;
   if ((rc = dev_alloc_t(h, &h->chunk_base, nchunks + 1))) return rc;
   if ((rc = dev_alloc_t(h, &h->outdeg, n_src))) return rc;
+  if ((rc = dev_alloc_t(h, &h->inv_deg, n_src + 4))) return rc;
   TK(cudaMemsetAsync(ids32, 0, sizeof(uint32_t) * h->m_pad, s));
   if (h->w) TK(cudaMemsetAsync(h->w, 0, sizeof(float) * h->m_pad, s));
 
@@ -355,7 +366,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   unsigned long long* d_dang;
   TK(tmp.alloc(&d_dang, 1));
   TK(cudaMemsetAsync(d_dang, 0, 8, s));
-  k_outdeg<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, h->outdeg, d_dang);
+  k_outdeg<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, h->outdeg, h->inv_deg, d_dang);
   TK(cudaGetLastError());
 
   uint32_t* G = nullptr;  // flat (p, j) group starts, k_src*k_dst + 1 entries
@@ -443,6 +454,12 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk_s, k_src * k_dst, G);
     k_png16<<<grid_for(ep), kT, 0, s>>>(ep, png32, (uint32_t)(q - 1), h->png16);
     TK(cudaGetLastError());
+    {
+      const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
+      if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;
+      k_grp_at<<<grid_for(nga), kT, 0, s>>>(ep, pk_s, nga, h->grp_at);
+      TK(cudaGetLastError());
+    }
 
     // ---- pull comparison: CSC (in-adjacency), sources ascending per destination
     if (flags & PCPM_BUILD_PULL) {
@@ -477,6 +494,8 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     h->e_prime = 0;
     if (h->wide && (rc = dev_alloc_t(h, &h->png_src, 8))) return rc;
     if ((rc = dev_alloc_t(h, &h->png16, 16))) return rc;
+    if ((rc = dev_alloc_t(h, &h->grp_at, 64))) return rc;
+    TK(cudaMemsetAsync(h->grp_at, 0, 256, s));
     if ((rc = dev_alloc_t(h, &h->upd, 8))) return rc;
     TK(cudaMemsetAsync(h->upd, 0, 32, s));
     TK(cudaMemsetAsync(G, 0, sizeof(uint32_t) * (k_src * k_dst + 1), s));
@@ -578,11 +597,10 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     }
     if (acc > 0) si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)k_dst, (uint32_t)acc});
   }
-  std::stable_sort(si.begin(), si.end(), [](const ScatterItem& a, const ScatterItem& c) { return a.pad > c.pad; });
   h->n_sitems = (int)si.size();
+  h->sitems_host = si;                     // source-partition order (see order_scatter_items)
   if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(si.size(), 1)))) return rc;
-  if (!si.empty())
-    TK(cudaMemcpyAsync(h->sitems, si.data(), sizeof(ScatterItem) * si.size(), cudaMemcpyHostToDevice, s));
+  if ((rc = order_scatter_items(h, s))) return rc;
 
   // ---- iteration scratch (kept zero between uses by the kernels)
   const int64_t nv = std::max(n_src, n_dst);
@@ -603,6 +621,20 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
   TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
+  TK(cudaStreamSynchronize(s));
+  return PCPM_OK;
+}
+
+// Claim order of the scatter items.  Default (opt_scatter_lpt = 0): ascending p, so the
+// ~148 items in flight are consecutive source partitions that write bin j at about the
+// same time -- the boundary sectors between group (p, j) and (p+1, j) are completed in L2
+// instead of being written back partially.  1: largest first (LPT).
+int order_scatter_items(pcpm_handle* h, cudaStream_t s) {
+  std::vector<ScatterItem> si = h->sitems_host;
+  if (h->opt_scatter_lpt)
+    std::stable_sort(si.begin(), si.end(), [](const ScatterItem& a, const ScatterItem& c) { return a.pad > c.pad; });
+  if (!si.empty())
+    TK(cudaMemcpyAsync(h->sitems, si.data(), sizeof(ScatterItem) * si.size(), cudaMemcpyHostToDevice, s));
   TK(cudaStreamSynchronize(s));
   return PCPM_OK;
 }
@@ -689,7 +721,7 @@ int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t 
   unsigned long long* d_dang;
   TK(tmp.alloc(&d_dang, 1));
   TK(cudaMemsetAsync(d_dang, 0, 8, s));
-  k_outdeg<<<grid_for(n), kT, 0, s>>>(n, row_ptr, h->outdeg, d_dang);
+  k_outdeg<<<grid_for(n), kT, 0, s>>>(n, row_ptr, h->outdeg, h->inv_deg, d_dang);
   TK(cudaGetLastError());
   unsigned long long hd = 0;
   TK(cudaMemcpyAsync(&hd, d_dang, 8, cudaMemcpyDeviceToHost, s));

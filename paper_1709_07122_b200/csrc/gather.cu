@@ -27,7 +27,7 @@
 //    fp32 smem atomics are CAS loops on sm_100a).  SpMV uses the signed
 //    ("balanced") variant of the same accumulator.
 //  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
-//    PR'/outdeg; per-item dangling mass and L1 residual, reduced in fixed
+//    fp32(PR') * fp32(1/outdeg) (<= 3 fp32 roundings, R23); per-item dangling mass and L1 residual, reduced in fixed
 //    order by the last CTA.  Split bins flush their low words to a global
 //    u64 partial and the last-arriving slice runs the epilogue.
 #include <type_traits>
@@ -63,11 +63,16 @@ struct Cfg {
   static constexpr bool kHot = kCompact && !W;
   static constexpr bool kBig = kHot && PCPM_GATHER_BIG_TILE;
   static constexpr int kTile = kBig ? 4 * kTileIds : (kHot ? 2 * kTileIds : kTileIds);
-  static constexpr int kStages = kBig ? 2 : ((!kCompact && W) ? 3 : 4);
+  static constexpr int kStages = kBig ? 2 : 4;
+  // Consumer warps form two groups that take alternate stages (group g: stages
+  // g, g+2, ...), so each warp decodes two sub-chunks per stage it sees and the
+  // per-stage bookkeeping is paid once per 2 sub-chunks; both groups run at once.
   static constexpr int kWarps = kHot ? 31 : 16;
   static constexpr int kThreads = 32 * (kWarps + 1);
   static constexpr int kSub = kHot ? kTile / 32 : kTile / 16;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
+  static constexpr int kGroupA = (kWarps + 1) / 2;          // warps of group 0 (stages 0, 2)
+  static constexpr int kGroupB = kWarps - kGroupA;          // warps of group 1 (stages 1, 3)
   static constexpr int kPer = kSub / 32;                   // decode steps of 32 IDs per sub-chunk
   static constexpr int kIdsBytes = kTile * (int)sizeof(IdT);
   static constexpr int kWinCap = kTile + 8;                // >= #flags + 1, 16 B aligned ends
@@ -78,7 +83,7 @@ struct Cfg {
   static constexpr int kFlagShift = kCompact ? 15 : 31;
   static_assert(kTileAlign % kTile == 0, "slices are cut at tile multiples");
   static_assert(kSub % kChunkIds == 0 && kSub % 32 == 0, "sub-chunks start on decode anchors");
-  static_assert(kThreads <= 1024 && kNsc >= kWarps, "launch shape");
+  static_assert(kThreads <= 1024 && kNsc >= kGroupA && kStages % 2 == 0, "launch shape");
   static_assert(kStageBytes % 16 == 0, "bulk copies need 16 B alignment");
 };
 
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::kWarps);
+      mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);   // stage s is consumed by group s & 1
     }
     fence_mbar_init();
   }
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         StageMeta m{};
         m.item = -1;
         m.flags = kFlagStop;
+        push_meta(m);                              // one per consumer group
         push_meta(m);
         break;
       }
@@ -176,6 +182,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         m.item = (int)it;
         m.j = item.j;
         m.flags = kFlagLast | kFlagEmpty;
+        push_meta(m);                              // both groups run the item's epilogue
         push_meta(m);
       } else {
         if constexpr (PR) {
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             const int64_t v0 = (int64_t)item.j << a.b;
             const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
             if (vb) {
-              bulk_prefetch_l2(a.outdeg + v0, vb);
+              bulk_prefetch_l2(a.inv_deg + v0, vb);
               bulk_prefetch_l2(a.pr_old + v0, vb);
             }
           }
@@ -214,7 +221,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               m.hi = min(tb + C::kTile, item.x1);
               m.tile_base = tb;
               m.win_base = alo;
-              m.flags = (t == t1) ? kFlagLast : 0u;
+              // the item's final stage of EACH group is flagged Last: tiles t1 and t1 - 1
+              m.flags = (t + 1 >= t1 + (t1 > t0 ? 0u : 1u)) ? kFlagLast : 0u;
               meta[stage] = m;
               uint8_t* sb = stage_base + stage * C::kStageBytes;
               const uint32_t win_bytes = (ahi - alo) * 4;
@@ -229,6 +237,13 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             if (++stage == S) { stage = 0; phase ^= 1; }
           }
         }
+        if (t1 == t0) {                             // single tile: the other group still needs its Last
+          StageMeta m{};
+          m.item = (int)it;
+          m.j = item.j;
+          m.flags = kFlagLast | kFlagEmpty;
+          push_meta(m);
+        }
       }
       it = it_next;
       item = item_next;
@@ -237,7 +252,10 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   }
 
   // ================= consumers =================
-  const int cw = warp - 1;                  // consumer warp: sub-chunk cw of every tile
+  const int cw = warp - 1;                  // consumer warp
+  const int grp = cw < C::kGroupA ? 0 : 1;  // its group takes stages grp, grp + 2, ...
+  const int gw = grp ? cw - C::kGroupA : cw;
+  const int gsz = grp ? C::kGroupB : C::kGroupA;
   const int ctid = threadIdx.x - 32;        // 0..511
   constexpr int kCons = 32 * C::kWarps;
   const uint32_t qmask = (uint32_t)(q - 1);
@@ -257,7 +275,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   named_bar_sync(1, kCons);
   const uint32_t lemask = lanemask_le();
 
-  int stage = 0, rot = 0;
+  int stage = grp, rot = 0;
   uint32_t phase = 0;
   for (;;) {
     mbar_wait(&full[stage], phase);
@@ -270,8 +288,6 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
       const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
       const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
-      // sub-chunk sc of the tile: warp cw takes sc = cw; the kNsc - kWarps extra
-      // sub-chunks rotate over the warps from stage to stage
       auto process = [&](const int sc) {
       const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
       if (xs < m.hi && xs + C::kSub > m.lo) {
@@ -366,16 +382,21 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         else body(std::false_type{});
       }
       };
-      process(cw);
-      if constexpr (C::kNsc > C::kWarps) {
-        for (int e = 0; e < C::kNsc - C::kWarps; ++e)
-          if (cw == (rot + e) % C::kWarps) process(C::kWarps + e);
+      // sub-chunks gw, gw + gsz, ... of the stage; the remaining kNsc mod gsz
+      // sub-chunks rotate over the group's warps from stage to stage
+      const int nmain = (C::kNsc / gsz) * gsz;
+      for (int sc = gw; sc < nmain; sc += gsz) process(sc);
+      int who = rot;
+      for (int sc = nmain; sc < C::kNsc; ++sc) {
+        if (gw == who) process(sc);
+        who = (who + 1 == gsz) ? 0 : who + 1;
       }
+      rot = who;
     }
-    if constexpr (C::kNsc > C::kWarps) rot = (rot + 1 == C::kWarps) ? 0 : rot + 1;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
-    if (++stage == S) { stage = 0; phase ^= 1; }
+    stage += 2;
+    if (stage >= S) { stage -= S; phase ^= 1; }
 
     if (m.flags & kFlagLast) {
       // ---------------- epilogue of this item ----------------
@@ -427,25 +448,25 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       if (run_apply) {
         if constexpr (PR) {
           const bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
-                           aligned16(a.spr_new + v0) && aligned16(a.outdeg + v0);
+                           aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0);
           if (vec) {
-            const uint4* dg4 = reinterpret_cast<const uint4*>(a.outdeg + v0);
+            const float4* id4 = reinterpret_cast<const float4*>(a.inv_deg + v0);
             const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
             float4* pn4 = reinterpret_cast<float4*>(a.pr_new + v0);
             float4* sp4 = reinterpret_cast<float4*>(a.spr_new + v0);
 #pragma unroll 1
             for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
-              const uint4 dg = __ldg(dg4 + i4);
+              const float4 idg = __ldg(id4 + i4);
               const float4 po = __ldg(po4 + i4);
-              const uint32_t dgv[4] = {dg.x, dg.y, dg.z, dg.w};
+              const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
               const float pov[4] = {po.x, po.y, po.z, po.w};
               float pn[4], sp[4];
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
                 const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
                 pn[c] = (float)prn;
-                sp[c] = dgv[c] ? (float)(prn / (double)dgv[c]) : 0.0f;
-                dang += dgv[c] ? 0.0 : prn;
+                sp[c] = pn[c] * idv[c];                 // SPR = PR / |N_o| (fp32; 0 if dangling)
+                dang += idv[c] != 0.0f ? 0.0 : prn;
                 res += fabs(prn - (double)pov[c]);
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
@@ -456,9 +477,9 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               const uint32_t v = v0 + (uint32_t)i;
               const double prn = base_pr + a.d * ((double)(long long)total(i) * inv_scale);
               a.pr_new[v] = (float)prn;
-              const uint32_t dg = __ldg(a.outdeg + v);
-              a.spr_new[v] = dg ? (float)(prn / (double)dg) : 0.0f;
-              if (dg == 0) dang += prn;
+              const float idg = __ldg(a.inv_deg + v);
+              a.spr_new[v] = (float)prn * idg;
+              if (idg == 0.0f) dang += prn;
               res += fabs(prn - (double)a.pr_old[v]);
             }
           }

@@ -25,6 +25,7 @@ constexpr int kChunkIds = 128;                         // chunk_base granularity
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
+constexpr int kPngChunk = 256;                         // grp_at granularity (scatter warp sub-ranges)
 
 struct GatherItem {        // one slice [x0, x1) of destination bin j
   uint32_t j, x0, x1;
@@ -75,11 +76,13 @@ struct pcpm_handle {
   uint32_t* png_src = nullptr;      // [E' (+pad)] 4-byte PNG sources (wide handles only)
   uint16_t* png16 = nullptr;        // [E' (+pad)] compact PNG sources: u & (q-1)
   uint32_t* png_off = nullptr;      // [k_src*(k_dst+1)]
+  uint32_t* grp_at = nullptr;       // [E'/kPngChunk + 8] flat group p*k_dst + j of PNG entry kPngChunk*c
   uint32_t* upd_off = nullptr;      // [k_src*k_dst]
   uint32_t* bin_id_start = nullptr; // [k_dst+1]
   uint32_t* bin_upd_start = nullptr;// [k_dst+1]
   uint32_t* chunk_base = nullptr;   // [m_pad/kChunkIds + 1]
   uint32_t* outdeg = nullptr;       // [n_src]
+  float* inv_deg = nullptr;         // [n_src] 1/|N_o(u)| (0 for dangling u), read by the apply
   float* upd = nullptr;             // [E' + 8]
   int wexp = 0;                     // max|w| <= 2^wexp (SpMV fixed-point scale)
   float* xmax = nullptr;            // [1] device max|x| of the last pcpm_spmv
@@ -95,6 +98,7 @@ struct pcpm_handle {
   uint32_t* bin_nslices = nullptr;  // [k_dst]
   pcpm::ScatterItem* sitems = nullptr;
   int n_sitems = 0;
+  std::vector<pcpm::ScatterItem> sitems_host;
 
   // iteration state
   float* pr[2] = {nullptr, nullptr};// [n]
@@ -112,10 +116,10 @@ struct pcpm_handle {
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
-  int opt_gather_pf = 8;            // gather: tiles prefetched into L2 ahead of the smem ring
-  int opt_epi_pf = 0;
+  int opt_epi_pf = 0;               // gather: prefetch the apply's vertex arrays into L2 at item claim
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
-  int opt_scatter_pf = 4;           // scatter: PNG stages prefetched into L2 ahead of the ring               // gather: prefetch the apply's vertex arrays into L2 at item claim
+  int opt_scatter_lpt = 0;          // scatter claim order: 0 ascending p, 1 largest first
+  int opt_scatter_pf = 0;           // scatter: PNG stages prefetched into L2 ahead of the ring
   int opt_phase_timing = 0;
   std::vector<cudaEvent_t> events;  // phase-timing events (created on demand)
   int n_events_used = 0;
@@ -228,7 +232,7 @@ struct GatherArgs {
   const double* red_in;    // D_t at red_in[0]
   double* res_out;         // L1 residual of this iteration
   double* dang_out;        // dangling mass of the new vector (D_{t+1})
-  const uint32_t* outdeg;
+  const float* inv_deg;    // 1/outdeg of the destinations (0 = dangling)
   const float* pr_old;
   float* pr_new;
   float* spr_new;
@@ -250,6 +254,7 @@ int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
                           float* spr_out, double* red_t, float d, cudaStream_t s);
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);
+int order_scatter_items(pcpm_handle* h, cudaStream_t s);
 int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags);
 int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, cudaStream_t s);
 

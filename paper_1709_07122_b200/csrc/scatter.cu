@@ -33,7 +33,7 @@ namespace {
 // ------------------------------------------------------------------ TMA variant
 constexpr int kScW = 16;                           // consumer warps
 constexpr int kScThreads = 32 * (kScW + 1);
-constexpr int kScStages = 3;
+constexpr int kScStages = 5;
 constexpr int kScStageBytes = 16384;               // PNG bytes per stage
 constexpr int kScOffCap = kScatterMaxGroups + 8;   // offsets of one item (+ alignment slack)
 
@@ -45,10 +45,13 @@ struct ScItemMeta {
   uint32_t pad[2];
 };
 struct ScStageMeta {
-  uint32_t base;         // PNG position of stage element 0 (16 B aligned)
+  uint32_t base;         // PNG position of stage element 0 (a multiple of kPngChunk)
   uint32_t lo, hi;       // valid PNG positions [lo, hi)
   uint32_t last;         // last stage of the item
+  uint32_t gshift;       // grp_at[base / kPngChunk] is at stage_grp[gshift]
+  uint32_t pad[3];
 };
+constexpr int kScGrpCap = kScStageBytes / 2 / kPngChunk + 8;   // grp_at entries per stage (+ alignment)
 
 struct ScatterArgs {
   const ScatterItem* items;
@@ -60,6 +63,7 @@ struct ScatterArgs {
   const void* png;
   const uint32_t* png_off;
   const uint32_t* upd_off;
+  const uint32_t* grp_at;
   float* upd;
   uint32_t* counters;    // [2] item counter, [3] done counter (kept zero)
   int pf_stages;         // L2 prefetch distance in stages
@@ -69,14 +73,16 @@ template <typename SrcT>
 __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs a) {
   constexpr int kChunk = kScStageBytes / (int)sizeof(SrcT);   // PNG entries per stage
   constexpr int kSub = kChunk / kScW;                           // entries per consumer warp
-  constexpr uint32_t kAlignE = 16 / sizeof(SrcT);               // entries per 16 B
+  constexpr uint32_t kAlignE = kPngChunk;                       // stage bases: multiples of kPngChunk
+  static_assert(kSub % kPngChunk == 0, "warp sub-ranges start on grp_at anchors");
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t q = int64_t(1) << a.b;
   float* xs = reinterpret_cast<float*>(smem);                                        // q floats
   uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + ((q * 4 + 127) & ~int64_t(127)));
   uint32_t* uo_s = off_s + kScOffCap;
   uint8_t* ring = reinterpret_cast<uint8_t*>(uo_s + kScOffCap);
-  ScStageMeta* smeta = reinterpret_cast<ScStageMeta*>(ring + kScStages * kScStageBytes);
+  uint32_t* grp_s = reinterpret_cast<uint32_t*>(ring + kScStages * kScStageBytes);       // [kScStages][kScGrpCap]
+  ScStageMeta* smeta = reinterpret_cast<ScStageMeta*>(grp_s + kScStages * kScGrpCap);
   ScItemMeta* imeta = reinterpret_cast<ScItemMeta*>(smeta + kScStages);
   uint64_t* full = reinterpret_cast<uint64_t*>(imeta + 1);
   uint64_t* empty = full + kScStages;
@@ -139,10 +145,14 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
           sm.lo = max(c, s0);
           sm.hi = min(c + (uint32_t)kChunk, s1);
           sm.last = (c + (uint32_t)kChunk >= s1) ? 1u : 0u;
+          const uint32_t c0 = c / kPngChunk, ca = c0 & ~3u;
+          const uint32_t nga = (((sm.hi - c + kPngChunk - 1) / kPngChunk) + (c0 - ca) + 3) & ~3u;
+          sm.gshift = c0 - ca;
           smeta[stage] = sm;
           const uint32_t bytes = (((sm.hi - c) * (uint32_t)sizeof(SrcT)) + 15) & ~15u;   // png is padded
-          mbar_arrive_expect_tx(&full[stage], bytes);
+          mbar_arrive_expect_tx(&full[stage], bytes + nga * 4);
           bulk_g2s(ring + stage * kScStageBytes, png + c, bytes, &full[stage], pol_stream);
+          bulk_g2s(grp_s + stage * kScGrpCap, a.grp_at + ca, nga * 4, &full[stage], pol_stream);   // grp_at padded
           if (++stage == kScStages) { stage = 0; phase ^= 1; }
         };
         if (!stop) {
@@ -204,22 +214,25 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
         const uint32_t wb = sm.base + (uint32_t)(cw * kSub);
         const uint32_t wlo = max(wb, sm.lo), whi = min(wb + (uint32_t)kSub, sm.hi);
         if (wlo < whi) {
-          // group of the warp's first entry: largest g with offs[g] <= wlo (broadcast search)
-          uint32_t lo = 0, hi = im.ng;                 // offs[lo] <= wlo < offs[hi]
-          while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (offs[mid] <= wlo) lo = mid; else hi = mid;
-          }
-          uint32_t g = lo;
+          // group of the warp's first entry from the precomputed grp_at anchor of its
+          // sub-range (flat group p*k_dst + j), then advanced per lane as e crosses
+          // group ends; (gend, delta) stay in registers between crossings
+          const int32_t ga = (int32_t)(grp_s[stage * kScGrpCap + sm.gshift + (wb - sm.base) / kPngChunk] -
+                                       (im.p * (uint32_t)a.k_dst + im.j0));
+          uint32_t g = ga > 0 ? (uint32_t)ga : 0u;
           uint32_t gend = offs[g + 1];
+          uint32_t delta = uos[g] - offs[g];                 // dst = e + delta within group g
 #pragma unroll 4
           for (uint32_t e = wlo + lane; e < whi; e += 32) {
-            while (e >= gend) {                          // cross (possibly empty) groups
-              ++g;
-              gend = offs[g + 1];
+            if (e >= gend) {
+              do {
+                ++g;
+                gend = offs[g + 1];
+              } while (e >= gend);
+              delta = uos[g] - offs[g];
             }
             const uint32_t u = (uint32_t)ps[e - sm.base] - ubase;
-            a.upd[uos[g] + (e - offs[g])] = xs[u];
+            a.upd[e + delta] = xs[u];
           }
         }
         __syncwarp();
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
 int scatter_tma_smem_bytes(int b) {
   const int64_t q = int64_t(1) << b;
   return (int)(((q * 4 + 127) & ~int64_t(127)) + 2 * kScOffCap * 4 + kScStages * kScStageBytes +
-               kScStages * sizeof(ScStageMeta) + sizeof(ScItemMeta) + (2 * kScStages + 2) * 8 + 16);
+               kScStages * kScGrpCap * 4 + kScStages * sizeof(ScStageMeta) + sizeof(ScItemMeta) + (2 * kScStages + 2) * 8 + 16);
 }
 
 // ------------------------------------------------------------------ warp-per-group variant
@@ -360,6 +373,7 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
     a.png = h->wide ? static_cast<const void*>(h->png_src) : static_cast<const void*>(h->png16);
     a.png_off = h->png_off;
     a.upd_off = h->upd_off;
+    a.grp_at = h->grp_at;
     a.upd = h->upd;
     a.counters = h->counters;
     a.pf_stages = h->opt_scatter_pf;

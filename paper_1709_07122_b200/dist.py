@@ -56,7 +56,7 @@ class ShardedPageRank:
     column slice of this rank is kept on its device after the build).
     """
 
-    def __init__(self, n, row_ptr, col, b, group=None, device=None, stream=None, step_impl=None):
+    def __init__(self, n, row_ptr, col, b, group=None, device=None, stream=None, step_impl=None, timing=False):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
@@ -81,6 +81,23 @@ class ShardedPageRank:
         self.red = torch.zeros(2, dtype=torch.float64, device=device)     # residual, dangling mass
         self.D = torch.zeros(1, dtype=torch.float64, device=device)
         self.residuals = []
+        self.timing = timing and step_impl is None
+        self.events = []          # per iteration: (before step, after step, after exchange)
+
+    def info(self):
+        return self.pcpm.pcpm_get_info(self.h) if self.h is not None else None
+
+    def phase_ms(self):
+        """(compute ms, exchange ms) summed over the iterations of the last run (device events)."""
+        self.torch.cuda.synchronize()
+        comp = sum(a.elapsed_time(b) for a, b, _ in self.events)
+        comm = sum(b.elapsed_time(c) for _, b, c in self.events)
+        return comp, comm
+
+    def _event(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
 
     def close(self):
         if self.h is not None:
@@ -113,17 +130,24 @@ class ShardedPageRank:
         self.D.copy_(self.red[1:])
         self._allreduce(self.D)
         self.residuals = []
+        self.events = []
         for t in range(iters):
             cur, nxt = t & 1, (t + 1) & 1
             self.red.zero_()
+            ev = [self._event()] if self.timing else None
             if n_loc > 0:
                 args = (d, self.spr[cur], self.D, self.pr[cur], self.pr[nxt], self._chunk(self.spr[nxt]), self.red)
                 if self.step_impl is None:
                     self.pcpm.pcpm_shard_step(self.h, *args)
                 else:
                     self.step_impl.step(self, *args)
+            if ev:
+                ev.append(self._event())
             self._allgather(self.spr[nxt])                 # SPR_{t+1} of all vertices
             self._allreduce(self.red)                       # global residual and D_{t+1}
+            if ev:
+                ev.append(self._event())
+                self.events.append(tuple(ev))
             self.D.copy_(self.red[1:])
             self.residuals.append(self.red[0].clone())
         return self.pr[iters & 1][:n_loc]
