@@ -108,6 +108,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.fbits = fbits;
   a.inv_deg = h->inv_deg + h->shard_lo;  // apply: 1 / global out-degree of destination v (shards: lo + v)
   a.epi_pf = h->opt_epi_pf;
+  a.pf_tiles = h->opt_gather_pf;
   return a;
 }
 
@@ -133,7 +134,7 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
   h->last_was_spmv = false;
   h->n_events_used = 0;
   if ((rc = mark(h, s))) return rc;
-  if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, s))) return rc;
+  if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0, fbits), s))) return rc;
   if ((rc = mark(h, s))) return rc;
   if (iters == 0) {
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
@@ -162,7 +163,7 @@ int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s)
   float* sprb[2] = {h->spr, h->xbuf};
   h->n_events_used = 0;
   if ((rc = mark(h, s))) return rc;
-  if ((rc = launch_pr_init(h, h->pr[0], sprb[0], h->red, h->red_cap, s))) return rc;
+  if ((rc = launch_pr_init(h, h->pr[0], sprb[0], h->red, h->red_cap, 1.0, s))) return rc;
   if ((rc = mark(h, s))) return rc;
   if (iters == 0) {
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
@@ -368,7 +369,7 @@ int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0) {
     return PCPM_EINVAL;
   }
   h->launches = 0;
-  return launch_pr_init_slice(h, pr0, spr0, dang0, h->stream);
+  return launch_pr_init_slice(h, pr0, spr0, dang0, std::ldexp(1.0, pr_fixed_bits(h->n_global)), h->stream);
 }
 
 int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
@@ -592,6 +593,15 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
       return PCPM_EINVAL;
     }
     h->opt_scatter_variant = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "gather_prefetch")) {
+    if (value < 0 || value > 16) {
+      set_error(PCPM_EINVAL, "gather_prefetch must be in [0, 16]");
+      return PCPM_EINVAL;
+    }
+    h->opt_gather_pf = (int)value;
     free_graph(h);
     return PCPM_OK;
   }

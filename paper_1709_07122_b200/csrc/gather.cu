@@ -205,9 +205,22 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             fb = (tl == t1) ? item.fx1 : __ldg(a.chunk_base + (tb + C::kTile) / kChunkIds);
           }
           const uint32_t nb = min(32u, t1 - tb0 + 1);
+          const uint32_t pf = (uint32_t)a.pf_tiles;
+          // L2 prefetch of the batch's first pf tiles (the ring then loads them from L2)
+          if (pf && lane < nb && lane < pf) {
+            const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
+            bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
+            if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+          }
           for (uint32_t k = 0; k < nb; ++k) {
             const uint32_t flo = __shfl_sync(0xffffffffu, fa, k);
             const uint32_t fhi = __shfl_sync(0xffffffffu, fb, k);
+            // keep the L2 prefetch pf tiles ahead of the ring (within the batch)
+            if (pf && lane == k + pf && lane < nb) {
+              const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
+              bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
+              if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+            }
             if (lane == 0) {
               const uint32_t t = tb0 + k;
               const uint32_t tb = t * C::kTile;
@@ -315,11 +328,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             val[c] = ok[c] ? win_s[ptr] : 0.0f;
           }
           if constexpr (PR) {
-            // PageRank: SPR >= 0, val * 2^F is exact in fp32; round to the u64 grid
+            // PageRank: the apply stores SPR * 2^F (a power-of-two scaling, exact in fp32),
+            // so one conversion rounds each term to the 2^-F grid
             uint32_t tlo[P], thi[P], old[P];
 #pragma unroll
             for (int c = 0; c < P; ++c) {
-              const unsigned long long T = __float2ull_rn(val[c] * fscale);
+              const unsigned long long T = __float2ull_rn(val[c]);   // SPR is stored as SPR * 2^F
               tlo[c] = (uint32_t)T;
               thi[c] = (uint32_t)(T >> 32);
             }
@@ -454,23 +468,39 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
             float4* pn4 = reinterpret_cast<float4*>(a.pr_new + v0);
             float4* sp4 = reinterpret_cast<float4*>(a.spr_new + v0);
+            // loads of 4 float4 groups first (more bytes in flight per thread), then the math
+            const int64_t n4 = cnt / 4;
+            constexpr int kU = 4;
 #pragma unroll 1
-            for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
-              const float4 idg = __ldg(id4 + i4);
-              const float4 po = __ldg(po4 + i4);
-              const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
-              const float pov[4] = {po.x, po.y, po.z, po.w};
-              float pn[4], sp[4];
+            for (int64_t b4 = ctid; b4 < n4; b4 += kU * kCons) {
+              float4 idg[kU], po[kU];
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
-                pn[c] = (float)prn;
-                sp[c] = pn[c] * idv[c];                 // SPR = PR / |N_o| (fp32; 0 if dangling)
-                dang += idv[c] != 0.0f ? 0.0 : prn;
-                res += fabs(prn - (double)pov[c]);
+              for (int u = 0; u < kU; ++u) {
+                const int64_t i4 = b4 + u * kCons;
+                if (i4 < n4) {
+                  idg[u] = __ldg(id4 + i4);
+                  po[u] = __ldg(po4 + i4);
+                }
               }
-              pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
-              sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
+#pragma unroll
+              for (int u = 0; u < kU; ++u) {
+                const int64_t i4 = b4 + u * kCons;
+                if (i4 < n4) {
+                  const float idv[4] = {idg[u].x, idg[u].y, idg[u].z, idg[u].w};
+                  const float pov[4] = {po[u].x, po[u].y, po[u].z, po[u].w};
+                  float pn[4], sp[4];
+#pragma unroll
+                  for (int c = 0; c < 4; ++c) {
+                    const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
+                    pn[c] = (float)prn;
+                    sp[c] = pn[c] * idv[c] * fscale;    // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
+                    dang += idv[c] != 0.0f ? 0.0 : prn;
+                    res += fabs(prn - (double)pov[c]);
+                  }
+                  pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
+                  sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
+                }
+              }
             }
           } else {
             for (int64_t i = ctid; i < cnt; i += kCons) {
@@ -478,7 +508,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               const double prn = base_pr + a.d * ((double)(long long)total(i) * inv_scale);
               a.pr_new[v] = (float)prn;
               const float idg = __ldg(a.inv_deg + v);
-              a.spr_new[v] = (float)prn * idg;
+              a.spr_new[v] = (float)prn * idg * fscale;
               if (idg == 0.0f) dang += prn;
               res += fabs(prn - (double)a.pr_old[v]);
             }

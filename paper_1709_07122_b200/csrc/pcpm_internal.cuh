@@ -116,6 +116,7 @@ struct pcpm_handle {
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
+  int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
   int opt_epi_pf = 0;               // gather: prefetch the apply's vertex arrays into L2 at item claim
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
   int opt_scatter_lpt = 0;          // scatter claim order: 0 ascending p, 1 largest first
@@ -240,6 +241,7 @@ struct GatherArgs {
   float* y;
   const float* xmax;       // device max|x| of this call (fixed-point scale)
   int wexp;                // max|w| <= 2^wexp
+  int pf_tiles;            // L2 prefetch distance of the gather producer, in tiles
   int epi_pf;              // prefetch outdeg / pr_old of the item's partition into L2
 };
 __device__ int spmv_fbits(float xmax, int wexp);
@@ -250,12 +252,12 @@ int gather_smem_bytes(int b, bool wide, bool weighted);
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
 int prepare_gather(pcpm_handle* h);
 int prepare_scatter(pcpm_handle* h);
-int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, cudaStream_t s);
+int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, double spr_scale, cudaStream_t s);
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
                           float* spr_out, double* red_t, float d, cudaStream_t s);
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);
 int order_scatter_items(pcpm_handle* h, cudaStream_t s);
 int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags);
-int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, cudaStream_t s);
+int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, double spr_scale, cudaStream_t s);
 
 }  // namespace pcpm

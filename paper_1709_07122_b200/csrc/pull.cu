@@ -7,13 +7,15 @@
 namespace pcpm {
 namespace {
 
+// spr_scale: 2^F for the PCPM path (the gather converts SPR * 2^F straight to its
+// fixed-point grid, R21), 1 for the pull comparison.
 __global__ void k_pr_init(int64_t n, const uint32_t* __restrict__ outdeg, int64_t n_dangling, float* pr0,
-                          float* spr, double* red, int red_n) {
+                          float* spr, double* red, int red_n, double spr_scale) {
   const double inv_n = 1.0 / (double)n;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     pr0[v] = (float)inv_n;
     const uint32_t dg = outdeg[v];
-    spr[v] = dg ? (float)(inv_n / (double)dg) : 0.0f;
+    spr[v] = dg ? (float)(inv_n / (double)dg * spr_scale) : 0.0f;
   }
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < red_n; i += blockDim.x) red[i] = 0.0;
@@ -25,13 +27,13 @@ __global__ void k_pr_init(int64_t n, const uint32_t* __restrict__ outdeg, int64_
 // PR_0 = 1/n_global on a destination shard's slice (R2), SPR_0 = PR_0 / outdeg, and the
 // slice's dangling count; k_dang0 turns the count into D_0's share (exact: count / n).
 __global__ void k_pr_init_slice(int64_t n_local, const uint32_t* __restrict__ outdeg, double inv_n, float* pr0,
-                                float* spr, unsigned long long* cnt) {
+                                float* spr, unsigned long long* cnt, double spr_scale) {
   unsigned long long local = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n_local;
        v += (int64_t)gridDim.x * blockDim.x) {
     pr0[v] = (float)inv_n;
     const uint32_t dg = outdeg[v];
-    spr[v] = dg ? (float)(inv_n / (double)dg) : 0.0f;
+    spr[v] = dg ? (float)(inv_n / (double)dg * spr_scale) : 0.0f;
     local += dg == 0;
   }
   for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
@@ -72,21 +74,22 @@ __global__ void __launch_bounds__(256) k_pull(int64_t n, const uint32_t* __restr
 
 }  // namespace
 
-int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, cudaStream_t s) {
+int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, double spr_scale, cudaStream_t s) {
   int grid = (int)std::min<int64_t>((h->n_src + 255) / 256, h->num_sms * 8);
-  k_pr_init<<<std::max(grid, 1), 256, 0, s>>>(h->n_src, h->outdeg, h->n_dangling, pr0, spr, red, red_n);
+  k_pr_init<<<std::max(grid, 1), 256, 0, s>>>(h->n_src, h->outdeg, h->n_dangling, pr0, spr, red, red_n,
+                                                  spr_scale);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return PCPM_OK;
 }
 
-int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, cudaStream_t s) {
+int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, double spr_scale, cudaStream_t s) {
   const int64_t n_local = h->n_dst;
   const double inv_n = 1.0 / (double)h->n_global;
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(h->counters + 4);   // [4..5] scratch
   PCPM_CK(cudaMemsetAsync(cnt, 0, 8, s));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_local + 255) / 256, h->num_sms * 8));
-  k_pr_init_slice<<<grid, 256, 0, s>>>(n_local, h->outdeg + h->shard_lo, inv_n, pr0, spr, cnt);
+  k_pr_init_slice<<<grid, 256, 0, s>>>(n_local, h->outdeg + h->shard_lo, inv_n, pr0, spr, cnt, spr_scale);
   PCPM_CK(cudaGetLastError());
   k_dang0<<<1, 1, 0, s>>>(cnt, inv_n, dang0);
   PCPM_CK(cudaGetLastError());
