@@ -100,7 +100,8 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.bin_nslices = h->bin_nslices;
   a.counters = h->counters;
   a.bin_arrive = h->bin_arrive;
-  a.part = h->part;
+  a.slot_buf = h->slot_buf;
+  a.bin_slot_base = h->bin_slot_base;
   a.hi = h->hi;
   a.item_red = h->item_red;
   a.b = h->b;

@@ -551,7 +551,8 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   // item exceeds ~m / (2 SMs) IDs; largest first (LPT, the GPU analogue of the
   // paper's dynamic scheduling).
   std::vector<GatherItem> gi;
-  std::vector<uint32_t> nsl(k_dst, 0);
+  std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
+  uint32_t nslots = 0;
   int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (2 * h->num_sms)) / kTileAlign + 1) * kTileAlign);
   for (int64_t j = 0; j < k_dst; ++j) {
     int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
@@ -563,14 +564,19 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       if (c > cuts.back() && c < s1) cuts.push_back(c);
     }
     cuts.push_back(s1);
+    const uint32_t ns = (uint32_t)(cuts.size() - 1);
+    // slices of a split bin each own a slot: a q-word buffer for their low words
+    sbase[j] = ns > 1 ? nslots : 0u;
     for (size_t i = 0; i + 1 < cuts.size(); ++i) {
       GatherItem it{};
       it.j = (uint32_t)j;
       it.x0 = (uint32_t)cuts[i];
       it.x1 = (uint32_t)cuts[i + 1];
+      it.pad[0] = ns > 1 ? nslots + (uint32_t)i : 0xFFFFFFFFu;
       gi.push_back(it);
     }
-    nsl[j] = (uint32_t)(cuts.size() - 1);
+    nsl[j] = ns;
+    if (ns > 1) nslots += ns;
   }
   std::stable_sort(gi.begin(), gi.end(),
                    [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
@@ -579,6 +585,10 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
   TK(cudaMemcpyAsync(h->gitems, gi.data(), sizeof(GatherItem) * gi.size(), cudaMemcpyHostToDevice, s));
   TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_dst))) return rc;
+  TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  h->n_slots = nslots;
+  if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
   TK(cudaGetLastError());
 
@@ -609,13 +619,11 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->spr, n_src + 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->xbuf, n_src + 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->part, n_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
   if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
-  TK(cudaMemsetAsync(h->part, 0, sizeof(uint64_t) * n_dst, s));
   TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
   TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
   TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));

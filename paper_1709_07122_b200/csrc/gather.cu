@@ -28,8 +28,8 @@
 //    ("balanced") variant of the same accumulator.
 //  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
 //    fp32(PR') * fp32(1/outdeg) (<= 3 fp32 roundings, R23); per-item dangling mass and L1 residual, reduced in fixed
-//    order by the last CTA.  Split bins flush their low words to a global
-//    u64 partial and the last-arriving slice runs the epilogue.
+//    order by the last CTA.  Slices of split bins store their low words to a
+//    slot buffer and the last-arriving slice sums the slots and runs the epilogue.
 #include <type_traits>
 
 #include "pcpm_internal.cuh"
@@ -419,13 +419,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       const uint32_t nsl = a.bin_nslices[m.j];
       bool run_apply = true;
       if (nsl > 1) {
+        // a slice of a split bin: store its low words to its slot (coalesced plain stores);
+        // the last slice to arrive sums the bin's slots
+        uint32_t* sbuf = a.slot_buf + (size_t)a.items[m.item].pad[0] * (size_t)q;
         for (int64_t i = ctid; i < q; i += kCons) {
-          const uint32_t lo = acc[i];
-          if (lo) {
-            // PageRank: unsigned low word; SpMV: balanced (signed) low word, sign-extended
-            const unsigned long long add = PR ? (unsigned long long)lo : (unsigned long long)(long long)(int32_t)lo;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&a.part[v0 + i]), add);
-          }
+          __stcg(sbuf + i, acc[i]);
           acc[i] = 0u;
         }
         __threadfence();
@@ -445,8 +443,13 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         const uint32_t v = v0 + (uint32_t)i;
         uint64_t tot;
         if (nsl > 1) {
-          tot = ldcg_u64(&a.part[v]) + ((uint64_t)ldcg_u32(&a.hi[v]) << 32);
-          a.part[v] = 0ull;
+          // PageRank: unsigned low words; SpMV: balanced (signed) low words, sign-extended
+          const uint32_t* sb = a.slot_buf + (size_t)a.bin_slot_base[m.j] * (size_t)q + i;
+          tot = (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+          for (uint32_t sl = 0; sl < nsl; ++sl) {
+            const uint32_t w = ldcg_u32(sb + (size_t)sl * (size_t)q);
+            tot += PR ? (uint64_t)w : (uint64_t)(long long)(int32_t)w;
+          }
           a.hi[v] = 0u;
         } else {
           tot = PR ? (uint64_t)acc[i] : (uint64_t)(long long)(int32_t)acc[i];
@@ -468,39 +471,25 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
             float4* pn4 = reinterpret_cast<float4*>(a.pr_new + v0);
             float4* sp4 = reinterpret_cast<float4*>(a.spr_new + v0);
-            // loads of 4 float4 groups first (more bytes in flight per thread), then the math
-            const int64_t n4 = cnt / 4;
-            constexpr int kU = 4;
+            // (batching the loads of several float4 groups per thread measured slower:
+            // the extra registers cost the decode loop more than the epilogue gains)
 #pragma unroll 1
-            for (int64_t b4 = ctid; b4 < n4; b4 += kU * kCons) {
-              float4 idg[kU], po[kU];
+            for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
+              const float4 idg = __ldg(id4 + i4);
+              const float4 po = __ldg(po4 + i4);
+              const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
+              const float pov[4] = {po.x, po.y, po.z, po.w};
+              float pn[4], sp[4];
 #pragma unroll
-              for (int u = 0; u < kU; ++u) {
-                const int64_t i4 = b4 + u * kCons;
-                if (i4 < n4) {
-                  idg[u] = __ldg(id4 + i4);
-                  po[u] = __ldg(po4 + i4);
-                }
+              for (int c = 0; c < 4; ++c) {
+                const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
+                pn[c] = (float)prn;
+                sp[c] = pn[c] * idv[c] * fscale;        // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
+                dang += idv[c] != 0.0f ? 0.0 : prn;
+                res += fabs(prn - (double)pov[c]);
               }
-#pragma unroll
-              for (int u = 0; u < kU; ++u) {
-                const int64_t i4 = b4 + u * kCons;
-                if (i4 < n4) {
-                  const float idv[4] = {idg[u].x, idg[u].y, idg[u].z, idg[u].w};
-                  const float pov[4] = {po[u].x, po[u].y, po[u].z, po[u].w};
-                  float pn[4], sp[4];
-#pragma unroll
-                  for (int c = 0; c < 4; ++c) {
-                    const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
-                    pn[c] = (float)prn;
-                    sp[c] = pn[c] * idv[c] * fscale;    // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
-                    dang += idv[c] != 0.0f ? 0.0 : prn;
-                    res += fabs(prn - (double)pov[c]);
-                  }
-                  pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
-                  sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
-                }
-              }
+              pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
+              sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
             }
           } else {
             for (int64_t i = ctid; i < cnt; i += kCons) {

@@ -30,7 +30,7 @@ constexpr int kPngChunk = 256;                         // grp_at granularity (sc
 struct GatherItem {        // one slice [x0, x1) of destination bin j
   uint32_t j, x0, x1;
   uint32_t fx0, fx1;       // #flags in ids[0..x0), ids[0..x1)  (global decode identity)
-  uint32_t pad[3];
+  uint32_t pad[3];         // pad[0]: slot of a split bin's slice (0xFFFFFFFF if the bin is whole)
 };
 static_assert(sizeof(GatherItem) == 32, "GatherItem is 32 B");
 
@@ -105,7 +105,9 @@ struct pcpm_handle {
   float* spr = nullptr;             // [n_src (+pad)]
   float* xbuf = nullptr;            // [n_src (+pad)] staging for host x
   float* ybuf = nullptr;            // [n_dst]      staging for host y / out
-  uint64_t* part = nullptr;         // [n_dst] split-bin partial sums (kept zero between uses)
+  uint32_t* slot_buf = nullptr;     // [n_slots * q] low words of the slices of split bins
+  uint32_t* bin_slot_base = nullptr;// [k_dst] first slot of bin j's slices
+  uint32_t n_slots = 0;
   uint32_t* hi = nullptr;           // [n_dst] fixed-point carry words (kept zero)
   uint32_t* bin_arrive = nullptr;   // [k_dst]
   uint32_t* counters = nullptr;     // [4] work counter, done counter (kept zero)
@@ -222,7 +224,8 @@ struct GatherArgs {
   const uint32_t* bin_nslices;
   uint32_t* counters;      // [0] work, [1] done
   uint32_t* bin_arrive;
-  uint64_t* part;
+  uint32_t* slot_buf;      // split bins: slice s of bin j writes its low words to slot_buf[(base_j + s) q ..]
+  const uint32_t* bin_slot_base;
   uint32_t* hi;
   double* item_red;        // [2*n_items]
   int b;
