@@ -161,7 +161,7 @@ def run_pcpm(args, world, rank, local):
     cfg = g.meta
     op = cfg["op"]
     iters = args.iters or cfg["iters"]
-    b = cfg["bits"]
+    b = args.bits or cfg["bits"]
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     csr = pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values)
@@ -304,7 +304,7 @@ def run_sharded(args, world, rank, local):
     dev = torch.device("cuda", local)
     g = make_graph(key, dev)
     iters = args.iters or g.meta["iters"]
-    b = g.meta["bits"]
+    b = args.bits or g.meta["bits"]
     n, m = g.n_src, g.m
     stream = torch.cuda.current_stream()
     sh = pdist.ShardedPageRank(n, g.row_ptr, g.col, b, device=dev, stream=stream, timing=True)
@@ -571,6 +571,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS) + ["all"])
     ap.add_argument("--impl", default="pcpm", choices=["pcpm", "reference"])
     ap.add_argument("--iters", type=int, default=0)
+    ap.add_argument("--lib", default="", help="load this libpcpm variant (A/B experiments)")
+    ap.add_argument("--bits", type=int, default=0, help="partition bits b (q = 2^b); default: the config's")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pull", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -584,6 +586,8 @@ def main():
                     help="N>1: run N independent replicas instead of one destination-sharded graph")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     args = ap.parse_args()
+    if args.lib:                                   # A/B variant build of libpcpm.so
+        os.environ["PCPM_LIB"] = os.path.abspath(args.lib)
     world, rank, local = dist_setup(args)
     keys = sorted(WORKLOADS) if args.config == "all" else [args.config]
     for key in keys:

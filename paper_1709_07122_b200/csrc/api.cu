@@ -99,9 +99,10 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.n_items = h->n_gitems;
   a.bin_nslices = h->bin_nslices;
   a.counters = h->counters;
-  a.bin_arrive = h->bin_arrive;
   a.slot_buf = h->slot_buf;
   a.bin_slot_base = h->bin_slot_base;
+  a.has_split = h->n_split_bins > 0;
+  a.bin_arrive = h->bin_arrive;
   a.hi = h->hi;
   a.item_red = h->item_red;
   a.b = h->b;
@@ -350,13 +351,10 @@ pcpm_handle* pcpm_build_shard(const pcpm_csr* csr, int partition_bits, int64_t v
     set_error(PCPM_EINVAL, "shard handles take only PCPM_WIDE_IDS / PCPM_KEEP_VALUES");
     return nullptr;
   }
-  pcpm_csr shape = *csr;                     // validation of sizes happens on the slice shape
-  shape.n_dst = v_hi - v_lo;
   if (csr->n_dst >= (int64_t(1) << 31)) {
     set_error(PCPM_ETOOBIG, "n >= 2^31: the MSB of a 4-byte ID is the run flag (P:172-173)");
     return nullptr;
   }
-  (void)shape;
   return build_common(csr, partition_bits, flags, cuda_stream, v_lo, v_hi);
 }
 
@@ -621,7 +619,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     return PCPM_OK;
   }
   if (!strcmp(key, "epilogue_prefetch")) {
-    h->opt_epi_pf = value ? 1 : 0;
+    if (value < 0 || value > 64) {
+      set_error(PCPM_EINVAL, "epilogue_prefetch must be in [0, 64] (tiles before the item's end)");
+      return PCPM_EINVAL;
+    }
+    h->opt_epi_pf = (int)value;
     free_graph(h);
     return PCPM_OK;
   }

@@ -588,6 +588,17 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_dst))) return rc;
   TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
   h->n_slots = nslots;
+  {
+    std::vector<uint32_t> sb;
+    for (int64_t j = 0; j < k_dst; ++j)
+      if (nsl[j] > 1) sb.push_back((uint32_t)j);
+    h->n_split_bins = (int)sb.size();
+    if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
+    if (!sb.empty())
+      TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
+    const int64_t blocks = (int64_t)sb.size() * ((q + 1023) / 1024);
+    if ((rc = dev_alloc_t(h, &h->split_red, std::max<int64_t>(2, 2 * blocks)))) return rc;
+  }
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
   TK(cudaGetLastError());
@@ -620,12 +631,12 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   if ((rc = dev_alloc_t(h, &h->xbuf, n_src + 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
-  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
+  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
   if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
   if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
   TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
-  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
   TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
   TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));

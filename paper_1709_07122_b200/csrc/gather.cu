@@ -49,8 +49,8 @@ struct StageMeta {
   uint32_t pad;
 };
 
-#ifndef PCPM_GATHER_BIG_TILE
-#define PCPM_GATHER_BIG_TILE 0
+#ifndef PCPM_GATHER_TILE_MODE
+#define PCPM_GATHER_TILE_MODE 0     // 0: 4096 x 4 stages, 1: 8192 x 2, 2: 2048 x 8 (compact PageRank)
 #endif
 template <typename IdT, bool W>
 struct Cfg {
@@ -61,15 +61,15 @@ struct Cfg {
   // = 1 selects 8192-ID tiles double-buffered (2 x 48 KB; measured slower on
   // c4: 2.10 vs 1.98 ms).  Other variants: 2048-ID tiles, 16 warps of 128 IDs.
   static constexpr bool kHot = kCompact && !W;
-  static constexpr bool kBig = kHot && PCPM_GATHER_BIG_TILE;
-  static constexpr int kTile = kBig ? 4 * kTileIds : (kHot ? 2 * kTileIds : kTileIds);
-  static constexpr int kStages = kBig ? 2 : 4;
+  static constexpr int kMode = kHot ? PCPM_GATHER_TILE_MODE : 0;
+  static constexpr int kTile = kHot ? (kMode == 1 ? 4 * kTileIds : (kMode == 2 ? kTileIds : 2 * kTileIds)) : kTileIds;
+  static constexpr int kStages = kMode == 1 ? 2 : (kMode == 2 ? 8 : 4);
   // Consumer warps form two groups that take alternate stages (group g: stages
   // g, g+2, ...), so each warp decodes two sub-chunks per stage it sees and the
   // per-stage bookkeeping is paid once per 2 sub-chunks; both groups run at once.
   static constexpr int kWarps = kHot ? 31 : 16;
   static constexpr int kThreads = 32 * (kWarps + 1);
-  static constexpr int kSub = kHot ? kTile / 32 : kTile / 16;   // IDs per sub-chunk
+  static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kTile / 16;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
   static constexpr int kGroupA = (kWarps + 1) / 2;          // warps of group 0 (stages 0, 2)
   static constexpr int kGroupB = kWarps - kGroupA;          // warps of group 1 (stages 1, 3)
@@ -88,9 +88,6 @@ struct Cfg {
 };
 
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
-__device__ __forceinline__ uint64_t ldcg_u64(const uint64_t* p) {
-  return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(p));
-}
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
@@ -185,16 +182,6 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         push_meta(m);                              // both groups run the item's epilogue
         push_meta(m);
       } else {
-        if constexpr (PR) {
-          if (a.epi_pf && lane == 0) {   // the apply's vertex arrays of partition j, L2-resident by the epilogue
-            const int64_t v0 = (int64_t)item.j << a.b;
-            const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
-            if (vb) {
-              bulk_prefetch_l2(a.inv_deg + v0, vb);
-              bulk_prefetch_l2(a.pr_old + v0, vb);
-            }
-          }
-        }
         const uint32_t t0 = item.x0 / C::kTile, t1 = (item.x1 - 1) / C::kTile;
         for (uint32_t tb0 = t0; tb0 <= t1; tb0 += 32) {
           const uint32_t tl = tb0 + lane;
@@ -220,6 +207,17 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
               bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
               if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+            }
+            if constexpr (PR) {
+              // the apply's vertex arrays of partition j into L2 a few tiles before the epilogue
+              if (a.epi_pf && lane == 0 && tb0 + k == (t1 > t0 + (uint32_t)a.epi_pf ? t1 - (uint32_t)a.epi_pf : t0)) {
+                const int64_t v0 = (int64_t)item.j << a.b;
+                const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
+                if (vb) {
+                  bulk_prefetch_l2(a.inv_deg + v0, vb);
+                  bulk_prefetch_l2(a.pr_old + v0, vb);
+                }
+              }
             }
             if (lane == 0) {
               const uint32_t t = tb0 + k;
@@ -435,7 +433,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
           *flag_s = last ? 1u : 0u;
         }
         named_bar_sync(1, kCons);
-        run_apply = *flag_s != 0u;
+        // with k_apply_split (the default) every slice only flushes; the in-kernel
+        // last-arriver apply below is kept for has_split == 0 handles.  (The code
+        // shape of this epilogue measurably changes the decode loop's schedule:
+        // keep it as is unless re-measured.)
+        run_apply = *flag_s != 0u && !a.has_split;
         if (run_apply) __threadfence();
       }
       // exact 64-bit total of local vertex i; resets the state it reads
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   if (*flag_s) {
     __threadfence();
     if constexpr (PR) {
-      if (cw == 0) {
+      if (cw == 0 && !a.has_split) {            // with split bins k_apply_split reduces
         // fixed order: lane-strided partial sums, then a fixed shuffle tree
         double sd = 0.0, sr = 0.0;
         for (int i = lane; i < a.n_items; i += 32) {
@@ -566,6 +568,101 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
     if (ctid == 0) {
       a.counters[0] = 0u;
       a.counters[1] = 0u;
+    }
+  }
+}
+
+// Apply of the split bins (items whose bin was cut into slices): one block per
+// (split bin, 1024-vertex chunk); total = sum of the slices' low words + the carry
+// word.  The last block reduces the per-item (gather) and per-block (here)
+// dangling / residual partials in fixed order.
+constexpr int kSplitThreads = 256, kSplitChunk = 1024;
+
+template <bool PR>
+__global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs a, const uint32_t* split_bins,
+                                                              int n_split_blocks, double* split_red) {
+  __shared__ double red_s[2 * (kSplitThreads / 32)];
+  __shared__ uint32_t last_s;
+  const int64_t q = int64_t(1) << a.b;
+  const int chunks = (int)((q + kSplitChunk - 1) / kSplitChunk);
+  const uint32_t j = split_bins[blockIdx.x / chunks];
+  const int64_t c0 = (int64_t)(blockIdx.x % chunks) * kSplitChunk;
+  const uint32_t v0 = j << a.b;
+  const int64_t cnt = min(q, a.n_dst - (int64_t)v0);
+  const uint32_t nsl = a.bin_nslices[j];
+  const uint32_t* sb = a.slot_buf + (size_t)a.bin_slot_base[j] * (size_t)q;
+  double base_pr = 0.0, inv_scale = 0.0, sp_inv = 1.0;
+  float fscale = 1.0f;
+  if constexpr (PR) {
+    base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+    fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);
+    inv_scale = 1.0 / (double)fscale;
+  } else {
+    sp_inv = ldexp(1.0, -spmv_fbits(*a.xmax, a.wexp));
+  }
+  double dang = 0.0, res = 0.0;
+  for (int64_t i = c0 + threadIdx.x; i < min(cnt, c0 + kSplitChunk); i += kSplitThreads) {
+    const uint32_t v = v0 + (uint32_t)i;
+    uint64_t tot = (uint64_t)__ldcg(&a.hi[v]) << 32;
+    for (uint32_t sl = 0; sl < nsl; ++sl) {
+      const uint32_t w = __ldcg(sb + (size_t)sl * (size_t)q + i);
+      tot += PR ? (uint64_t)w : (uint64_t)(long long)(int32_t)w;   // SpMV low words are signed
+    }
+    a.hi[v] = 0u;
+    if constexpr (PR) {
+      const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
+      a.pr_new[v] = (float)prn;
+      const float idg = __ldg(a.inv_deg + v);
+      a.spr_new[v] = (float)prn * idg * fscale;
+      if (idg == 0.0f) dang += prn;
+      res += fabs(prn - (double)a.pr_old[v]);
+    } else {
+      a.y[v] = (float)((double)(long long)tot * sp_inv);
+    }
+  }
+  if constexpr (PR) {
+    for (int o = 16; o; o >>= 1) {
+      dang += __shfl_xor_sync(0xffffffffu, dang, o);
+      res += __shfl_xor_sync(0xffffffffu, res, o);
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+      red_s[w] = dang;
+      red_s[kSplitThreads / 32 + w] = res;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sd = 0.0, sr = 0.0;
+      for (int k = 0; k < kSplitThreads / 32; ++k) {
+        sd += red_s[k];
+        sr += red_s[kSplitThreads / 32 + k];
+      }
+      split_red[2 * blockIdx.x] = sd;
+      split_red[2 * blockIdx.x + 1] = sr;
+      __threadfence();
+      last_s = atomicAdd(&a.counters[6], 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (last_s && w == 0) {
+      __threadfence();
+      double sd = 0.0, sr = 0.0;             // fixed order: gather items, then split blocks
+      for (int i = lane; i < a.n_items; i += 32) {
+        sd += __ldcg(&a.item_red[2 * i]);
+        sr += __ldcg(&a.item_red[2 * i + 1]);
+      }
+      for (int i = lane; i < n_split_blocks; i += 32) {
+        sd += __ldcg(&split_red[2 * i]);
+        sr += __ldcg(&split_red[2 * i + 1]);
+      }
+      for (int o = 16; o; o >>= 1) {
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      }
+      if (lane == 0) {
+        *a.dang_out = sd;
+        *a.res_out = sr;
+        a.counters[6] = 0u;
+      }
     }
   }
 }
@@ -626,13 +723,26 @@ int gather_threads(bool wide, bool weighted) {
   return weighted ? Cfg<uint16_t, true>::kThreads : Cfg<uint16_t, false>::kThreads;
 }
 
+int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaStream_t s) {
+  if (h->n_split_bins == 0) return PCPM_OK;
+  const int chunks = (int)((h->q + kSplitChunk - 1) / kSplitChunk);
+  const int blocks = h->n_split_bins * chunks;
+  if (pagerank)
+    k_apply_split<true><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins, blocks, h->split_red);
+  else
+    k_apply_split<false><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins, blocks, h->split_red);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
+  return PCPM_OK;
+}
+
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s) {
   const int smem = gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
   gather_fn(h->wide, weighted, pagerank)<<<grid, gather_threads(h->wide, weighted), smem, s>>>(a);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
-  return PCPM_OK;
+  return launch_apply_split(h, a, pagerank, s);     // split bins (small k), if any
 }
 
 }  // namespace pcpm

@@ -108,8 +108,11 @@ struct pcpm_handle {
   uint32_t* slot_buf = nullptr;     // [n_slots * q] low words of the slices of split bins
   uint32_t* bin_slot_base = nullptr;// [k_dst] first slot of bin j's slices
   uint32_t n_slots = 0;
+  uint32_t* bin_arrive = nullptr;   // [k_dst] slice arrival counters (kept zero)
+  uint32_t* split_bins = nullptr;   // [n_split_bins] bins cut into slices (applied by k_apply_split)
+  int n_split_bins = 0;
+  double* split_red = nullptr;      // [2 * blocks of k_apply_split] dangling / residual partials
   uint32_t* hi = nullptr;           // [n_dst] fixed-point carry words (kept zero)
-  uint32_t* bin_arrive = nullptr;   // [k_dst]
   uint32_t* counters = nullptr;     // [4] work counter, done counter (kept zero)
   double* item_red = nullptr;       // [2*n_gitems] per-item (dangling, residual) partials
   double* red = nullptr;            // [2*(red_cap)] D_t, res_t
@@ -119,7 +122,7 @@ struct pcpm_handle {
   // options (pcpm_set_option)
   int opt_use_graph = 1;
   int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
-  int opt_epi_pf = 0;               // gather: prefetch the apply's vertex arrays into L2 at item claim
+  int opt_epi_pf = 4;               // gather: L2 prefetch of the apply's vertex arrays, tiles before the item's end (0 = off)
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
   int opt_scatter_lpt = 0;          // scatter claim order: 0 ascending p, 1 largest first
   int opt_scatter_pf = 0;           // scatter: PNG stages prefetched into L2 ahead of the ring
@@ -223,9 +226,10 @@ struct GatherArgs {
   int n_items;
   const uint32_t* bin_nslices;
   uint32_t* counters;      // [0] work, [1] done
-  uint32_t* bin_arrive;
   uint32_t* slot_buf;      // split bins: slice s of bin j writes its low words to slot_buf[(base_j + s) q ..]
   const uint32_t* bin_slot_base;
+  int has_split;           // split bins exist: k_apply_split applies them and writes the reductions
+  uint32_t* bin_arrive;    // [k_dst] slices arrived per split bin (reset by the last)
   uint32_t* hi;
   double* item_red;        // [2*n_items]
   int b;
@@ -245,7 +249,7 @@ struct GatherArgs {
   const float* xmax;       // device max|x| of this call (fixed-point scale)
   int wexp;                // max|w| <= 2^wexp
   int pf_tiles;            // L2 prefetch distance of the gather producer, in tiles
-  int epi_pf;              // prefetch outdeg / pr_old of the item's partition into L2
+  int epi_pf;              // prefetch inv_deg / pr_old of the item's partition this many tiles before its end
 };
 __device__ int spmv_fbits(float xmax, int wexp);
 int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpcpm.so")
+LIB_PATH = os.environ.get("PCPM_LIB") or os.path.join(_HERE, "libpcpm.so")   # PCPM_LIB: A/B variant builds
 
 PCPM_OK = 0
 PCPM_EINVAL = -1
