@@ -190,6 +190,11 @@ int64_t pcpm_last_launch_count(const pcpm_handle* h);
  * ms[1+2t] = scatter_t, ms[2+2t] = gather_t (pull: ms[1+t] = pull_t).
  * Returns the number of floats written (synchronises the stream). */
 int pcpm_get_phase_times(pcpm_handle* h, float* ms, int cap);
+/* Consumer-warp cycle counters of the gather accumulated since the last reset, for
+ * builds with -DPCPM_GATHER_PROFILE=1 (all zero otherwise): out[0] waiting for
+ * stages, out[1] decoding, out[2] at the epilogue's first barrier, out[3] in the
+ * epilogue, out[4] number of warps that reported.  Synchronous; returns the count. */
+int pcpm_get_debug_counters(uint64_t* out, int cap, int reset);
 
 #ifdef __cplusplus
 }

@@ -631,6 +631,14 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
   return PCPM_EINVAL;
 }
 
+int pcpm_get_debug_counters(uint64_t* out, int cap, int reset) {
+  if (!out || cap < 0) {
+    set_error(PCPM_EINVAL, "NULL output");
+    return PCPM_EINVAL;
+  }
+  return read_debug_counters(reinterpret_cast<unsigned long long*>(out), cap, reset != 0);
+}
+
 int64_t pcpm_last_launch_count(const pcpm_handle* h) { return h ? h->launches : 0; }
 
 int pcpm_get_phase_times(pcpm_handle* h, float* ms, int cap) {

@@ -63,7 +63,10 @@ struct Cfg {
   static constexpr bool kHot = kCompact && !W;
   static constexpr int kMode = kHot ? PCPM_GATHER_TILE_MODE : 0;
   static constexpr int kTile = kHot ? (kMode == 1 ? 4 * kTileIds : (kMode == 2 ? kTileIds : 2 * kTileIds)) : kTileIds;
-  static constexpr int kStages = kMode == 1 ? 2 : (kMode == 2 ? 8 : 4);
+#ifndef PCPM_GATHER_STAGES
+#define PCPM_GATHER_STAGES 4
+#endif
+  static constexpr int kStages = kMode == 1 ? 2 : (kMode == 2 ? 8 : (kHot ? PCPM_GATHER_STAGES : 4));
   // Consumer warps form two groups that take alternate stages (group g: stages
   // g, g+2, ...), so each warp decodes two sub-chunks per stage it sees and the
   // per-stage bookkeeping is paid once per 2 sub-chunks; both groups run at once.
@@ -90,6 +93,14 @@ struct Cfg {
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
+
+// Debug timing of the consumer warps (built with -DPCPM_GATHER_PROFILE=1 only):
+// [0] cycles waiting for full stages, [1] decoding stages, [2] at the epilogue's
+// first barrier, [3] in the epilogue, [4] warp count.  Read by pcpm_get_debug_counters.
+__device__ unsigned long long g_gather_prof[8];
+#ifndef PCPM_GATHER_PROFILE
+#define PCPM_GATHER_PROFILE 0
+#endif
 
 __device__ int spmv_fbits(float xmax, int wexp) {
   int ex = 0;
@@ -288,8 +299,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
 
   int stage = grp, rot = 0;
   uint32_t phase = 0;
+  unsigned long long pt[4] = {0, 0, 0, 0};
+  long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
   for (;;) {
     mbar_wait(&full[stage], phase);
+    if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[0] += t - tc; tc = t; }
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;
     const uint32_t v0 = m.j << a.b;
@@ -409,10 +423,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
     if (lane == 0) mbar_arrive(&empty[stage]);
     stage += 2;
     if (stage >= S) { stage -= S; phase ^= 1; }
+    if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[1] += t - tc; tc = t; }
 
     if (m.flags & kFlagLast) {
       // ---------------- epilogue of this item ----------------
       named_bar_sync(1, kCons);
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[2] += t - tc; tc = t; }
       const int64_t cnt = min(q, a.n_dst - (int64_t)v0);
       const uint32_t nsl = a.bin_nslices[m.j];
       bool run_apply = true;
@@ -534,7 +550,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       }
       for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
       named_bar_sync(1, kCons);
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[3] += t - tc; tc = t; }
     }
+  }
+  if (PCPM_GATHER_PROFILE && lane == 0) {
+    for (int k = 0; k < 4; ++k) atomicAdd(&g_gather_prof[k], pt[k]);
+    atomicAdd(&g_gather_prof[4], 1ull);
   }
 
   // ---------------- last CTA: fixed-order reduction, counter reset ----------------
@@ -700,8 +721,8 @@ int prepare_gather(pcpm_handle* h) {
   for (int wd = 0; wd < 2; ++wd)
     for (int w = 0; w < 2; ++w)
       for (int p = 0; p < 2; ++p) {
-        if (gather_smem_bytes(kMaxBits, wd, w) > maxsm) {
-          set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit");
+        if (gather_smem_bytes(h->b, wd, w) > maxsm) {
+          set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit for this partition size");
           return PCPM_ECUDA;
         }
         PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
@@ -721,6 +742,17 @@ int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStr
 int gather_threads(bool wide, bool weighted) {
   if (wide) return weighted ? Cfg<uint32_t, true>::kThreads : Cfg<uint32_t, false>::kThreads;
   return weighted ? Cfg<uint16_t, true>::kThreads : Cfg<uint16_t, false>::kThreads;
+}
+
+int read_debug_counters(unsigned long long* out, int cap, bool reset) {
+  unsigned long long v[8];
+  PCPM_CK(cudaMemcpyFromSymbol(v, g_gather_prof, sizeof(v)));
+  for (int i = 0; i < cap && i < 8; ++i) out[i] = v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    PCPM_CK(cudaMemcpyToSymbol(g_gather_prof, z, sizeof(z)));
+  }
+  return cap < 8 ? cap : 8;
 }
 
 int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaStream_t s) {

@@ -257,6 +257,7 @@ int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pager
 int gather_smem_bytes(int b, bool wide, bool weighted);
 
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
+int read_debug_counters(unsigned long long* out, int cap, bool reset);
 int prepare_gather(pcpm_handle* h);
 int prepare_scatter(pcpm_handle* h);
 int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, double spr_scale, cudaStream_t s);

@@ -30,7 +30,7 @@ PCPM_WIDE_IDS = 0x8
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
-            "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step"]
+            "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters"]
 
 
 class PcpmError(RuntimeError):
@@ -91,6 +91,7 @@ def _load():
         "pcpm_build_shard": (P, [ctypes.POINTER(pcpm_csr), I, I64, I64, ctypes.c_uint, P]),
         "pcpm_shard_init": (I, [P, P, P, P]),
         "pcpm_shard_step": (I, [P, ctypes.c_float, P, P, P, P, P, P]),
+        "pcpm_get_debug_counters": (I, [P, I, I]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -240,3 +241,11 @@ def pcpm_shard_init(h, pr0, spr0, dang0):
 def pcpm_shard_step(h, d: float, spr_in, D_in, pr_old, pr_new, spr_out, red_out):
     return _check(_lib.pcpm_shard_step(h, float(d), _ptr(spr_in), _ptr(D_in), _ptr(pr_old), _ptr(pr_new),
                                        _ptr(spr_out), _ptr(red_out)))
+
+
+def pcpm_get_debug_counters(reset: bool = True) -> np.ndarray:
+    buf = np.zeros(8, dtype=np.uint64)
+    n = _lib.pcpm_get_debug_counters(_ptr(buf), 8, int(reset))
+    if n < 0:
+        _check(n)
+    return buf[:n]

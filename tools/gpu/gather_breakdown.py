@@ -1,0 +1,35 @@
+"""Consumer-warp time breakdown of the gather (needs a -DPCPM_GATHER_PROFILE=1 build).
+
+    PCPM_LIB=paper_1709_07122_b200/libpcpm_prof.so python tools/gpu/gather_breakdown.py [c4] [opt=val ...]
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from inputs import graphs  # noqa: E402
+from paper_1709_07122_b200 import pcpm  # noqa: E402
+
+key = sys.argv[1] if len(sys.argv) > 1 else "c4"
+g = graphs.make_config(key, backend="torch", device="cuda")
+cfg = graphs.CONFIGS[key]
+bits = int(os.environ.get("PCPM_BITS", cfg["bits"]))
+h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values), bits, 0,
+                       torch.cuda.current_stream())
+for kv in sys.argv[2:]:
+    k, v = kv.split("=")
+    pcpm.pcpm_set_option(h, k, int(v))
+out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+pcpm.pcpm_pagerank(h, 0.85, cfg["iters"], out)
+torch.cuda.synchronize()
+pcpm.pcpm_get_debug_counters(reset=True)
+pcpm.pcpm_pagerank(h, 0.85, cfg["iters"], out)
+torch.cuda.synchronize()
+c = pcpm.pcpm_get_debug_counters(reset=True)
+tot = float(sum(c[:4]))
+names = ["wait for stage", "decode", "epilogue barrier", "epilogue"]
+print(key, "warps", int(c[4]), " ".join(f"{n}={c[i] / tot:.3f}" for i, n in enumerate(names)))
+pcpm.pcpm_destroy(h)
