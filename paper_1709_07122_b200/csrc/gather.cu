@@ -70,9 +70,12 @@ struct Cfg {
   // Consumer warps form two groups that take alternate stages (group g: stages
   // g, g+2, ...), so each warp decodes two sub-chunks per stage it sees and the
   // per-stage bookkeeping is paid once per 2 sub-chunks; both groups run at once.
-  static constexpr int kWarps = kHot ? 31 : 16;
+#ifndef PCPM_GATHER_COLD_WARPS
+#define PCPM_GATHER_COLD_WARPS 31
+#endif
+  static constexpr int kWarps = kHot ? 31 : PCPM_GATHER_COLD_WARPS;
   static constexpr int kThreads = 32 * (kWarps + 1);
-  static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kTile / 16;   // IDs per sub-chunk
+  static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kChunkIds;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
   static constexpr int kGroupA = (kWarps + 1) / 2;          // warps of group 0 (stages 0, 2)
   static constexpr int kGroupB = kWarps - kGroupA;          // warps of group 1 (stages 1, 3)

@@ -31,8 +31,15 @@ namespace pcpm {
 namespace {
 
 // ------------------------------------------------------------------ TMA variant
-constexpr int kScW = 16;                           // consumer warps
-constexpr int kScThreads = 32 * (kScW + 1);
+// consumer warps: 31 for the compact (2-byte) PNG -- 32 sub-ranges of 256 entries per
+// 16 KB stage, the extra one rotating -- and 16 for the 4-byte PNG (16 sub-ranges)
+#ifndef PCPM_SCATTER_WARPS16
+#define PCPM_SCATTER_WARPS16 31
+#endif
+template <typename SrcT> struct ScCfg {
+  static constexpr int kW = sizeof(SrcT) == 2 ? PCPM_SCATTER_WARPS16 : 16;
+  static constexpr int kThreads = 32 * (kW + 1);
+};
 constexpr int kScStages = 5;
 constexpr int kScStageBytes = 16384;               // PNG bytes per stage
 constexpr int kScOffCap = kScatterMaxGroups + 8;   // offsets of one item (+ alignment slack)
@@ -70,11 +77,13 @@ struct ScatterArgs {
 };
 
 template <typename SrcT>
-__global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs a) {
+__global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const ScatterArgs a) {
+  constexpr int kScW = ScCfg<SrcT>::kW;
   constexpr int kChunk = kScStageBytes / (int)sizeof(SrcT);   // PNG entries per stage
-  constexpr int kSub = kChunk / kScW;                           // entries per consumer warp
+  constexpr int kSub = kPngChunk;                               // entries per sub-range
+  constexpr int kNsr = kChunk / kSub;                           // sub-ranges per stage
   constexpr uint32_t kAlignE = kPngChunk;                       // stage bases: multiples of kPngChunk
-  static_assert(kSub % kPngChunk == 0, "warp sub-ranges start on grp_at anchors");
+  static_assert(kSub % kPngChunk == 0 && kNsr >= kScW, "warp sub-ranges start on grp_at anchors");
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t q = int64_t(1) << a.b;
   float* xs = reinterpret_cast<float*>(smem);                                        // q floats
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
   } else {
     // ================= consumers =================
     const int cw = warp - 1;
-    int stage = 0;
+    int stage = 0, rot = 0;
     uint32_t phase = 0, iphase = 0;
     const uint32_t ubase_wide = 0;
     (void)ubase_wide;
@@ -211,12 +220,13 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
         mbar_wait(&full[stage], phase);
         const ScStageMeta sm = smeta[stage];
         const SrcT* ps = reinterpret_cast<const SrcT*>(ring + stage * kScStageBytes);
-        const uint32_t wb = sm.base + (uint32_t)(cw * kSub);
+        auto range = [&](const int sr) {
+        const uint32_t wb = sm.base + (uint32_t)(sr * kSub);
         const uint32_t wlo = max(wb, sm.lo), whi = min(wb + (uint32_t)kSub, sm.hi);
         if (wlo < whi) {
-          // group of the warp's first entry from the precomputed grp_at anchor of its
-          // sub-range (flat group p*k_dst + j), then advanced per lane as e crosses
-          // group ends; (gend, delta) stay in registers between crossings
+          // group of the sub-range's first entry from its precomputed grp_at anchor
+          // (flat group p*k_dst + j), then advanced per lane as e crosses group
+          // ends; (gend, delta) stay in registers between crossings
           const int32_t ga = (int32_t)(grp_s[stage * kScGrpCap + sm.gshift + (wb - sm.base) / kPngChunk] -
                                        (im.p * (uint32_t)a.k_dst + im.j0));
           uint32_t g = ga > 0 ? (uint32_t)ga : 0u;
@@ -235,6 +245,14 @@ __global__ void __launch_bounds__(kScThreads, 1) k_scatter_tma(const ScatterArgs
             a.upd[e + delta] = xs[u];
           }
         }
+        };
+        for (int sr = cw; sr < (kNsr / kScW) * kScW; sr += kScW) range(sr);
+        int who = rot;                                 // leftover sub-ranges rotate over the warps
+        for (int sr = (kNsr / kScW) * kScW; sr < kNsr; ++sr) {
+          if (cw == who) range(sr);
+          who = (who + 1 == kScW) ? 0 : who + 1;
+        }
+        rot = who;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == kScStages) { stage = 0; phase ^= 1; }
@@ -379,9 +397,9 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
     a.pf_stages = h->opt_scatter_pf;
     const int smem = scatter_tma_smem_bytes(h->b);
     if (h->wide)
-      k_scatter_tma<uint32_t><<<grid, kScThreads, smem, s>>>(a);
+      k_scatter_tma<uint32_t><<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
     else
-      k_scatter_tma<uint16_t><<<grid, kScThreads, smem, s>>>(a);
+      k_scatter_tma<uint16_t><<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
   }
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
