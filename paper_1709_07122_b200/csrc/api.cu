@@ -34,9 +34,24 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   return code;
 }
 
+// Device memory comes from the stream-ordered default pool (cudaMallocAsync on the
+// handle's stream), kept cached between builds: repeated builds (the e2e path) then
+// skip the synchronous cudaMalloc/cudaFree of multi-GB buffers.
+void pool_setup(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
 int dev_alloc(pcpm_handle* h, void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(p, bytes);
+  cudaError_t e = cudaMallocAsync(p, bytes, h->stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error(PCPM_ENOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
@@ -70,7 +85,7 @@ int ensure_red(pcpm_handle* h, int iters) {
   const int need = 2 * (iters + 2);
   if (h->red_cap >= need) return PCPM_OK;
   if (h->red) {
-    cudaFree(h->red);
+    cudaFreeAsync(h->red, h->stream);
     for (auto& p : h->allocs)
       if (p == h->red) p = nullptr;
     h->red = nullptr;
@@ -297,6 +312,7 @@ static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsign
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->b = partition_bits;
   cudaGetDevice(&h->device);
+  pool_setup(h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -472,7 +488,7 @@ void pcpm_destroy(pcpm_handle* h) {
   free_graph(h);
   for (cudaEvent_t e : h->events) cudaEventDestroy(e);
   for (void* p : h->allocs)
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, h->stream);
   delete h;
 }
 

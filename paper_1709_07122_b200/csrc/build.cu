@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -107,6 +109,13 @@ __global__ void k_gather_ids(int64_t m, const uint32_t* __restrict__ perm, const
     ids[x] = id;
     ids16[x] = (uint16_t)((id & qmask) | ((id >> 31) << 15));
     if (w) w[x] = values ? values[e] : 1.0f;
+  }
+}
+
+__global__ void k_ids16(int64_t m, const uint32_t* __restrict__ ids, uint32_t qmask, uint16_t* ids16) {
+  GRID_STRIDE(x, m) {
+    const uint32_t id = ids[x];
+    ids16[x] = (uint16_t)((id & qmask) | ((id >> 31) << 15));
   }
 }
 
@@ -244,15 +253,32 @@ __global__ void k_slice_fill(int64_t n, const int64_t* __restrict__ new_ptr, con
   }
 }
 
-struct Temp {
+// PCPM_BUILD_TIMING=1: synchronise and print the wall time of each build phase (stderr).
+struct PhaseTimer {
+  bool on = getenv("PCPM_BUILD_TIMING") != nullptr;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit PhaseTimer(cudaStream_t st) : s(st) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pcpm build] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
+
+struct Temp {                 // build scratch: stream-ordered pool memory, freed in stream order
   std::vector<void*> ptrs;
+  cudaStream_t s = nullptr;
+  explicit Temp(cudaStream_t st) : s(st) {}
   ~Temp() {
-    for (void* p : ptrs) cudaFree(p);
+    for (void* p : ptrs) cudaFreeAsync(p, s);
   }
   template <typename T>
   cudaError_t alloc(T** p, size_t count) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+    cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), s);
     if (e == cudaSuccess) ptrs.push_back(q);
     *p = reinterpret_cast<T*>(q);
     return e;
@@ -302,7 +328,8 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
   if (h->m_pad == 0) h->m_pad = kTileAlign;
 
-  Temp tmp;
+  Temp tmp(s);
+  PhaseTimer pt(s);
   // ---- inputs on the device
   const int64_t* row_ptr = csr->row_ptr;
   const uint32_t* col = csr->col_idx;
@@ -339,6 +366,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     return PCPM_EBADCSR;
   }
 
+  pt.mark("inputs + row validation");
   // ---- layout arrays owned by the handle
   int rc;
   uint32_t* ids32 = nullptr;           // 4-byte IDs: handle-owned for wide handles, else scratch
@@ -369,6 +397,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   k_outdeg<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, h->outdeg, h->inv_deg, d_dang);
   TK(cudaGetLastError());
 
+  pt.mark("allocations + outdeg");
   uint32_t* G = nullptr;  // flat (p, j) group starts, k_src*k_dst + 1 entries
   TK(tmp.alloc(&G, k_src * k_dst + 1));
   int64_t ep = 0;
@@ -387,6 +416,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       TK(tmp.alloc(&t, bytes));
       TK(cub::DeviceScan::InclusiveScan(t, bytes, rowmark, rowid, MaxOp(), m, s));
     }
+    pt.mark("row ids");
     // ---- classify + validate
     uint32_t *keyj, *enc;
     uint8_t* fl;
@@ -405,6 +435,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       set_error(PCPM_EBADCSR, "a row's columns are not strictly increasing (sorted, deduplicated) (R6)");
       return PCPM_EBADCSR;
     }
+    pt.mark("classify + validate");
     // ---- destID bins: stable sort of edge indices by j
     uint32_t *iota, *keyj_s, *perm;
     TK(tmp.alloc(&iota, m));
@@ -412,12 +443,23 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(tmp.alloc(&perm, m));
     k_iota<<<grid_for(m), kT, 0, s>>>(m, iota);
     TK(cudaGetLastError());
-    TK(radix_sort_pairs(tmp, keyj, keyj_s, iota, perm, m, bits_for((uint64_t)std::max<int64_t>(k_dst - 1, 0)), s));
+    const int jbits = bits_for((uint64_t)std::max<int64_t>(k_dst - 1, 0));
+    if (h->w) {
+      // weights travel with the IDs: sort edge indices, then gather IDs and weights
+      TK(radix_sort_pairs(tmp, keyj, keyj_s, iota, perm, m, jbits, s));
+      pt.mark("sort edges by j");
+      k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, (uint32_t)(q - 1), ids32, h->ids16, h->w);
+    } else {
+      // the encoded IDs are the sort's payload: no random gather afterwards
+      TK(radix_sort_pairs(tmp, keyj, keyj_s, enc, ids32, m, jbits, s));
+      pt.mark("sort edges by j");
+      k_ids16<<<grid_for(m), kT, 0, s>>>(m, ids32, (uint32_t)(q - 1), h->ids16);
+    }
+    TK(cudaGetLastError());
     k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keyj_s, k_dst, h->bin_id_start);
     TK(cudaGetLastError());
-    k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, (uint32_t)(q - 1), ids32, h->ids16, h->w);
-    TK(cudaGetLastError());
 
+    pt.mark("destID bins");
     // ---- PNG: flagged edges, stable sort by (p, j)
     uint32_t* sel;
     int64_t* d_nsel;
@@ -451,6 +493,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     k_png_keys<<<grid_for(ep), kT, 0, s>>>(ep, sel, rowid, col, b, k_dst, pk, pv);
     TK(cudaGetLastError());
     TK(radix_sort_pairs(tmp, pk, pk_s, pv, png32, ep, bits_for((uint64_t)(k_src * k_dst - 1)), s));
+    pt.mark("select + sort PNG");
     k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk_s, k_src * k_dst, G);
     k_png16<<<grid_for(ep), kT, 0, s>>>(ep, png32, (uint32_t)(q - 1), h->png16);
     TK(cudaGetLastError());
@@ -461,6 +504,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       TK(cudaGetLastError());
     }
 
+    pt.mark("PNG arrays");
     // ---- pull comparison: CSC (in-adjacency), sources ascending per destination
     if (flags & PCPM_BUILD_PULL) {
       if ((rc = dev_alloc_t(h, &h->in_ptr, n_dst + 1))) return rc;
@@ -537,6 +581,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, h->chunk_base, nchunks + 1, s));
   }
 
+  pt.mark("pull CSC + offsets + anchors");
   // ---- host-side work lists (small copies)
   std::vector<uint32_t> hbin(k_dst + 1), hG(k_src * k_dst + 1);
   unsigned long long hdang = 0;
@@ -641,6 +686,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaStreamSynchronize(s));
+  pt.mark("work lists + iteration state");
   return PCPM_OK;
 }
 
@@ -664,7 +710,7 @@ int order_scatter_items(pcpm_handle* h, cudaStream_t s) {
 int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags) {
   cudaStream_t s = h->stream;
   const int64_t n = csr->n_src, m = csr->nnz;
-  Temp tmp;
+  Temp tmp(s);
   const int64_t* row_ptr = csr->row_ptr;
   const uint32_t* col = csr->col_idx;
   const float* values = csr->values;
