@@ -359,3 +359,30 @@ def test_spmv_non_square(pcpm):
         assert e.value.code == pcpm.PCPM_ESTATE
     finally:
         pcpm.pcpm_destroy(h)
+
+
+@pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
+                                  {"epilogue_prefetch": 0}, {"gather_prefetch": 8, "epilogue_prefetch": 16},
+                                  {"use_graph": 0}],
+                         ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
+def test_kernel_variants_keep_parity(pcpm, opts):
+    """Every A/B kernel variant of DESIGN.md's design-evidence table stays oracle-exact."""
+    g = graphs.make_graph("rmat", 12, scale=14, permute=True)
+    h = build(pcpm, g, 10)
+    try:
+        for k, v in opts.items():
+            pcpm.pcpm_set_option(h, k, v)
+        ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 12)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 12, out)
+        pr_check(out.cpu().numpy(), ref, str(opts))
+        x = graphs.make_x(g.n_src, 5)
+        pcpm.pcpm_scatter(h, torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        v = pcpm.pcpm_export_layout(h)
+        info = pcpm.pcpm_get_info(h)
+        got = d2h(v.upd, info.e_prime, np.float32)
+        want = oracle.scatter(oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, 10), x)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    finally:
+        pcpm.pcpm_destroy(h)
