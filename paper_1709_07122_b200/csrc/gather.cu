@@ -325,9 +325,13 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
           // lane-strided decode: step c covers the 32 consecutive IDs c*32 .. c*32+31
           // of the sub-chunk, so the window reads of a step hit ~32/r consecutive
           // words (one or two smem wavefronts)
+          // IDs are read sign-extended: the run flag (MSB) becomes the sign, one
+          // compare per ID for the ballot
+          using SIdT = typename std::conditional<sizeof(IdT) == 2, int16_t, int32_t>::type;
+          const SIdT* sids = reinterpret_cast<const SIdT*>(ids_s);
           uint32_t id[P];
 #pragma unroll
-          for (int c = 0; c < P; ++c) id[c] = ids_s[sc * C::kSub + c * 32 + lane];
+          for (int c = 0; c < P; ++c) id[c] = (uint32_t)(int32_t)sids[sc * C::kSub + c * 32 + lane];
           // Alg. 5 update_ptr = #flags in ids[0..x] - 1 (R5), from the sub-chunk's
           // anchor plus a warp prefix count of the MSB flags, step by step
           uint32_t run = cb_s[(sc * C::kSub) / kChunkIds] - 1u - m.win_base;
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
           bool ok[P];
 #pragma unroll
           for (int c = 0; c < P; ++c) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, id[c] & (1u << C::kFlagShift));
+            const uint32_t bal = __ballot_sync(0xffffffffu, (int32_t)id[c] < 0);
             const uint32_t ptr = run + __popc(bal & lemask);
             run += __popc(bal);
             const uint32_t x = xs + c * 32 + lane;
