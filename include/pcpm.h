@@ -180,7 +180,10 @@ int pcpm_get_residuals(pcpm_handle* h, double* host, int cap);
  * update bins (exported as pcpm_layout_view.upd); for bit-exact tests. */
 int pcpm_scatter(pcpm_handle* h, const float* x);
 /* Select a kernel variant for A/B experiments.
- * key "gather_threads", "scatter_split", ... ; returns PCPM_EINVAL for unknown keys. */
+ * Keys: "phase_timing", "use_graph", "scatter_variant" (0|1), "scatter_lpt",
+ * "scatter_prefetch", "gather_prefetch", "epilogue_prefetch".  Every variant
+ * computes the same result.  Returns PCPM_EINVAL for unknown keys or
+ * out-of-range values. */
 int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value);
 /* Kernel launches issued by the last pcpm_pagerank / pcpm_spmv call (per call). */
 int64_t pcpm_last_launch_count(const pcpm_handle* h);

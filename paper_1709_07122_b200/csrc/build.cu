@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 
 #include "pcpm_internal.cuh"
 
@@ -168,14 +169,14 @@ __global__ void k_add_bin_start(int64_t k_src, int64_t k_dst, const uint32_t* __
   GRID_STRIDE(i, k_src * k_dst) upd_off[i] += bin_upd_start[i % k_dst];
 }
 
-// flags per kChunkIds-ID chunk: one warp per chunk, 4 IDs per lane
-__global__ void k_chunk_counts(int64_t nchunks, const uint32_t* __restrict__ ids, uint32_t* cnt) {
+// flags per kChunkIds-ID chunk from the compact IDs (flag = bit 15): one warp per chunk, 4 IDs per lane
+__global__ void k_chunk_counts16(int64_t nchunks, const uint16_t* __restrict__ ids16, uint32_t* cnt) {
   int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t c = warp; c < nchunks; c += nw) {
-    uint4 v = reinterpret_cast<const uint4*>(ids + c * kChunkIds)[lane];
-    uint32_t f = (v.x >> 31) + (v.y >> 31) + (v.z >> 31) + (v.w >> 31);
+    uint2 v = reinterpret_cast<const uint2*>(ids16 + c * kChunkIds)[lane];
+    uint32_t f = ((v.x >> 15) & 1u) + (v.x >> 31) + ((v.y >> 15) & 1u) + (v.y >> 31);
     for (int o = 16; o; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
     if (lane == 0) cnt[c] = f;
   }
@@ -183,13 +184,14 @@ __global__ void k_chunk_counts(int64_t nchunks, const uint32_t* __restrict__ ids
 }
 
 // |N_o(u)| and its fp32 reciprocal (0 for dangling u; the apply multiplies by it)
-__global__ void k_outdeg(int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* outdeg, float* inv_deg,
+__global__ void k_outdeg(int64_t u0, int64_t n, const int64_t* __restrict__ row_ptr, uint32_t* outdeg, float* inv_deg,
                          unsigned long long* n_dangling) {
   __shared__ unsigned int s;
   if (threadIdx.x == 0) s = 0;
   __syncthreads();
   unsigned int local = 0;
-  GRID_STRIDE(u, n) {
+  GRID_STRIDE(i, n) {
+    const int64_t u = u0 + i;
     uint32_t dg = static_cast<uint32_t>(row_ptr[u + 1] - row_ptr[u]);
     outdeg[u] = dg;
     inv_deg[u] = dg ? 1.0f / (float)dg : 0.0f;
@@ -253,6 +255,103 @@ __global__ void k_slice_fill(int64_t n, const int64_t* __restrict__ new_ptr, con
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Chunked construction (the default; DESIGN.md §5 "build").  The CSR is cut into
+// chunks of whole source partitions [p0, p1).  Each chunk's edges are stably
+// sorted by the flat group key g = (u >> b) * k_dst + (v >> b); one payload word
+// carries everything else: (v & (q-1)) | flag << 15 | (u & (q-1)) << 16.  Since a
+// chunk holds whole partitions and the CSR lists u ascending (v ascending per
+// row), the concatenated chunk sorts are sorted by g with edges in (u, v) order
+// inside each group (p, j).  Then
+//   * destID bin j = groups (0, j), (1, j), ... concatenated: each
+//     group is placed at id_off[p][j] = bin_id_start[j] + sum_{p' < p} |(p', j)|;
+//   * the PNG = the flagged edges in the same order (Eff_1: one per
+//     (u, j) run; transposed: grouped by (p, j), u ascending).
+// With host inputs, chunk c+1 is copied (copy stream) while chunk c is sorted.
+struct PayW {                // payload of weighted builds: the word above + the fp32 value
+  uint32_t x, y;
+};
+__device__ __forceinline__ uint32_t pay_word(uint32_t p) { return p; }
+__device__ __forceinline__ uint32_t pay_word(PayW p) { return p.x; }
+__device__ __forceinline__ float pay_value(uint32_t) { return 1.0f; }
+__device__ __forceinline__ float pay_value(PayW p) { return __uint_as_float(p.y); }
+
+__global__ void k_check_rows_c(int64_t u0, int64_t nr, const int64_t* __restrict__ row_ptr, int64_t e0, int64_t e1,
+                               uint32_t* err) {
+  GRID_STRIDE(i, nr) {
+    const int64_t a = row_ptr[u0 + i], c = row_ptr[u0 + i + 1];
+    if (a > c || a < e0 || c > e1) atomicOr(err, 1u);
+  }
+}
+
+__global__ void k_mark_rows_c(int64_t u0, int64_t nr, const int64_t* __restrict__ row_ptr, int64_t e0, int64_t e1,
+                              uint32_t* mark) {
+  GRID_STRIDE(i, nr) {
+    const int64_t a = row_ptr[u0 + i], c = row_ptr[u0 + i + 1];
+    if (a < c && a >= e0 && a < e1) mark[a - e0] = static_cast<uint32_t>(u0 + i);
+  }
+}
+
+// Per edge of the chunk: group key, run flag (Alg. 2 prev_bin / MSB demarcation,
+// P:172-173), payload; validation (col < n_dst, rows strictly increasing).
+template <typename P>
+__global__ void k_classify_c(int64_t e0, int64_t mc, const uint32_t* __restrict__ col, const float* __restrict__ val,
+                             const uint32_t* __restrict__ rowid, int b, int64_t n_dst, int64_t k_dst, bool compress,
+                             uint32_t* key, P* pay, uint32_t* err) {
+  const uint32_t qmask = (1u << b) - 1u;
+  GRID_STRIDE(i, mc) {
+    const uint32_t u = rowid[i];
+    const uint32_t v = col[e0 + i];
+    const bool first = (i == 0) || rowid[i - 1] != u;
+    const uint32_t pv = first ? 0u : col[e0 + i - 1];
+    if (v >= n_dst) atomicOr(err, 2u);
+    if (!first && pv >= v) atomicOr(err, 4u);
+    uint32_t j = v >> b;
+    if (j >= (uint32_t)k_dst) j = (uint32_t)k_dst - 1;      // invalid input: keep the key in range
+    const bool flag = compress ? (first || (pv >> b) != (v >> b)) : true;
+    key[i] = static_cast<uint32_t>((int64_t)(u >> b) * k_dst + j);
+    const uint32_t w = (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
+    if constexpr (std::is_same<P, PayW>::value) pay[i] = PayW{w, __float_as_uint(val[e0 + i])};
+    else pay[i] = w;
+  }
+}
+
+template <typename P>
+__global__ void k_run_flags(int64_t n, const P* __restrict__ pay, uint8_t* fl) {
+  GRID_STRIDE(i, n) fl[i] = (uint8_t)((pay_word(pay[i]) >> 15) & 1u);
+}
+
+// destID bins: sorted edge x of group g goes to id_off[g] + (x - Gs[g]).
+template <typename P>
+__global__ void k_place_ids(int64_t m, const uint32_t* __restrict__ keys, const P* __restrict__ pay,
+                            const uint32_t* __restrict__ Gs, const uint32_t* __restrict__ id_off, int b, int64_t k_dst,
+                            uint16_t* ids16, uint32_t* ids32, float* w) {
+  const uint32_t qmask = (1u << b) - 1u;
+  GRID_STRIDE(x, m) {
+    const uint32_t g = keys[x];
+    const P pv = pay[x];
+    const uint32_t word = pay_word(pv);
+    const uint32_t dst = id_off[g] + (uint32_t)(x - Gs[g]);
+    ids16[dst] = (uint16_t)(word & 0xFFFFu);
+    if (ids32) ids32[dst] = ((uint32_t)(g % (uint32_t)k_dst) << b | (word & qmask)) | ((word >> 15) & 1u) << 31;
+    if (w) w[dst] = pay_value(pv);
+  }
+}
+
+// PNG: chunk c's flagged edges (in group order) to positions off .. off + n.
+template <typename P>
+__global__ void k_png_place(int64_t n, const uint32_t* __restrict__ fk, const P* __restrict__ fp, int64_t off,
+                            int b, int64_t k_dst, uint32_t* pk, uint16_t* png16, uint32_t* png32) {
+  GRID_STRIDE(i, n) {
+    const uint32_t g = fk[i];
+    const uint32_t ul = pay_word(fp[i]) >> 16;
+    pk[off + i] = g;
+    png16[off + i] = (uint16_t)ul;
+    if (png32) png32[off + i] = (g / (uint32_t)k_dst) << b | ul;
+  }
+}
+
 // PCPM_BUILD_TIMING=1: synchronise and print the wall time of each build phase (stderr).
 struct PhaseTimer {
   bool on = getenv("PCPM_BUILD_TIMING") != nullptr;
@@ -308,9 +407,156 @@ cudaError_t radix_sort_pairs(Temp& tmp, const KeyT* kin, KeyT* kout, const ValT*
   return cub::DeviceRadixSort::SortPairs(t, bytes, kin, kout, vin, vout, n, 0, end_bit, s);
 }
 
+
+// Offsets, decode anchors, work lists and iteration state: the part of the
+// build shared by both layout constructions.  G = flat (p, j) PNG group starts.
+int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsigned long long* d_dang) {
+  cudaStream_t s = h->stream;
+  const int64_t k_src = h->k_src, k_dst = h->k_dst, q = h->q, n_src = h->n_src, n_dst = h->n_dst, m = h->m;
+  const int64_t ep = h->e_prime;
+  const int64_t nchunks = h->m_pad / kChunkIds;
+  int rc;
+  // ---- offsets (P:148): png_off, column scans, bin update starts
+  k_png_off<<<grid_for(k_src * (k_dst + 1)), kT, 0, s>>>(k_src, k_dst, G, h->png_off);
+  uint32_t* col_tot;
+  TK(tmp.alloc(&col_tot, k_dst + 1));
+  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, G, h->upd_off, col_tot);
+  TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
+  {
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+  }
+  k_add_bin_start<<<grid_for(k_src * k_dst), kT, 0, s>>>(k_src, k_dst, h->bin_upd_start, h->upd_off);
+  TK(cudaGetLastError());
+
+  // ---- decode anchors: chunk_base[c] = #flags in ids[0 .. c*kChunkIds)
+  {
+    uint32_t* cnt;
+    TK(tmp.alloc(&cnt, nchunks + 1));
+    k_chunk_counts16<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, h->ids16, cnt);
+    TK(cudaGetLastError());
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, h->chunk_base, nchunks + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, h->chunk_base, nchunks + 1, s));
+  }
+
+  pt.mark("pull CSC + offsets + anchors");
+  // ---- host-side work lists (small copies)
+  std::vector<uint32_t> hbin(k_dst + 1), hG(k_src * k_dst + 1);
+  unsigned long long hdang = 0;
+  TK(cudaMemcpyAsync(hbin.data(), h->bin_id_start, sizeof(uint32_t) * (k_dst + 1), cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(hG.data(), G, sizeof(uint32_t) * (k_src * k_dst + 1), cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(&hdang, d_dang, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  h->n_dangling = (int64_t)hdang;
+
+  // gather items: every destination partition gets >= 1 item (its apply runs even
+  // when the bin is empty); heavy bins are cut at tile-aligned points so no
+  // item exceeds ~m / (2 SMs) IDs; largest first (LPT, the GPU analogue of the
+  // paper's dynamic scheduling, P:434).
+  std::vector<GatherItem> gi;
+  std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
+  uint32_t nslots = 0;
+  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (2 * h->num_sms)) / kTileAlign + 1) * kTileAlign);
+  for (int64_t j = 0; j < k_dst; ++j) {
+    int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
+    int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
+    int64_t per = (sz + nslc - 1) / nslc;
+    std::vector<int64_t> cuts{s0};
+    for (int64_t i = 1; i < nslc; ++i) {
+      int64_t c = ((s0 + i * per + kTileAlign - 1) / kTileAlign) * kTileAlign;
+      if (c > cuts.back() && c < s1) cuts.push_back(c);
+    }
+    cuts.push_back(s1);
+    const uint32_t ns = (uint32_t)(cuts.size() - 1);
+    // slices of a split bin each own a slot: a q-word buffer for their low words
+    sbase[j] = ns > 1 ? nslots : 0u;
+    for (size_t i = 0; i + 1 < cuts.size(); ++i) {
+      GatherItem it{};
+      it.j = (uint32_t)j;
+      it.x0 = (uint32_t)cuts[i];
+      it.x1 = (uint32_t)cuts[i + 1];
+      it.pad[0] = ns > 1 ? nslots + (uint32_t)i : 0xFFFFFFFFu;
+      gi.push_back(it);
+    }
+    nsl[j] = ns;
+    if (ns > 1) nslots += ns;
+  }
+  std::stable_sort(gi.begin(), gi.end(),
+                   [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
+  h->n_gitems = (int)gi.size();
+  if ((rc = dev_alloc_t(h, &h->gitems, gi.size()))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
+  TK(cudaMemcpyAsync(h->gitems, gi.data(), sizeof(GatherItem) * gi.size(), cudaMemcpyHostToDevice, s));
+  TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_dst))) return rc;
+  TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  h->n_slots = nslots;
+  {
+    std::vector<uint32_t> sb;
+    for (int64_t j = 0; j < k_dst; ++j)
+      if (nsl[j] > 1) sb.push_back((uint32_t)j);
+    h->n_split_bins = (int)sb.size();
+    if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
+    if (!sb.empty())
+      TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
+    const int64_t blocks = (int64_t)sb.size() * ((q + 1023) / 1024);
+    if ((rc = dev_alloc_t(h, &h->split_red, std::max<int64_t>(2, 2 * blocks)))) return rc;
+  }
+  if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
+  k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
+  TK(cudaGetLastError());
+
+  // scatter items: (p, [j0, j1)) holding ~E' / (2 SMs) updates each
+  std::vector<ScatterItem> si;
+  int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
+  for (int64_t p = 0; p < k_src; ++p) {
+    int64_t acc = 0, j0 = 0;
+    for (int64_t j = 0; j < k_dst; ++j) {
+      acc += hG[p * k_dst + j + 1] - hG[p * k_dst + j];
+      if (acc >= target || j + 1 - j0 >= kScatterMaxGroups) {   // item offsets fit in smem
+        si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)(j + 1), (uint32_t)acc});
+        acc = 0;
+        j0 = j + 1;
+      }
+    }
+    if (acc > 0) si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)k_dst, (uint32_t)acc});
+  }
+  h->n_sitems = (int)si.size();
+  h->sitems_host = si;                     // source-partition order (see order_scatter_items)
+  if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(si.size(), 1)))) return rc;
+  if ((rc = order_scatter_items(h, s))) return rc;
+
+  // ---- iteration scratch (kept zero between uses by the kernels)
+  const int64_t nv = std::max(n_src, n_dst);
+  if ((rc = dev_alloc_t(h, &h->pr[0], nv + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->pr[1], nv + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->spr, n_src + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->xbuf, n_src + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
+  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
+  if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
+  TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
+  TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
+  TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
+  TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
+  TK(cudaStreamSynchronize(s));
+  pt.mark("work lists + iteration state");
+  return PCPM_OK;
+}
+
 }  // namespace
 
-int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+int build_layout_legacy(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   cudaStream_t s = h->stream;
   const int64_t n_src = csr->n_src, n_dst = csr->n_dst, m = csr->nnz;
   const int b = h->b;
@@ -394,7 +640,7 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   unsigned long long* d_dang;
   TK(tmp.alloc(&d_dang, 1));
   TK(cudaMemsetAsync(d_dang, 0, 8, s));
-  k_outdeg<<<grid_for(n_src), kT, 0, s>>>(n_src, row_ptr, h->outdeg, h->inv_deg, d_dang);
+  k_outdeg<<<grid_for(n_src), kT, 0, s>>>(0, n_src, row_ptr, h->outdeg, h->inv_deg, d_dang);
   TK(cudaGetLastError());
 
   pt.mark("allocations + outdeg");
@@ -552,142 +798,301 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     }
   }
 
-  // ---- offsets (P:148): png_off, column scans, bin update starts
-  k_png_off<<<grid_for(k_src * (k_dst + 1)), kT, 0, s>>>(k_src, k_dst, G, h->png_off);
-  uint32_t* col_tot;
+  return finish_layout(h, tmp, pt, G, d_dang);
+}
+
+namespace {
+
+template <typename P>
+int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+  cudaStream_t s = h->stream;
+  const int64_t n_src = csr->n_src, n_dst = csr->n_dst, m = csr->nnz;
+  const int b = h->b;
+  const int64_t q = int64_t(1) << b;
+  const int64_t k_src = (n_src + q - 1) / q, k_dst = (n_dst + q - 1) / q;
+  h->k_src = k_src;
+  h->k_dst = k_dst;
+  h->q = q;
+  h->n_src = n_src;
+  h->n_dst = n_dst;
+  h->m = m;
+  h->compressed = !(flags & PCPM_NO_COMPRESS);
+  h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
+  h->wide = (flags & PCPM_WIDE_IDS) != 0;
+  h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
+  if (h->m_pad == 0) h->m_pad = kTileAlign;
+  const int64_t ng = k_src * k_dst;             // groups (p, j)
+  const int gbits = bits_for((uint64_t)(ng - 1));
+
+  Temp tmp(s);
+  PhaseTimer pt(s);
+  const int64_t* row_ptr = csr->row_ptr;
+  const uint32_t* col = csr->col_idx;
+  const float* values = csr->values;
+  const bool host_rp = !is_device_ptr(row_ptr);
+  const bool host_col = !is_device_ptr(col);
+  const bool host_val = values && !is_device_ptr(values);
+  const bool copies = host_rp || host_col || host_val;
+
+  // ---- partition boundaries of row_ptr (host): global checks and the chunk plan
+  std::vector<int64_t> pb(k_src + 1);
+  if (host_rp) {
+    for (int64_t p = 0; p < k_src; ++p) pb[p] = row_ptr[p * q];
+    pb[k_src] = row_ptr[n_src];
+  } else {
+    TK(cudaMemcpy2DAsync(pb.data(), sizeof(int64_t), row_ptr, sizeof(int64_t) * q, sizeof(int64_t), k_src,
+                         cudaMemcpyDeviceToHost, s));
+    TK(cudaMemcpyAsync(&pb[k_src], row_ptr + n_src, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+  }
+  bool rp_ok = pb[0] == 0 && pb[k_src] == m;
+  for (int64_t p = 0; p < k_src && rp_ok; ++p) rp_ok = pb[p] <= pb[p + 1];
+  if (!rp_ok) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+  int64_t target = copies ? std::max<int64_t>(m / 24, int64_t(1) << 22) : std::max<int64_t>(m / 4, int64_t(1) << 24);
+  if (const char* e = getenv("PCPM_BUILD_CHUNK_EDGES")) target = std::max<int64_t>(1, atoll(e));   // tests: many chunks
+  std::vector<int64_t> cp{0};
+  for (int64_t p = 0; p < k_src; ++p)
+    if (pb[p + 1] - pb[cp.back()] >= target || p + 1 == k_src) cp.push_back(p + 1);
+  const int nck = (int)cp.size() - 1;
+  int64_t mc_max = 1;
+  for (int c = 0; c < nck; ++c) mc_max = std::max(mc_max, pb[cp[c + 1]] - pb[cp[c]]);
+
+  // ---- device copies of host inputs (filled chunk by chunk on a copy stream)
+  int64_t* d_rp = const_cast<int64_t*>(row_ptr);
+  uint32_t* d_col = const_cast<uint32_t*>(col);
+  float* d_val = const_cast<float*>(values);
+  if (host_rp) TK(tmp.alloc(&d_rp, n_src + 1));
+  if (host_col) TK(tmp.alloc(&d_col, m));
+  if (host_val) TK(tmp.alloc(&d_val, m));
+
+  // ---- layout arrays owned by the handle
+  int rc;
+  uint32_t* ids32 = nullptr;
+  if (h->wide) {
+    if ((rc = dev_alloc_t(h, &h->ids, h->m_pad))) return rc;
+    ids32 = h->ids;
+    TK(cudaMemsetAsync(ids32, 0, sizeof(uint32_t) * h->m_pad, s));
+  }
+  if ((rc = dev_alloc_t(h, &h->ids16, h->m_pad))) return rc;
+  TK(cudaMemsetAsync(h->ids16 + m, 0, sizeof(uint16_t) * (h->m_pad - m), s));
+  if (h->weighted) {
+    if ((rc = dev_alloc_t(h, &h->w, h->m_pad))) return rc;
+    TK(cudaMemsetAsync(h->w + m, 0, sizeof(float) * (h->m_pad - m), s));
+  }
+  if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1) + 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->upd_off, ng + 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_id_start, k_dst + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_upd_start, k_dst + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->chunk_base, h->m_pad / kChunkIds + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->outdeg, n_src))) return rc;
+  if ((rc = dev_alloc_t(h, &h->inv_deg, n_src + 4))) return rc;
+
+  // ---- scratch: sorted edges (keys, payloads) and their flagged subsets, per-chunk buffers
+  uint32_t *err, *keys_s, *fk, *mark, *rowid, *key_c;
+  P *pay_s, *fp, *pay_c;
+  uint8_t* fl_c;
+  int64_t* d_cnt;
+  unsigned long long* d_dang;
+  const bool pull = (flags & PCPM_BUILD_PULL) != 0;
+  TK(tmp.alloc(&err, 4));
+  TK(tmp.alloc(&d_dang, 1));
+  TK(tmp.alloc(&d_cnt, 2 * nck + 2));
+  TK(tmp.alloc(&keys_s, m));
+  TK(tmp.alloc(&pay_s, m));
+  TK(tmp.alloc(&fk, m));
+  TK(tmp.alloc(&fp, m));
+  TK(tmp.alloc(&mark, mc_max));
+  TK(tmp.alloc(&rowid, pull ? m : mc_max));
+  TK(tmp.alloc(&key_c, mc_max));
+  TK(tmp.alloc(&pay_c, mc_max));
+  TK(tmp.alloc(&fl_c, mc_max));
+  TK(cudaMemsetAsync(err, 0, 16, s));
+  TK(cudaMemsetAsync(d_dang, 0, 8, s));
+  TK(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (2 * nck + 2), s));
+  // CUB scratch, sized once for the largest chunk
+  size_t b_scan = 0, b_sort = 0, b_sel = 0, b_sel2 = 0;
+  TK(cub::DeviceScan::InclusiveScan(nullptr, b_scan, mark, rowid, MaxOp(), mc_max, s));
+  TK(cub::DeviceRadixSort::SortPairs(nullptr, b_sort, key_c, keys_s, pay_c, pay_s, mc_max, 0, gbits, s));
+  TK(cub::DeviceSelect::Flagged(nullptr, b_sel, keys_s, fl_c, fk, d_cnt, mc_max, s));
+  TK(cub::DeviceSelect::Flagged(nullptr, b_sel2, pay_s, fl_c, fp, d_cnt, mc_max, s));
+  uint8_t* cub_tmp;
+  const size_t b_cub = std::max(std::max(b_scan, b_sort), std::max(b_sel, b_sel2));
+  TK(tmp.alloc(&cub_tmp, b_cub));
+
+  cudaStream_t cs = nullptr;
+  std::vector<cudaEvent_t> evs;
+  struct Cleanup {
+    cudaStream_t& cs;
+    std::vector<cudaEvent_t>& evs;
+    ~Cleanup() {
+      if (cs) cudaStreamSynchronize(cs);          // no copy may outlive the scratch it writes
+      for (cudaEvent_t e : evs) cudaEventDestroy(e);
+      if (cs) cudaStreamDestroy(cs);
+    }
+  } cleanup{cs, evs};
+  if (copies) {
+    TK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    evs.resize(nck + 1);
+    for (auto& e : evs) TK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TK(cudaEventRecord(evs[nck], s));               // the pool allocations above precede the copies
+    TK(cudaStreamWaitEvent(cs, evs[nck], 0));
+  }
+  pt.mark("plan + allocations");
+
+  // ---- per chunk: copy in, validate, out-degrees, row ids, classify, sort, select the PNG
+  for (int c = 0; c < nck; ++c) {
+    const int64_t p0 = cp[c], p1 = cp[c + 1];
+    const int64_t u0 = p0 * q, u1 = std::min(p1 * q, n_src), nr = u1 - u0;
+    const int64_t e0 = pb[p0], e1 = pb[p1], mc = e1 - e0;
+    if (copies) {
+      if (host_rp)
+        TK(cudaMemcpyAsync(d_rp + u0, row_ptr + u0, sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, cs));
+      if (host_col && mc)
+        TK(cudaMemcpyAsync(d_col + e0, col + e0, sizeof(uint32_t) * mc, cudaMemcpyHostToDevice, cs));
+      if (host_val && mc)
+        TK(cudaMemcpyAsync(d_val + e0, values + e0, sizeof(float) * mc, cudaMemcpyHostToDevice, cs));
+      TK(cudaEventRecord(evs[c], cs));
+      TK(cudaStreamWaitEvent(s, evs[c], 0));
+    }
+    k_check_rows_c<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, e0, e1, err);
+    k_outdeg<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, h->outdeg, h->inv_deg, d_dang);
+    TK(cudaGetLastError());
+    if (mc == 0) continue;
+    uint32_t* rid = pull ? rowid + e0 : rowid;
+    TK(cudaMemsetAsync(mark, 0, sizeof(uint32_t) * mc, s));
+    k_mark_rows_c<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, e0, e1, mark);
+    TK(cudaGetLastError());
+    size_t bt = b_cub;
+    TK(cub::DeviceScan::InclusiveScan(cub_tmp, bt, mark, rid, MaxOp(), mc, s));
+    k_classify_c<P><<<grid_for(mc), kT, 0, s>>>(e0, mc, d_col, d_val, rid, b, n_dst, k_dst, h->compressed, key_c,
+                                                 pay_c, err);
+    TK(cudaGetLastError());
+    bt = b_cub;
+    TK(cub::DeviceRadixSort::SortPairs(cub_tmp, bt, key_c, keys_s + e0, pay_c, pay_s + e0, mc, 0, gbits, s));
+    k_run_flags<P><<<grid_for(mc), kT, 0, s>>>(mc, pay_s + e0, fl_c);
+    TK(cudaGetLastError());
+    bt = b_cub;
+    TK(cub::DeviceSelect::Flagged(cub_tmp, bt, keys_s + e0, fl_c, fk + e0, d_cnt + c, mc, s));
+    bt = b_cub;
+    TK(cub::DeviceSelect::Flagged(cub_tmp, bt, pay_s + e0, fl_c, fp + e0, d_cnt + nck + c, mc, s));
+  }
+  std::vector<int64_t> hcnt(nck);
+  uint32_t herr[4] = {0, 0, 0, 0};
+  if (nck) TK(cudaMemcpyAsync(hcnt.data(), d_cnt, sizeof(int64_t) * nck, cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(herr, err, 16, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  if (herr[0] & 1u) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+  if (herr[0] & 2u) {
+    set_error(PCPM_EBADCSR, "col_idx has an entry >= n_dst");
+    return PCPM_EBADCSR;
+  }
+  if (herr[0] & 4u) {
+    set_error(PCPM_EBADCSR, "a row's columns are not strictly increasing (sorted, deduplicated) (R6)");
+    return PCPM_EBADCSR;
+  }
+  int64_t ep = 0;
+  for (int c = 0; c < nck; ++c) ep += hcnt[c];
+  h->e_prime = ep;
+  pt.mark("chunks: copy + sort");
+
+  // ---- destID bins: group starts in sorted order, column scans, placement
+  uint32_t *Gs, *id_off, *col_tot;
+  TK(tmp.alloc(&Gs, ng + 1));
+  TK(tmp.alloc(&id_off, ng));
   TK(tmp.alloc(&col_tot, k_dst + 1));
-  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, G, h->upd_off, col_tot);
+  k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keys_s, ng, Gs);
+  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, Gs, id_off, col_tot);
+  TK(cudaGetLastError());
   TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
   {
     size_t bytes = 0;
-    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, col_tot, h->bin_id_start, k_dst + 1, s));
     uint8_t* t;
     TK(tmp.alloc(&t, bytes));
-    TK(cub::DeviceScan::ExclusiveSum(t, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, col_tot, h->bin_id_start, k_dst + 1, s));
   }
-  k_add_bin_start<<<grid_for(k_src * k_dst), kT, 0, s>>>(k_src, k_dst, h->bin_upd_start, h->upd_off);
+  k_add_bin_start<<<grid_for(ng), kT, 0, s>>>(k_src, k_dst, h->bin_id_start, id_off);
+  k_place_ids<P><<<grid_for(m), kT, 0, s>>>(m, keys_s, pay_s, Gs, id_off, b, k_dst, h->ids16, ids32, h->w);
   TK(cudaGetLastError());
+  pt.mark("destID bins");
 
-  // ---- decode anchors: chunk_base[c] = #flags in ids[0 .. c*kChunkIds)
-  {
-    uint32_t* cnt;
-    TK(tmp.alloc(&cnt, nchunks + 1));
-    k_chunk_counts<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, ids32, cnt);
+  // ---- PNG: the chunks' flagged edges concatenated
+  uint32_t* png32 = nullptr;
+  if (h->wide && (rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+  png32 = h->png_src;
+  if ((rc = dev_alloc_t(h, &h->png16, ep + 16))) return rc;
+  if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
+  TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+  TK(cudaMemsetAsync(h->png16 + ep, 0, sizeof(uint16_t) * 16, s));
+  if (png32) TK(cudaMemsetAsync(png32 + ep, 0, sizeof(uint32_t) * 8, s));
+  uint32_t *pk, *G;
+  TK(tmp.alloc(&pk, ep));
+  TK(tmp.alloc(&G, ng + 1));
+  int64_t off = 0;
+  for (int c = 0; c < nck; ++c) {
+    if (hcnt[c] == 0) continue;
+    const int64_t e0 = pb[cp[c]];
+    k_png_place<P><<<grid_for(hcnt[c]), kT, 0, s>>>(hcnt[c], fk + e0, fp + e0, off, b, k_dst, pk, h->png16, png32);
     TK(cudaGetLastError());
-    size_t bytes = 0;
-    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, h->chunk_base, nchunks + 1, s));
-    uint8_t* t;
-    TK(tmp.alloc(&t, bytes));
-    TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, h->chunk_base, nchunks + 1, s));
+    off += hcnt[c];
   }
-
-  pt.mark("pull CSC + offsets + anchors");
-  // ---- host-side work lists (small copies)
-  std::vector<uint32_t> hbin(k_dst + 1), hG(k_src * k_dst + 1);
-  unsigned long long hdang = 0;
-  TK(cudaMemcpyAsync(hbin.data(), h->bin_id_start, sizeof(uint32_t) * (k_dst + 1), cudaMemcpyDeviceToHost, s));
-  TK(cudaMemcpyAsync(hG.data(), G, sizeof(uint32_t) * (k_src * k_dst + 1), cudaMemcpyDeviceToHost, s));
-  TK(cudaMemcpyAsync(&hdang, d_dang, 8, cudaMemcpyDeviceToHost, s));
-  TK(cudaStreamSynchronize(s));
-  h->n_dangling = (int64_t)hdang;
-
-  // gather items: every destination partition gets >= 1 item (its apply runs even
-  // when the bin is empty); heavy bins are cut at tile-aligned points so no
-  // item exceeds ~m / (2 SMs) IDs; largest first (LPT, the GPU analogue of the
-  // paper's dynamic scheduling, P:434).
-  std::vector<GatherItem> gi;
-  std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
-  uint32_t nslots = 0;
-  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (2 * h->num_sms)) / kTileAlign + 1) * kTileAlign);
-  for (int64_t j = 0; j < k_dst; ++j) {
-    int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
-    int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
-    int64_t per = (sz + nslc - 1) / nslc;
-    std::vector<int64_t> cuts{s0};
-    for (int64_t i = 1; i < nslc; ++i) {
-      int64_t c = ((s0 + i * per + kTileAlign - 1) / kTileAlign) * kTileAlign;
-      if (c > cuts.back() && c < s1) cuts.push_back(c);
-    }
-    cuts.push_back(s1);
-    const uint32_t ns = (uint32_t)(cuts.size() - 1);
-    // slices of a split bin each own a slot: a q-word buffer for their low words
-    sbase[j] = ns > 1 ? nslots : 0u;
-    for (size_t i = 0; i + 1 < cuts.size(); ++i) {
-      GatherItem it{};
-      it.j = (uint32_t)j;
-      it.x0 = (uint32_t)cuts[i];
-      it.x1 = (uint32_t)cuts[i + 1];
-      it.pad[0] = ns > 1 ? nslots + (uint32_t)i : 0xFFFFFFFFu;
-      gi.push_back(it);
-    }
-    nsl[j] = ns;
-    if (ns > 1) nslots += ns;
-  }
-  std::stable_sort(gi.begin(), gi.end(),
-                   [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
-  h->n_gitems = (int)gi.size();
-  if ((rc = dev_alloc_t(h, &h->gitems, gi.size()))) return rc;
-  if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
-  TK(cudaMemcpyAsync(h->gitems, gi.data(), sizeof(GatherItem) * gi.size(), cudaMemcpyHostToDevice, s));
-  TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
-  if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_dst))) return rc;
-  TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
-  h->n_slots = nslots;
+  k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk, ng, G);
   {
-    std::vector<uint32_t> sb;
-    for (int64_t j = 0; j < k_dst; ++j)
-      if (nsl[j] > 1) sb.push_back((uint32_t)j);
-    h->n_split_bins = (int)sb.size();
-    if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
-    if (!sb.empty())
-      TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
-    const int64_t blocks = (int64_t)sb.size() * ((q + 1023) / 1024);
-    if ((rc = dev_alloc_t(h, &h->split_red, std::max<int64_t>(2, 2 * blocks)))) return rc;
+    const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
+    if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;
+    k_grp_at<<<grid_for(nga), kT, 0, s>>>(ep, pk, nga, h->grp_at);
+    TK(cudaGetLastError());
   }
-  if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
-  k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
-  TK(cudaGetLastError());
+  pt.mark("PNG arrays");
 
-  // scatter items: (p, [j0, j1)) holding ~E' / (2 SMs) updates each
-  std::vector<ScatterItem> si;
-  int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
-  for (int64_t p = 0; p < k_src; ++p) {
-    int64_t acc = 0, j0 = 0;
-    for (int64_t j = 0; j < k_dst; ++j) {
-      acc += hG[p * k_dst + j + 1] - hG[p * k_dst + j];
-      if (acc >= target || j + 1 - j0 >= kScatterMaxGroups) {   // item offsets fit in smem
-        si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)(j + 1), (uint32_t)acc});
-        acc = 0;
-        j0 = j + 1;
-      }
-    }
-    if (acc > 0) si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)k_dst, (uint32_t)acc});
+  // ---- pull comparison: CSC (in-adjacency), sources ascending per destination
+  if (pull) {
+    if ((rc = dev_alloc_t(h, &h->in_ptr, n_dst + 1))) return rc;
+    if ((rc = dev_alloc_t(h, &h->in_src, m))) return rc;
+    uint32_t *ck, *ck_s, *cperm, *iota;
+    TK(tmp.alloc(&ck, m));
+    TK(tmp.alloc(&ck_s, m));
+    TK(tmp.alloc(&cperm, m));
+    TK(tmp.alloc(&iota, m));
+    k_iota<<<grid_for(m), kT, 0, s>>>(m, iota);
+    TK(cudaMemcpyAsync(ck, d_col, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
+    TK(radix_sort_pairs(tmp, ck, ck_s, iota, cperm, m, bits_for((uint64_t)std::max<int64_t>(n_dst - 1, 0)), s));
+    k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, ck_s, n_dst, h->in_ptr);
+    TK(cudaGetLastError());
+    k_gather_u32<<<grid_for(m), kT, 0, s>>>(m, cperm, rowid, h->in_src);
+    TK(cudaGetLastError());
+    h->has_pull = true;
   }
-  h->n_sitems = (int)si.size();
-  h->sitems_host = si;                     // source-partition order (see order_scatter_items)
-  if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(si.size(), 1)))) return rc;
-  if ((rc = order_scatter_items(h, s))) return rc;
+  // ---- max|w| (fixed-point range of the signed SpMV accumulator)
+  if (values) {
+    float* mx;
+    TK(tmp.alloc(&mx, 1));
+    float hmx = 0.f;
+    int rc2 = launch_absmax(h, d_val, m, mx, s);
+    if (rc2) return rc2;
+    TK(cudaMemcpyAsync(&hmx, mx, 4, cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+    int ex = 0;
+    if (hmx > 0.f) frexpf(hmx, &ex);
+    h->wexp = ex;
+  }
+  return finish_layout(h, tmp, pt, G, d_dang);
+}
 
-  // ---- iteration scratch (kept zero between uses by the kernels)
-  const int64_t nv = std::max(n_src, n_dst);
-  if ((rc = dev_alloc_t(h, &h->pr[0], nv + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->pr[1], nv + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->spr, n_src + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->xbuf, n_src + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
-  if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
-  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
-  if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
-  if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
-  TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
-  TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
-  TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
-  TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
-  TK(cudaStreamSynchronize(s));
-  pt.mark("work lists + iteration state");
-  return PCPM_OK;
+}  // namespace
+
+// Layout construction: the chunked sort (default) or the two-sort legacy path
+// (PCPM_BUILD_LEGACY=1, and graphs without edges).
+int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+  const bool legacy = getenv("PCPM_BUILD_LEGACY") != nullptr;
+  if (legacy || csr->nnz == 0 || csr->n_src <= 0 || csr->n_dst <= 0) return build_layout_legacy(h, csr, flags);
+  return csr->values ? build_layout_chunked<PayW>(h, csr, flags) : build_layout_chunked<uint32_t>(h, csr, flags);
 }
 
 // Claim order of the scatter items.  Default (opt_scatter_lpt = 0): ascending p, so the
@@ -786,7 +1191,7 @@ int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t 
   unsigned long long* d_dang;
   TK(tmp.alloc(&d_dang, 1));
   TK(cudaMemsetAsync(d_dang, 0, 8, s));
-  k_outdeg<<<grid_for(n), kT, 0, s>>>(n, row_ptr, h->outdeg, h->inv_deg, d_dang);
+  k_outdeg<<<grid_for(n), kT, 0, s>>>(0, n, row_ptr, h->outdeg, h->inv_deg, d_dang);
   TK(cudaGetLastError());
   unsigned long long hd = 0;
   TK(cudaMemcpyAsync(&hd, d_dang, 8, cudaMemcpyDeviceToHost, s));

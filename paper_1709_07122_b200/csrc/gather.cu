@@ -104,6 +104,14 @@ __device__ unsigned long long g_gather_prof[8];
 #ifndef PCPM_GATHER_PROFILE
 #define PCPM_GATHER_PROFILE 0
 #endif
+// Timing-only experiment builds (results are wrong): NOOP = consumers release
+// stages without decoding (the producer's streaming rate); NO_EPI = skip the apply.
+#ifndef PCPM_GATHER_NOOP
+#define PCPM_GATHER_NOOP 0
+#endif
+#ifndef PCPM_GATHER_NO_EPI
+#define PCPM_GATHER_NO_EPI 0
+#endif
 
 __device__ int spmv_fbits(float xmax, int wexp) {
   int ex = 0;
@@ -304,8 +312,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   uint32_t phase = 0;
   unsigned long long pt[4] = {0, 0, 0, 0};
   long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
+#ifndef PCPM_GATHER_WAIT_HINT
+#define PCPM_GATHER_WAIT_HINT 0
+#endif
   for (;;) {
-    mbar_wait(&full[stage], phase);
+    if (PCPM_GATHER_WAIT_HINT) mbar_wait_sleep(&full[stage], phase, PCPM_GATHER_WAIT_HINT);
+    else mbar_wait(&full[stage], phase);
     if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[0] += t - tc; tc = t; }
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
       auto process = [&](const int sc) {
       const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
-      if (xs < m.hi && xs + C::kSub > m.lo) {
+      if (!PCPM_GATHER_NOOP && xs < m.hi && xs + C::kSub > m.lo) {
         const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
         auto body = [&](auto WHOLE) {
           constexpr bool kWhole = decltype(WHOLE)::value;
@@ -487,6 +499,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
         return tot;
       };
       double dang = 0.0, res = 0.0;
+      if (PCPM_GATHER_NO_EPI) run_apply = false;
       if (run_apply) {
         if constexpr (PR) {
           const bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&

@@ -386,3 +386,41 @@ def test_kernel_variants_keep_parity(pcpm, opts):
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     finally:
         pcpm.pcpm_destroy(h)
+
+
+CHUNK_CASES = [
+    ("c1", lambda: graphs.make_config("c1"), 8, False, 0),
+    ("rmat13_b6_host", lambda: graphs.make_graph("rmat", 8, scale=13, permute=True), 6, True, 0),
+    ("rmat12_b4_weights", lambda: graphs.make_graph("rmat", 9, scale=12, permute=True, values=True,
+                                                    transpose=True), 4, True, 0),
+    ("er_ragged_b9_wide", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 9, False, 8),
+    ("outstar_b5", lambda: star_graph(20000), 5, True, 0),
+    ("rmat11_b3_nocompress", lambda: graphs.make_graph("rmat", 3, scale=11, permute=True), 3, False, 1),
+]
+
+
+@pytest.mark.parametrize("name,mk,b,host,flags", CHUNK_CASES, ids=[c[0] for c in CHUNK_CASES])
+@pytest.mark.parametrize("chunk_edges", ["1", "777", "legacy"])
+def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, chunk_edges):
+    """The chunked build (chunks of whole source partitions, copied in and sorted
+    one by one) gives the oracle's layout for any chunk size, host or device
+    inputs, weights, wide IDs and uncompressed bins; so does the legacy path."""
+    if chunk_edges == "legacy":
+        monkeypatch.setenv("PCPM_BUILD_LEGACY", "1")
+    else:
+        monkeypatch.setenv("PCPM_BUILD_CHUNK_EDGES", chunk_edges)
+    g = mk()
+    h = build(pcpm, g, b, device=not host, flags=flags)
+    try:
+        lay = export(pcpm, h)
+        if flags & 1:                          # PCPM_NO_COMPRESS: every ID flagged
+            ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, b)
+            assert lay["info"].e_prime == g.m
+            np.testing.assert_array_equal(lay["ids16"] >> 15, np.ones(g.m, np.uint16))
+            np.testing.assert_array_equal(lay["ids16"] & np.uint16(0x7FFF),
+                                          (ref.ids & np.uint32((1 << b) - 1)).astype(np.uint16))
+            np.testing.assert_array_equal(lay["bin_id_start"], ref.bin_id_start.astype(np.uint32))
+        else:
+            assert_layout_equal(g, lay, b)
+    finally:
+        pcpm.pcpm_destroy(h)
