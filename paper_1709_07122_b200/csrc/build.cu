@@ -150,17 +150,88 @@ __global__ void k_png_off(int64_t k_src, int64_t k_dst, const uint32_t* __restri
   }
 }
 
-// Column scans of the group sizes: upd_off[p][j] = sum_{p'<p} |(p', j)|, col_tot[j].
-__global__ void k_col_scan(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, uint32_t* upd_off,
-                           uint32_t* col_tot) {
-  GRID_STRIDE(j, k_dst) {
+// Column scans of the group sizes: out[p][j] = sum_{p'<p} |(p', j)|, col_tot[j].
+// Block = 32 columns x 32 row segments: segment sums, a scan over the segments, then
+// each segment's running offsets (coalesced over j).
+__global__ void __launch_bounds__(1024) k_col_scan(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G,
+                                                   uint32_t* out, uint32_t* col_tot) {
+  __shared__ uint32_t part[32][33];
+  const int64_t j = blockIdx.x * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  const int64_t per = (k_src + 31) / 32;
+  const int64_t p0 = min(k_src, y * per), p1 = min(k_src, p0 + per);
+  uint32_t sum = 0;
+  if (j < k_dst)
+    for (int64_t p = p0; p < p1; ++p) sum += G[p * k_dst + j + 1] - G[p * k_dst + j];
+  part[y][threadIdx.x] = sum;
+  __syncthreads();
+  if (y == 0) {
     uint32_t run = 0;
-    for (int64_t p = 0; p < k_src; ++p) {
-      int64_t g = p * k_dst + j;
-      upd_off[g] = run;
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t t = part[k][threadIdx.x];
+      part[k][threadIdx.x] = run;
+      run += t;
+    }
+    if (j < k_dst) col_tot[j] = run;
+  }
+  __syncthreads();
+  uint32_t run = part[y][threadIdx.x];
+  if (j < k_dst)
+    for (int64_t p = p0; p < p1; ++p) {
+      const int64_t g = p * k_dst + j;
+      out[g] = run;
       run += G[g + 1] - G[g];
     }
-    col_tot[j] = run;
+}
+inline void col_scan(int64_t k_src, int64_t k_dst, const uint32_t* G, uint32_t* out, uint32_t* col_tot,
+                     cudaStream_t s) {
+  k_col_scan<<<(unsigned)((k_dst + 31) / 32), dim3(32, 32), 0, s>>>(k_src, k_dst, G, out, col_tot);
+}
+
+// starts[g] = base + first x with keys[x] >= g, for g in [g0, g1]; keys (n of them)
+// sorted and in [g0, g1).  n and base may come from device memory (n_dev, base_dev).
+__global__ void k_bounds_range(int64_t n_max, const int64_t* n_dev, const uint32_t* __restrict__ keys, int64_t g0,
+                               int64_t g1, int64_t base, const int64_t* base_dev, uint32_t* starts) {
+  const int64_t n = n_dev ? *n_dev : n_max;
+  const int64_t b0 = base_dev ? *base_dev : base;
+  GRID_STRIDE(x, n + 1) {
+    const int64_t kx = x < n ? (int64_t)keys[x] : g1;
+    const int64_t kp = x > 0 ? (int64_t)keys[x - 1] : g0 - 1;
+    for (int64_t k = kp + 1; k <= kx; ++k) starts[k] = static_cast<uint32_t>(b0 + x);
+  }
+}
+
+// Scatter work items (p, [j0, j1)) of ~target updates (at most maxg groups), one warp
+// per source partition p: count pass (out == nullptr) or fill pass at off[p].
+__global__ void k_sitems(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, int64_t target, int maxg,
+                         const uint32_t* __restrict__ off, uint32_t* cnt, ScatterItem* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = w0; p < k_src; p += nw) {
+    uint32_t n = 0, j0 = 0;
+    int64_t acc = 0;
+    const uint32_t o = out ? off[p] : 0u;
+    for (int64_t jb = 0; jb < k_dst; jb += 32) {
+      const int64_t jl = jb + lane;
+      const uint32_t sz = jl < k_dst ? G[p * k_dst + jl + 1] - G[p * k_dst + jl] : 0u;
+      const int nt = (int)(k_dst - jb < 32 ? k_dst - jb : 32);
+      for (int t = 0; t < nt; ++t) {
+        acc += __shfl_sync(0xffffffffu, sz, t);
+        const uint32_t jj = (uint32_t)(jb + t);
+        if (acc >= target || jj + 1 - j0 >= (uint32_t)maxg) {      // item offsets fit in smem
+          if (out && lane == 0) out[o + n] = ScatterItem{(uint32_t)p, j0, jj + 1, (uint32_t)acc};
+          ++n;
+          acc = 0;
+          j0 = jj + 1;
+        }
+      }
+    }
+    if (acc > 0) {
+      if (out && lane == 0) out[o + n] = ScatterItem{(uint32_t)p, j0, (uint32_t)k_dst, (uint32_t)acc};
+      ++n;
+    }
+    if (!out && lane == 0) cnt[p] = n;
   }
 }
 
@@ -339,10 +410,15 @@ __global__ void k_place_ids(int64_t m, const uint32_t* __restrict__ keys, const 
   }
 }
 
-// PNG: chunk c's flagged edges (in group order) to positions off .. off + n.
+// PNG, per chunk: its n = *n_dev flagged edges (in group order) go to positions
+// off .. off + n, off = *off_dev (the flagged edges of the earlier chunks);
+// *off_next = off + n.
 template <typename P>
-__global__ void k_png_place(int64_t n, const uint32_t* __restrict__ fk, const P* __restrict__ fp, int64_t off,
-                            int b, int64_t k_dst, uint32_t* pk, uint16_t* png16, uint32_t* png32) {
+__global__ void k_png_place_c(const int64_t* __restrict__ n_dev, const int64_t* off_dev, int64_t* off_next,
+                              const uint32_t* __restrict__ fk, const P* __restrict__ fp, int b, int64_t k_dst,
+                              uint32_t* pk, uint16_t* png16, uint32_t* png32) {
+  const int64_t n = *n_dev, off = *off_dev;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *off_next = off + n;
   GRID_STRIDE(i, n) {
     const uint32_t g = fk[i];
     const uint32_t ul = pay_word(fp[i]) >> 16;
@@ -351,6 +427,7 @@ __global__ void k_png_place(int64_t n, const uint32_t* __restrict__ fk, const P*
     if (png32) png32[off + i] = (g / (uint32_t)k_dst) << b | ul;
   }
 }
+
 
 // PCPM_BUILD_TIMING=1: synchronise and print the wall time of each build phase (stderr).
 struct PhaseTimer {
@@ -420,7 +497,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   k_png_off<<<grid_for(k_src * (k_dst + 1)), kT, 0, s>>>(k_src, k_dst, G, h->png_off);
   uint32_t* col_tot;
   TK(tmp.alloc(&col_tot, k_dst + 1));
-  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, G, h->upd_off, col_tot);
+  col_scan(k_src, k_dst, G, h->upd_off, col_tot, s);
   TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
   {
     size_t bytes = 0;
@@ -447,13 +524,35 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
 
   pt.mark("pull CSC + offsets + anchors");
   // ---- host-side work lists (small copies)
-  std::vector<uint32_t> hbin(k_dst + 1), hG(k_src * k_dst + 1);
+  // scatter items (p, [j0, j1)) holding ~E' / (2 SMs) updates each, counted on the device
+  const int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
+  uint32_t *si_cnt, *si_off;
+  TK(tmp.alloc(&si_cnt, k_src + 1));
+  TK(tmp.alloc(&si_off, k_src + 1));
+  TK(cudaMemsetAsync(si_cnt + k_src, 0, 4, s));
+  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, nullptr, si_cnt, nullptr);
+  TK(cudaGetLastError());
+  {
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, si_cnt, si_off, k_src + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, si_cnt, si_off, k_src + 1, s));
+  }
+  std::vector<uint32_t> hbin(k_dst + 1);
   unsigned long long hdang = 0;
+  uint32_t n_si = 0;
   TK(cudaMemcpyAsync(hbin.data(), h->bin_id_start, sizeof(uint32_t) * (k_dst + 1), cudaMemcpyDeviceToHost, s));
-  TK(cudaMemcpyAsync(hG.data(), G, sizeof(uint32_t) * (k_src * k_dst + 1), cudaMemcpyDeviceToHost, s));
   TK(cudaMemcpyAsync(&hdang, d_dang, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(&n_si, si_off + k_src, 4, cudaMemcpyDeviceToHost, s));
   TK(cudaStreamSynchronize(s));
   h->n_dangling = (int64_t)hdang;
+  h->n_sitems = (int)n_si;
+  if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(n_si, 1)))) return rc;
+  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, si_off, nullptr,
+                                               h->sitems);
+  TK(cudaGetLastError());
+  if (h->opt_scatter_lpt && (rc = order_scatter_items(h, s))) return rc;
 
   // gather items: every destination partition gets >= 1 item (its apply runs even
   // when the bin is empty); heavy bins are cut at tile-aligned points so no
@@ -511,26 +610,6 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
   TK(cudaGetLastError());
-
-  // scatter items: (p, [j0, j1)) holding ~E' / (2 SMs) updates each
-  std::vector<ScatterItem> si;
-  int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
-  for (int64_t p = 0; p < k_src; ++p) {
-    int64_t acc = 0, j0 = 0;
-    for (int64_t j = 0; j < k_dst; ++j) {
-      acc += hG[p * k_dst + j + 1] - hG[p * k_dst + j];
-      if (acc >= target || j + 1 - j0 >= kScatterMaxGroups) {   // item offsets fit in smem
-        si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)(j + 1), (uint32_t)acc});
-        acc = 0;
-        j0 = j + 1;
-      }
-    }
-    if (acc > 0) si.push_back(ScatterItem{(uint32_t)p, (uint32_t)j0, (uint32_t)k_dst, (uint32_t)acc});
-  }
-  h->n_sitems = (int)si.size();
-  h->sitems_host = si;                     // source-partition order (see order_scatter_items)
-  if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(si.size(), 1)))) return rc;
-  if ((rc = order_scatter_items(h, s))) return rc;
 
   // ---- iteration scratch (kept zero between uses by the kernels)
   const int64_t nv = std::max(n_src, n_dst);
@@ -909,6 +988,18 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(tmp.alloc(&key_c, mc_max));
   TK(tmp.alloc(&pay_c, mc_max));
   TK(tmp.alloc(&fl_c, mc_max));
+  // group starts in sorted-edge order (Gs) and in the PNG (G), PNG arrays at their
+  // final positions (exact-size copies at the end), filled chunk by chunk
+  uint32_t *Gs, *G, *pk, *png32_t = nullptr;
+  uint16_t* png16_t;
+  int64_t* d_off;
+  TK(tmp.alloc(&Gs, ng + 1));
+  TK(tmp.alloc(&G, ng + 1));
+  TK(tmp.alloc(&pk, m));
+  TK(tmp.alloc(&png16_t, m));
+  if (h->wide) TK(tmp.alloc(&png32_t, m));
+  TK(tmp.alloc(&d_off, nck + 1));
+  TK(cudaMemsetAsync(d_off, 0, sizeof(int64_t) * (nck + 1), s));
   TK(cudaMemsetAsync(err, 0, 16, s));
   TK(cudaMemsetAsync(d_dang, 0, 8, s));
   TK(cudaMemsetAsync(d_cnt, 0, sizeof(int64_t) * (2 * nck + 2), s));
@@ -960,7 +1051,14 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     k_check_rows_c<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, e0, e1, err);
     k_outdeg<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, h->outdeg, h->inv_deg, d_dang);
     TK(cudaGetLastError());
-    if (mc == 0) continue;
+    const int64_t g0 = p0 * k_dst, g1 = p1 * k_dst;
+    if (mc == 0) {
+      k_bounds_range<<<1, kT, 0, s>>>(0, nullptr, keys_s, g0, g1, e0, nullptr, Gs);
+      k_png_place_c<P><<<1, kT, 0, s>>>(d_cnt + c, d_off + c, d_off + c + 1, fk, fp, b, k_dst, pk, png16_t, png32_t);
+      k_bounds_range<<<1, kT, 0, s>>>(0, d_cnt + c, fk, g0, g1, 0, d_off + c, G);
+      TK(cudaGetLastError());
+      continue;
+    }
     uint32_t* rid = pull ? rowid + e0 : rowid;
     TK(cudaMemsetAsync(mark, 0, sizeof(uint32_t) * mc, s));
     k_mark_rows_c<<<grid_for(nr), kT, 0, s>>>(u0, nr, d_rp, e0, e1, mark);
@@ -978,6 +1076,12 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(cub::DeviceSelect::Flagged(cub_tmp, bt, keys_s + e0, fl_c, fk + e0, d_cnt + c, mc, s));
     bt = b_cub;
     TK(cub::DeviceSelect::Flagged(cub_tmp, bt, pay_s + e0, fl_c, fp + e0, d_cnt + nck + c, mc, s));
+    // this chunk's groups: starts among the sorted edges and in the PNG
+    k_bounds_range<<<grid_for(mc + 1), kT, 0, s>>>(mc, nullptr, keys_s + e0, g0, g1, e0, nullptr, Gs);
+    k_png_place_c<P><<<grid_for(mc), kT, 0, s>>>(d_cnt + c, d_off + c, d_off + c + 1, fk + e0, fp + e0, b, k_dst,
+                                                 pk, png16_t, png32_t);
+    k_bounds_range<<<grid_for(mc + 1), kT, 0, s>>>(mc, d_cnt + c, fk + e0, g0, g1, 0, d_off + c, G);
+    TK(cudaGetLastError());
   }
   std::vector<int64_t> hcnt(nck);
   uint32_t herr[4] = {0, 0, 0, 0};
@@ -1002,12 +1106,10 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   pt.mark("chunks: copy + sort");
 
   // ---- destID bins: group starts in sorted order, column scans, placement
-  uint32_t *Gs, *id_off, *col_tot;
-  TK(tmp.alloc(&Gs, ng + 1));
+  uint32_t *id_off, *col_tot;
   TK(tmp.alloc(&id_off, ng));
   TK(tmp.alloc(&col_tot, k_dst + 1));
-  k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keys_s, ng, Gs);
-  k_col_scan<<<grid_for(k_dst), kT, 0, s>>>(k_src, k_dst, Gs, id_off, col_tot);
+  col_scan(k_src, k_dst, Gs, id_off, col_tot, s);
   TK(cudaGetLastError());
   TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
   {
@@ -1022,27 +1124,17 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(cudaGetLastError());
   pt.mark("destID bins");
 
-  // ---- PNG: the chunks' flagged edges concatenated
-  uint32_t* png32 = nullptr;
-  if (h->wide && (rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
-  png32 = h->png_src;
+  // ---- PNG: exact-size copies of the arrays the chunks filled
+  if (h->wide) {
+    if ((rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+    TK(cudaMemcpyAsync(h->png_src, png32_t, sizeof(uint32_t) * ep, cudaMemcpyDeviceToDevice, s));
+    TK(cudaMemsetAsync(h->png_src + ep, 0, sizeof(uint32_t) * 8, s));
+  }
   if ((rc = dev_alloc_t(h, &h->png16, ep + 16))) return rc;
+  TK(cudaMemcpyAsync(h->png16, png16_t, sizeof(uint16_t) * ep, cudaMemcpyDeviceToDevice, s));
+  TK(cudaMemsetAsync(h->png16 + ep, 0, sizeof(uint16_t) * 16, s));
   if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
   TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
-  TK(cudaMemsetAsync(h->png16 + ep, 0, sizeof(uint16_t) * 16, s));
-  if (png32) TK(cudaMemsetAsync(png32 + ep, 0, sizeof(uint32_t) * 8, s));
-  uint32_t *pk, *G;
-  TK(tmp.alloc(&pk, ep));
-  TK(tmp.alloc(&G, ng + 1));
-  int64_t off = 0;
-  for (int c = 0; c < nck; ++c) {
-    if (hcnt[c] == 0) continue;
-    const int64_t e0 = pb[cp[c]];
-    k_png_place<P><<<grid_for(hcnt[c]), kT, 0, s>>>(hcnt[c], fk + e0, fp + e0, off, b, k_dst, pk, h->png16, png32);
-    TK(cudaGetLastError());
-    off += hcnt[c];
-  }
-  k_boundaries<<<grid_for(ep + 1), kT, 0, s>>>(ep, pk, ng, G);
   {
     const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
     if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;
@@ -1100,7 +1192,13 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 // same time -- the boundary sectors between group (p, j) and (p+1, j) are completed in L2
 // instead of being written back partially.  1: largest first (LPT).
 int order_scatter_items(pcpm_handle* h, cudaStream_t s) {
-  std::vector<ScatterItem> si = h->sitems_host;
+  std::vector<ScatterItem> si(h->n_sitems);
+  if (si.empty()) return PCPM_OK;
+  TK(cudaMemcpyAsync(si.data(), h->sitems, sizeof(ScatterItem) * si.size(), cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  // natural order: (p, j0) ascending; LPT: largest first, ties in natural order
+  std::sort(si.begin(), si.end(),
+            [](const ScatterItem& a, const ScatterItem& c) { return a.p != c.p ? a.p < c.p : a.j0 < c.j0; });
   if (h->opt_scatter_lpt)
     std::stable_sort(si.begin(), si.end(), [](const ScatterItem& a, const ScatterItem& c) { return a.pad > c.pad; });
   if (!si.empty())

@@ -98,7 +98,6 @@ struct pcpm_handle {
   uint32_t* bin_nslices = nullptr;  // [k_dst]
   pcpm::ScatterItem* sitems = nullptr;
   int n_sitems = 0;
-  std::vector<pcpm::ScatterItem> sitems_host;
 
   // iteration state
   float* pr[2] = {nullptr, nullptr};// [n]
