@@ -5,7 +5,12 @@ mkdir -p gpurun_out
 cfgs=$1; shift
 for c in $cfgs; do for t in "$@"; do
   lib=""
-  case "$t" in base) ;; o_*) lib="--opt ${t#o_}" ;; *) lib="--lib paper_1709_07122_b200/libpcpm_$t.so" ;; esac
+  case "$t" in
+    base) ;;
+    o_*) lib="--opt ${t#o_}" ;;
+    *:*) lib="--lib paper_1709_07122_b200/libpcpm_${t%%:*}.so --opt ${t#*:}" ;;   # lib:key=val
+    *) lib="--lib paper_1709_07122_b200/libpcpm_$t.so" ;;
+  esac
   timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-pull $lib --out gpurun_out/ab_raw.jsonl > gpurun_out/ab_${c}_$t.log 2>&1
   python - "$c" "$t" <<'PY'
 import json,sys
