@@ -299,10 +299,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   double base_pr = 0.0;
   if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
   // SpMV scale: F = 30 - ceil(log2 max|w|) - ceil(log2 max|x|), so |w x| 2^F <= 2^30
-  double sp_scale = 1.0, sp_inv = 1.0;
+  double sp_inv = 1.0;
+  float sp_scale_f = 1.0f;
   if constexpr (!PR) {
     const int F = spmv_fbits(*a.xmax, a.wexp);
-    sp_scale = ldexp(1.0, F);
+    sp_scale_f = ldexpf(1.0f, F);       // 2^F, F in [-120, 62]: a normal fp32
     sp_inv = ldexp(1.0, -F);
   }
   named_bar_sync(1, kCons);
@@ -391,15 +392,16 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             // word is read as a signed int32, so a running sum that hovers
             // around zero never wraps; only signed overflow of the low word
             // (|partial| >= 2^31 units) carries +-1 into the global high word.
-            // w*x is exact in fp64; F keeps |w x| 2^F <= 2^30 (R19).
+            // w*x is rounded once to fp32 (<= 2^-24 |w x|, R22); F keeps
+            // |w x| 2^F <= 2^30, so each term T is an int32 and the high part of the
+            // balanced form is zero: only the low word's signed overflow carries.
             uint32_t tlo[P], old[P];
             int32_t thi[P];
 #pragma unroll
             for (int c = 0; c < P; ++c) {
-              const double tv = W ? (double)val[c] * (double)w_s[sc * C::kSub + c * 32 + lane] : (double)val[c];
-              const long long T = __double2ll_rn(tv * sp_scale);
-              tlo[c] = (uint32_t)T;
-              thi[c] = (int32_t)(T >> 32) + ((int32_t)tlo[c] < 0 ? 1 : 0);   // T = thi*2^32 + (int32)tlo
+              const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+              tlo[c] = (uint32_t)__float2int_rn(tv * sp_scale_f);
+              thi[c] = 0;
             }
 #pragma unroll
             for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
