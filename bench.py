@@ -312,7 +312,13 @@ def run_sharded(args, world, rank, local):
     b = args.bits or g.meta["bits"]
     n, m = g.n_src, g.m
     stream = torch.cuda.current_stream()
-    sh = pdist.ShardedPageRank(n, g.row_ptr, g.col, b, device=dev, stream=stream, timing=True)
+    sh = pdist.ShardedPageRank(n, g.row_ptr, g.col, b, device=dev, stream=stream, timing=True,
+                               exchange=args.exchange)
+    exchange = sh.exchange
+    exchange_desc = ("SPR stored to every rank by the gather's apply (NVLink P2P, pcpm_shard_step_peers)"
+                     if exchange == "p2p" else "NCCL all-gather of SPR") + " + all-reduce of (res, D)"
+    if sh.exchange_note:
+        exchange_desc += "; " + sh.exchange_note
     info = sh.info()
     rp_h = col_h = None
     if not args.no_e2e:
@@ -364,7 +370,7 @@ def run_sharded(args, world, rank, local):
             torch.cuda.synchronize()
             barrier(world)
             t0 = time.perf_counter()
-            s2 = pdist.ShardedPageRank(n, rp_h, col_h, b, device=dev, stream=stream)
+            s2 = pdist.ShardedPageRank(n, rp_h, col_h, b, device=dev, stream=stream, exchange=exchange)
             pr_host = s2.run(0.85, iters).cpu()
             s2.close()
             torch.cuda.synchronize()
@@ -384,7 +390,7 @@ def run_sharded(args, world, rank, local):
         "dtype": "f32 values, i64 fixed-point accumulation, f64 apply", "data": "synthetic (seeded RMAT/ER, inputs/)",
         "config": {"workload": WORKLOADS[key], "n": n, "m": m, "iters": iters, "partition_bits": b,
                    "l2": "inputs larger than L2 (no flush)",
-                   "parallelism": f"destination shards x{world}, NCCL all-gather of SPR + all-reduce of (res, D)"},
+                   "parallelism": f"destination shards x{world}, {exchange_desc}"},
         "phases_ms_per_step_max_over_ranks": {"shard_compute": round(comp_max, 4), "exchange": round(comm_max, 4)},
         "roofline": {"bound": "hbm", "kernel": "scatter+gather_apply (rank 0 shard)", "achieved": round(shard_gbs, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(shard_gbs / peak, 4), "traffic": None,
@@ -587,6 +593,8 @@ def main():
     ap.add_argument("--no-compress", action="store_true",
                     help="uncompressed bins: one update per edge (the BVGAS-like traffic of Eq. 4)")
     ap.add_argument("--sharded", action="store_true", help="use the destination-sharded path even at N=1")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "allgather"],
+                    help="N>1 sharded PageRank: SPR exchange fused into the gather (P2P stores) or NCCL all-gather")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: run N independent replicas instead of one destination-sharded graph")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")

@@ -164,6 +164,35 @@ int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0);
 int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
                     float* pr_new, float* spr_out, double* red_out);
 
+/* pcpm_shard_step_peers: pcpm_shard_step with the SPR exchange fused into the apply
+ * (DESIGN.md §7).  The gather's epilogue stores every SPR_{t+1} vertex group it
+ * produces to all of spr_outs[0 .. n_outs): spr_outs[0] is this rank's own chunk
+ * (as pcpm_shard_step's spr_out), spr_outs[1..] the same chunk in the other ranks'
+ * full-SPR buffers -- peer device memory opened with pcpm_ipc_open, written over
+ * NVLink / NVSwitch as the tiles finish -- so no all-gather follows.  spr_outs is a
+ * HOST array of n_outs (1 .. PCPM_MAX_PEERS + 1) DEVICE pointers, each 16-byte
+ * aligned for the vector path.  The gather ends with a system-scope fence: once the
+ * kernel completes its stores are visible to the peers; the caller orders each
+ * peer's next iteration after a collective (dist.py: the all-reduce of red_out).
+ * Returns 0 or PCPM_E*. */
+#define PCPM_MAX_PEERS 8
+/* pcpm_shard_init_peers: pcpm_shard_init writing SPR_0 of the slice to spr_outs[0]
+ * and copying it to spr_outs[1..] (same layout as pcpm_shard_step_peers). */
+int pcpm_shard_init_peers(pcpm_handle* h, float* pr0, float* const* spr_outs, int n_outs, double* dang0);
+int pcpm_shard_step_peers(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                          float* pr_new, float* const* spr_outs, int n_outs, double* red_out);
+/* CUDA IPC plumbing for the fused exchange (one process per GPU).
+ * pcpm_ipc_alloc / _free: a plain cudaMalloc'ed, zeroed exchange buffer (IPC handles
+ * need a whole allocation); pcpm_ipc_get_handle writes pcpm_ipc_handle_bytes() bytes
+ * describing it; pcpm_ipc_open maps another process's buffer into this one (peer
+ * access enabled lazily) and pcpm_ipc_close unmaps it.  0 or PCPM_E*. */
+int pcpm_ipc_handle_bytes(void);
+int pcpm_ipc_alloc(int64_t bytes, void** dev_ptr);
+int pcpm_ipc_free(void* dev_ptr);
+int pcpm_ipc_get_handle(void* dev_ptr, void* handle_out);
+int pcpm_ipc_open(const void* handle, void** dev_ptr_out);
+int pcpm_ipc_close(void* dev_ptr);
+
 void pcpm_destroy(pcpm_handle* h);
 
 /* Support: stream, errors, introspection. */

@@ -387,23 +387,29 @@ int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0) {
   return launch_pr_init_slice(h, pr0, spr0, dang0, std::ldexp(1.0, pr_fixed_bits(h->n_global)), h->stream);
 }
 
-int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
-                    float* pr_new, float* spr_out, double* red_out) {
-  if (!h || !spr_in || !D_in || !pr_old || !pr_new || !spr_out || !red_out) {
+static int shard_step_common(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                             float* pr_new, float* const* outs, int n_outs, double* red_out, const char* fn) {
+  if (!h || !spr_in || !D_in || !pr_old || !pr_new || !outs || !red_out) {
     set_error(PCPM_EINVAL, "NULL handle or argument");
+    return PCPM_EINVAL;
+  }
+  if (n_outs < 1 || n_outs > 1 + kMaxPeers) {
+    set_error(PCPM_EINVAL, "n_outs must be in [1, PCPM_MAX_PEERS + 1]");
     return PCPM_EINVAL;
   }
   if (!(d > 0.f && d < 1.f)) {
     set_error(PCPM_EINVAL, "d must be in (0,1)");
     return PCPM_EINVAL;
   }
-  if (!is_device_ptr(spr_in) || !is_device_ptr(D_in) || !is_device_ptr(pr_old) || !is_device_ptr(pr_new) ||
-      !is_device_ptr(spr_out) || !is_device_ptr(red_out)) {
-    set_error(PCPM_EINVAL, "pcpm_shard_step takes device pointers");
+  bool dev = is_device_ptr(spr_in) && is_device_ptr(D_in) && is_device_ptr(pr_old) && is_device_ptr(pr_new) &&
+             is_device_ptr(red_out);
+  for (int i = 0; i < n_outs; ++i) dev = dev && outs[i] && is_device_ptr(outs[i]);
+  if (!dev) {
+    set_error(PCPM_EINVAL, std::string(fn) + " takes device pointers");
     return PCPM_EINVAL;
   }
   if (!h->shard && h->n_src != h->n_dst) {
-    set_error(PCPM_ESTATE, "pcpm_shard_step needs a shard handle or a square matrix");
+    set_error(PCPM_ESTATE, std::string(fn) + " needs a shard handle or a square matrix");
     return PCPM_ESTATE;
   }
   cudaStream_t s = h->stream;
@@ -421,8 +427,90 @@ int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* 
   a.dang_out = red_out + 1;
   a.pr_old = pr_old;
   a.pr_new = pr_new;
-  a.spr_new = spr_out;
-  return launch_gather(h, a, false, true, s);                // Alg. 5 + apply on the shard's vertices
+  a.spr_new = outs[0];
+  a.n_peer = n_outs - 1;
+  for (int i = 1; i < n_outs; ++i) a.spr_peer[i - 1] = outs[i];
+  return launch_gather(h, a, false, true, s, n_outs > 1);   // Alg. 5 + apply on the shard's vertices
+}
+
+int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                    float* pr_new, float* spr_out, double* red_out) {
+  float* outs[1] = {spr_out};
+  return shard_step_common(h, d, spr_in, D_in, pr_old, pr_new, spr_out ? outs : nullptr, 1, red_out,
+                           "pcpm_shard_step");
+}
+
+int pcpm_shard_step_peers(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+                          float* pr_new, float* const* spr_outs, int n_outs, double* red_out) {
+  return shard_step_common(h, d, spr_in, D_in, pr_old, pr_new, spr_outs, n_outs, red_out, "pcpm_shard_step_peers");
+}
+
+int pcpm_shard_init_peers(pcpm_handle* h, float* pr0, float* const* spr_outs, int n_outs, double* dang0) {
+  if (!spr_outs || n_outs < 1 || n_outs > 1 + kMaxPeers) {
+    set_error(PCPM_EINVAL, "spr_outs must hold 1 .. PCPM_MAX_PEERS + 1 pointers");
+    return PCPM_EINVAL;
+  }
+  for (int i = 0; i < n_outs; ++i)
+    if (!spr_outs[i] || !is_device_ptr(spr_outs[i])) {
+      set_error(PCPM_EINVAL, "pcpm_shard_init_peers takes device pointers");
+      return PCPM_EINVAL;
+    }
+  int rc = pcpm_shard_init(h, pr0, spr_outs[0], dang0);
+  if (rc) return rc;
+  for (int i = 1; i < n_outs; ++i)           // SPR_0 of the slice to the peers (once per run)
+    PCPM_CK(cudaMemcpyAsync(spr_outs[i], spr_outs[0], sizeof(float) * h->n_dst, cudaMemcpyDefault, h->stream));
+  return PCPM_OK;
+}
+
+int pcpm_ipc_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int pcpm_ipc_alloc(int64_t bytes, void** dev_ptr) {
+  if (!dev_ptr || bytes <= 0) {
+    set_error(PCPM_EINVAL, "NULL output or bytes <= 0");
+    return PCPM_EINVAL;
+  }
+  *dev_ptr = nullptr;
+  const cudaError_t e = cudaMalloc(dev_ptr, (size_t)bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    set_error(PCPM_ENOMEM, "cudaMalloc of an exchange buffer failed");
+    return PCPM_ENOMEM;
+  }
+  PCPM_CK(e);
+  PCPM_CK(cudaMemset(*dev_ptr, 0, (size_t)bytes));
+  return PCPM_OK;
+}
+
+int pcpm_ipc_free(void* dev_ptr) {
+  if (dev_ptr) PCPM_CK(cudaFree(dev_ptr));
+  return PCPM_OK;
+}
+
+int pcpm_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) {
+    set_error(PCPM_EINVAL, "NULL pointer or handle buffer");
+    return PCPM_EINVAL;
+  }
+  cudaIpcMemHandle_t hd;
+  PCPM_CK(cudaIpcGetMemHandle(&hd, dev_ptr));
+  memcpy(handle_out, &hd, sizeof(hd));
+  return PCPM_OK;
+}
+
+int pcpm_ipc_open(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) {
+    set_error(PCPM_EINVAL, "NULL handle or output");
+    return PCPM_EINVAL;
+  }
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, handle, sizeof(hd));
+  PCPM_CK(cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return PCPM_OK;
+}
+
+int pcpm_ipc_close(void* dev_ptr) {
+  if (dev_ptr) PCPM_CK(cudaIpcCloseMemHandle(dev_ptr));
+  return PCPM_OK;
 }
 
 pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits) {

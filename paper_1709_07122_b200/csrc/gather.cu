@@ -130,7 +130,10 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
 }
 
-template <typename IdT, bool W, bool PR>
+// MULTI (PageRank shards with a fused exchange, pcpm_shard_step_peers): the apply
+// also stores each SPR group to a.spr_peer[0 .. n_peer) -- other ranks' buffers,
+// NVLink P2P -- and the kernel ends with a system-scope fence.
+template <typename IdT, bool W, bool PR, bool MULTI = false>
 __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const GatherArgs a) {
   using C = Cfg<IdT, W>;
   constexpr int S = C::kStages;
@@ -504,8 +507,10 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       if (PCPM_GATHER_NO_EPI) run_apply = false;
       if (run_apply) {
         if constexpr (PR) {
-          const bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
-                           aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0);
+          bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
+                     aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0);
+          if constexpr (MULTI)
+            for (int r = 0; r < a.n_peer; ++r) vec = vec && aligned16(a.spr_peer[r] + v0);
           if (vec) {
             const float4* id4 = reinterpret_cast<const float4*>(a.inv_deg + v0);
             const float4* po4 = reinterpret_cast<const float4*>(a.pr_old + v0);
@@ -530,6 +535,9 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
               sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
+              if constexpr (MULTI)
+                for (int r = 0; r < a.n_peer; ++r)
+                  reinterpret_cast<float4*>(a.spr_peer[r] + v0)[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
             }
           } else {
             for (int64_t i = ctid; i < cnt; i += kCons) {
@@ -538,6 +546,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
               a.pr_new[v] = (float)prn;
               const float idg = __ldg(a.inv_deg + v);
               a.spr_new[v] = (float)prn * idg * fscale;
+              if constexpr (MULTI)
+                for (int r = 0; r < a.n_peer; ++r) a.spr_peer[r][v] = (float)prn * idg * fscale;
               if (idg == 0.0f) dang += prn;
               res += fabs(prn - (double)a.pr_old[v]);
             }
@@ -580,6 +590,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
     atomicAdd(&g_gather_prof[4], 1ull);
   }
 
+  if constexpr (MULTI) __threadfence_system();     // peer stores performed before the kernel completes
   // ---------------- last CTA: fixed-order reduction, counter reset ----------------
   named_bar_sync(1, kCons);
   if (ctid == 0) {
@@ -657,6 +668,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
       a.pr_new[v] = (float)prn;
       const float idg = __ldg(a.inv_deg + v);
       a.spr_new[v] = (float)prn * idg * fscale;
+      for (int r = 0; r < a.n_peer; ++r) a.spr_peer[r][v] = (float)prn * idg * fscale;   // fused exchange
       if (idg == 0.0f) dang += prn;
       res += fabs(prn - (double)a.pr_old[v]);
     } else {
@@ -722,7 +734,8 @@ int smem_bytes_for(int b) {
 
 using GatherFn = void (*)(const GatherArgs);
 
-GatherFn gather_fn(bool wide, bool weighted, bool pagerank) {
+GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false) {
+  if (multi) return wide ? k_gather<uint32_t, false, true, true> : k_gather<uint16_t, false, true, true>;
   if (wide)
     return weighted ? (pagerank ? k_gather<uint32_t, true, true> : k_gather<uint32_t, true, false>)
                     : (pagerank ? k_gather<uint32_t, false, true> : k_gather<uint32_t, false, false>);
@@ -748,6 +761,8 @@ int prepare_gather(pcpm_handle* h) {
           return PCPM_ECUDA;
         }
         PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  for (int wd = 0; wd < 2; ++wd)
+    PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, false, true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
       }
   return PCPM_OK;
 }
@@ -790,10 +805,11 @@ int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaS
   return PCPM_OK;
 }
 
-int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s) {
+int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi) {
   const int smem = gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
-  gather_fn(h->wide, weighted, pagerank)<<<grid, gather_threads(h->wide, weighted), smem, s>>>(a);
+  gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted)<<<grid, gather_threads(h->wide, weighted), smem,
+                                                                        s>>>(a);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return launch_apply_split(h, a, pagerank, s);     // split bins (small k), if any

@@ -22,6 +22,7 @@ namespace pcpm {
 constexpr int kTileIds = 2048;
 constexpr int kTileAlign = 4096;
 constexpr int kChunkIds = 128;                         // chunk_base granularity
+constexpr int kMaxPeers = 8;                           // fused exchange: SPR destinations besides spr_new
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
@@ -260,10 +261,15 @@ struct GatherArgs {
   int wexp;                // max|w| <= 2^wexp
   int pf_tiles;            // L2 prefetch distance of the gather producer, in tiles
   int epi_pf;              // prefetch inv_deg / pr_old of the item's partition this many tiles before its end
+  // fused exchange (pcpm_shard_step_peers): SPR_{t+1} of the slice is also stored to
+  // these (peer) buffers, indexed like spr_new
+  float* spr_peer[kMaxPeers];
+  int n_peer;
 };
 __device__ int spmv_fbits(float xmax, int wexp);
 int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);
-int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s);
+int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s,
+                  bool multi = false);
 int gather_smem_bytes(int b, bool wide, bool weighted);
 
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);

@@ -14,7 +14,14 @@ on every rank:
   3. all_reduce of (residual, dangling mass), 16 bytes, for D_{t+1}.
 
 The full-SPR buffers are padded to N equal chunks of ceil(k/N) * q floats so
-the gathered vector is contiguous in global vertex order.  This module is
+the gathered vector is contiguous in global vertex order.
+
+exchange="p2p" fuses step 2 into step 1: every rank's full-SPR buffers are plain
+cudaMalloc allocations whose CUDA IPC handles are exchanged once; the gather's
+apply then stores each SPR group of the slice into every rank's buffer directly
+(pcpm_shard_step_peers, NVLink P2P stores overlapping the gather), and the
+16-byte all-reduce of step 3 orders the ranks' next iteration after all stores
+(each gather ends with a system-scope fence).  This module is
 plumbing (torch.distributed + device buffers); all arithmetic of the method
 runs in libpcpm.so.  ``step_impl`` lets the CPU tests (gloo, world_size 2)
 drive the same exchange with a test-side per-shard step.
@@ -56,7 +63,8 @@ class ShardedPageRank:
     column slice of this rank is kept on its device after the build).
     """
 
-    def __init__(self, n, row_ptr, col, b, group=None, device=None, stream=None, step_impl=None, timing=False):
+    def __init__(self, n, row_ptr, col, b, group=None, device=None, stream=None, step_impl=None, timing=False,
+                 exchange="allgather"):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
@@ -83,6 +91,54 @@ class ShardedPageRank:
         self.residuals = []
         self.timing = timing and step_impl is None
         self.events = []          # per iteration: (before step, after step, after exchange)
+        self.exchange = exchange if (step_impl is None and self.world > 1) else "allgather"
+        self.exchange_note = ""
+        self.own = self.peers = None
+        if self.exchange == "p2p":
+            self._setup_p2p()
+
+    def _setup_p2p(self):
+        """Own full-SPR buffers (cudaMalloc, IPC-shareable) and the peers' buffers opened here.
+        If any rank cannot map a peer (no P2P path), every rank falls back to the all-gather."""
+        pc = self.pcpm
+        nbytes = (self.plan.padded + 8) * 4
+        ok, why = 1, ""
+        mine = None
+        try:
+            self.own = [pc.pcpm_ipc_alloc(nbytes), pc.pcpm_ipc_alloc(nbytes)]
+            mine = [pc.pcpm_ipc_get_handle(p) for p in self.own]
+        except Exception as e:               # noqa: BLE001 -- reported through self.exchange_note
+            ok, why = 0, str(e)
+        every = [None] * self.world
+        self.dist.all_gather_object(every, mine, group=self.group)
+        self.peers = {}
+        if ok and all(h is not None for h in every):
+            try:
+                for r in range(self.world):
+                    if r != self.rank:
+                        self.peers[r] = [pc.pcpm_ipc_open(hd) for hd in every[r]]
+            except Exception as e:           # noqa: BLE001
+                ok, why = 0, str(e)
+        else:
+            ok = 0
+        flag = self.torch.tensor([ok], dtype=self.torch.int32, device=self.device)
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:            # consistent fallback on every rank
+            for ptrs in self.peers.values():
+                for p in ptrs:
+                    pc.pcpm_ipc_close(p)
+            self.dist.barrier(group=self.group)
+            for p in self.own or []:
+                pc.pcpm_ipc_free(p)
+            self.own, self.peers = None, None
+            self.exchange = "allgather"
+            self.exchange_note = "p2p setup failed (" + (why or "on another rank") + "); NCCL all-gather"
+        self.dist.barrier(group=self.group)
+
+    def _outs(self, buf):
+        """This rank's chunk in its own buffer, then in every peer's (buf = 0 or 1)."""
+        off = self.rank * self.plan.per * 4
+        return [self.own[buf] + off] + [self.peers[r][buf] + off for r in sorted(self.peers)]
 
     def info(self):
         return self.pcpm.pcpm_get_info(self.h) if self.h is not None else None
@@ -103,6 +159,18 @@ class ShardedPageRank:
         if self.h is not None:
             self.pcpm.pcpm_destroy(self.h)
             self.h = None
+        if self.peers:
+            self.torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)          # no peer still writes into our buffers
+            for ptrs in self.peers.values():
+                for p in ptrs:
+                    self.pcpm.pcpm_ipc_close(p)
+            self.peers = None
+        if self.own:
+            self.dist.barrier(group=self.group)          # every peer closed its mapping first
+            for p in self.own:
+                self.pcpm.pcpm_ipc_free(p)
+            self.own = None
 
     def _chunk(self, buf):
         return buf[self.rank * self.plan.per:(self.rank + 1) * self.plan.per]
@@ -121,12 +189,16 @@ class ShardedPageRank:
         n_loc = self.hi - self.lo
         # PR_0 = 1/n, SPR_0, D_0 (R2, R1)
         self.red.zero_()
+        p2p = self.exchange == "p2p"
         if n_loc > 0:
-            if self.step_impl is None:
+            if p2p:
+                self.pcpm.pcpm_shard_init_peers(self.h, self.pr[0], self._outs(0), self.red[1:])
+            elif self.step_impl is None:
                 self.pcpm.pcpm_shard_init(self.h, self.pr[0], self._chunk(self.spr[0]), self.red[1:])
             else:
                 self.step_impl.init(self, self.pr[0][:n_loc], self._chunk(self.spr[0])[:n_loc], self.red[1:])
-        self._allgather(self.spr[0])
+        if not p2p:
+            self._allgather(self.spr[0])
         self.D.copy_(self.red[1:])
         self._allreduce(self.D)
         self.residuals = []
@@ -136,15 +208,22 @@ class ShardedPageRank:
             self.red.zero_()
             ev = [self._event()] if self.timing else None
             if n_loc > 0:
-                args = (d, self.spr[cur], self.D, self.pr[cur], self.pr[nxt], self._chunk(self.spr[nxt]), self.red)
-                if self.step_impl is None:
-                    self.pcpm.pcpm_shard_step(self.h, *args)
+                if p2p:                                     # SPR_{t+1} stored to every rank by the apply
+                    self.pcpm.pcpm_shard_step_peers(self.h, d, self.own[cur], self.D, self.pr[cur], self.pr[nxt],
+                                                    self._outs(nxt), self.red)
                 else:
-                    self.step_impl.step(self, *args)
+                    args = (d, self.spr[cur], self.D, self.pr[cur], self.pr[nxt], self._chunk(self.spr[nxt]),
+                            self.red)
+                    if self.step_impl is None:
+                        self.pcpm.pcpm_shard_step(self.h, *args)
+                    else:
+                        self.step_impl.step(self, *args)
             if ev:
                 ev.append(self._event())
-            self._allgather(self.spr[nxt])                 # SPR_{t+1} of all vertices
-            self._allreduce(self.red)                       # global residual and D_{t+1}
+            if not p2p:
+                self._allgather(self.spr[nxt])             # SPR_{t+1} of all vertices
+            self._allreduce(self.red)                       # global residual and D_{t+1} (p2p: also the
+                                                            # barrier after every rank's stores)
             if ev:
                 ev.append(self._event())
                 self.events.append(tuple(ev))

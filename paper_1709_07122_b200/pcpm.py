@@ -30,7 +30,9 @@ PCPM_WIDE_IDS = 0x8
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
-            "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters"]
+            "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters",
+            "pcpm_shard_step_peers", "pcpm_shard_init_peers", "pcpm_ipc_handle_bytes", "pcpm_ipc_alloc", "pcpm_ipc_free", "pcpm_ipc_get_handle",
+            "pcpm_ipc_open", "pcpm_ipc_close"]
 
 
 class PcpmError(RuntimeError):
@@ -92,6 +94,14 @@ def _load():
         "pcpm_shard_init": (I, [P, P, P, P]),
         "pcpm_shard_step": (I, [P, ctypes.c_float, P, P, P, P, P, P]),
         "pcpm_get_debug_counters": (I, [P, I, I]),
+        "pcpm_shard_step_peers": (I, [P, ctypes.c_float, P, P, P, P, ctypes.POINTER(P), I, P]),
+        "pcpm_shard_init_peers": (I, [P, P, ctypes.POINTER(P), I, P]),
+        "pcpm_ipc_handle_bytes": (I, []),
+        "pcpm_ipc_alloc": (I, [I64, ctypes.POINTER(P)]),
+        "pcpm_ipc_free": (I, [P]),
+        "pcpm_ipc_get_handle": (I, [P, P]),
+        "pcpm_ipc_open": (I, [P, ctypes.POINTER(P)]),
+        "pcpm_ipc_close": (I, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -241,6 +251,49 @@ def pcpm_shard_init(h, pr0, spr0, dang0):
 def pcpm_shard_step(h, d: float, spr_in, D_in, pr_old, pr_new, spr_out, red_out):
     return _check(_lib.pcpm_shard_step(h, float(d), _ptr(spr_in), _ptr(D_in), _ptr(pr_old), _ptr(pr_new),
                                        _ptr(spr_out), _ptr(red_out)))
+
+
+PCPM_MAX_PEERS = 8
+
+
+def pcpm_shard_step_peers(h, d: float, spr_in, D_in, pr_old, pr_new, spr_outs, red_out):
+    """pcpm_shard_step with the exchange fused: spr_outs = [own chunk, peer chunks...]
+    (device pointers or tensors)."""
+    outs = (ctypes.c_void_p * len(spr_outs))(*[_ptr(o).value for o in spr_outs])
+    return _check(_lib.pcpm_shard_step_peers(h, float(d), _ptr(spr_in), _ptr(D_in), _ptr(pr_old), _ptr(pr_new),
+                                             outs, len(spr_outs), _ptr(red_out)))
+
+
+def pcpm_shard_init_peers(h, pr0, spr_outs, dang0):
+    outs = (ctypes.c_void_p * len(spr_outs))(*[_ptr(o).value for o in spr_outs])
+    return _check(_lib.pcpm_shard_init_peers(h, _ptr(pr0), outs, len(spr_outs), _ptr(dang0)))
+
+
+def pcpm_ipc_alloc(nbytes: int) -> int:
+    """A zeroed cudaMalloc'ed exchange buffer (device pointer as int)."""
+    p = ctypes.c_void_p()
+    _check(_lib.pcpm_ipc_alloc(int(nbytes), ctypes.byref(p)))
+    return p.value
+
+
+def pcpm_ipc_free(ptr: int):
+    return _check(_lib.pcpm_ipc_free(ctypes.c_void_p(ptr)))
+
+
+def pcpm_ipc_get_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(_lib.pcpm_ipc_handle_bytes())
+    _check(_lib.pcpm_ipc_get_handle(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def pcpm_ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(_lib.pcpm_ipc_open(ctypes.create_string_buffer(handle, len(handle)), ctypes.byref(p)))
+    return p.value
+
+
+def pcpm_ipc_close(ptr: int):
+    return _check(_lib.pcpm_ipc_close(ctypes.c_void_p(ptr)))
 
 
 def pcpm_get_debug_counters(reset: bool = True) -> np.ndarray:

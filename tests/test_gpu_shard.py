@@ -110,3 +110,81 @@ def test_shard_arguments_rejected(pcpm):
     for lo, hi in [(-1, 10), (10, 5), (0, g.n_src + 1), (3, 64)]:   # v_lo must be a multiple of q
         with pytest.raises(pcpm.PcpmError):
             pcpm.pcpm_build_shard(csr, 5, lo, hi)
+
+
+def run_shards_fused(pcpm, g, b, nsh, d, iters):
+    """Each shard owns its own full-SPR buffers (as each rank would); its step stores
+    its SPR slice into every shard's buffer (pcpm_shard_step_peers, the fused
+    exchange) -- here all buffers are on one GPU and the shards run one after
+    another, so no shard waits on another."""
+    plan = pdist.shard_plan(g.n_src, b, nsh)
+    rp, col, _ = to_device(g)
+    csr = pcpm.make_csr(g.n_src, g.n_dst, rp, col, None)
+    hs = [pcpm.pcpm_build_shard(csr, b, *plan.bounds(r)) for r in range(nsh)]
+    try:
+        f32 = dict(dtype=torch.float32, device="cuda")
+        spr = [[torch.zeros(plan.padded + 8, **f32), torch.zeros(plan.padded + 8, **f32)] for _ in range(nsh)]
+        n_loc = [hi - lo for lo, hi in (plan.bounds(r) for r in range(nsh))]
+        pr = [[torch.zeros(max(nl, 1), **f32), torch.zeros(max(nl, 1), **f32)] for nl in n_loc]
+        red = torch.zeros(nsh, 2, dtype=torch.float64, device="cuda")
+        D = torch.zeros(1, dtype=torch.float64, device="cuda")
+        chunk = lambda buf, r: buf[r * plan.per:(r + 1) * plan.per]     # noqa: E731
+        for r, h in enumerate(hs):
+            outs = [chunk(spr[r][0], r)] + [chunk(spr[s][0], r) for s in range(nsh) if s != r]
+            pcpm.pcpm_shard_init_peers(h, pr[r][0], outs, red[r, 1:])
+        D.copy_(red[:, 1].sum().reshape(1))
+        for t in range(iters):
+            cur, nxt = t & 1, (t + 1) & 1
+            for r, h in enumerate(hs):
+                outs = [chunk(spr[r][nxt], r)] + [chunk(spr[s][nxt], r) for s in range(nsh) if s != r]
+                pcpm.pcpm_shard_step_peers(h, d, spr[r][cur], D, pr[r][cur], pr[r][nxt], outs, red[r])
+            D.copy_(red[:, 1].sum().reshape(1))
+        torch.cuda.synchronize()
+        for s in range(1, nsh):                         # every rank holds the same full SPR vector
+            assert torch.equal(spr[s][iters & 1][:g.n_src], spr[0][iters & 1][:g.n_src])
+        full = torch.cat([pr[r][iters & 1][:n_loc[r]] for r in range(nsh)]).cpu().numpy()
+        return full
+    finally:
+        for h in hs:
+            pcpm.pcpm_destroy(h)
+
+
+@pytest.mark.parametrize("case", ["rmat14_b9", "er_ragged_b10"])
+@pytest.mark.parametrize("nsh", [2, 3])
+def test_fused_exchange_matches_allgather_and_oracle(pcpm, nsh, case):
+    if case == "rmat14_b9":
+        g, b = graphs.make_graph("rmat", 31, scale=14, permute=True), 9
+    else:                                               # n % 4 != 0: scalar apply path, split bins
+        g, b = graphs.make_graph("er", 6, n=70001, m_raw=600000), 10
+    d, iters = 0.85, 12
+    fused = run_shards_fused(pcpm, g, b, nsh, d, iters)
+    ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, d, iters)
+    rel = np.abs(fused.astype(np.float64) - ref) / ref
+    assert rel.max() <= 1e-5 and np.abs(fused - ref).sum() <= 1e-6
+    shared, hs, _ = run_shards(pcpm, g, b, nsh, d, iters)
+    for h in hs:
+        pcpm.pcpm_destroy(h)
+    np.testing.assert_array_equal(fused, shared)      # same kernels, same sums: bit-identical
+
+
+def test_peer_step_arguments_and_ipc_buffers(pcpm):
+    g = graphs.make_graph("rmat", 31, scale=10, permute=True)
+    rp, col, _ = to_device(g)
+    h = pcpm.pcpm_build_shard(pcpm.make_csr(g.n_src, g.n_dst, rp, col, None), 6, 0, g.n_src)
+    try:
+        f = torch.zeros(g.n_src + 8, dtype=torch.float32, device="cuda")
+        red = torch.zeros(2, dtype=torch.float64, device="cuda")
+        D = torch.zeros(1, dtype=torch.float64, device="cuda")
+        for outs in ([], [f] * (pcpm.PCPM_MAX_PEERS + 2)):
+            with pytest.raises(pcpm.PcpmError) as e:
+                pcpm.pcpm_shard_step_peers(h, 0.85, f, D, f, f, outs, red)
+            assert e.value.code == pcpm.PCPM_EINVAL
+        with pytest.raises(pcpm.PcpmError):
+            pcpm.pcpm_shard_step_peers(h, 0.85, f, D, f, f, [f, np.zeros(4, np.float32)], red)   # host peer
+    finally:
+        pcpm.pcpm_destroy(h)
+    ptr = pcpm.pcpm_ipc_alloc(1 << 20)
+    try:
+        assert len(pcpm.pcpm_ipc_get_handle(ptr)) == 64
+    finally:
+        pcpm.pcpm_ipc_free(ptr)
