@@ -203,14 +203,19 @@ __global__ void k_bounds_range(int64_t n_max, const int64_t* n_dev, const uint32
 
 // Scatter work items (p, [j0, j1)) of ~target updates (at most maxg groups), one warp
 // per source partition p: count pass (out == nullptr) or fill pass at off[p].
+// Partitions p >= p_tail (the last ones claimed) are cut ~tail_split times finer, so the
+// final wave of the persistent scatter has small items (less idle tail).
 __global__ void k_sitems(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ G, int64_t target, int maxg,
-                         const uint32_t* __restrict__ off, uint32_t* cnt, ScatterItem* out) {
+                         int64_t p_tail, int tail_split, const uint32_t* __restrict__ off, uint32_t* cnt,
+                         ScatterItem* out) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t p = w0; p < k_src; p += nw) {
     uint32_t n = 0, j0 = 0;
     int64_t acc = 0;
+    const int64_t ep_p = (int64_t)G[(p + 1) * k_dst] - (int64_t)G[p * k_dst];
+    const int64_t tgt = (p >= p_tail && tail_split > 1) ? max((int64_t)4096, min(target, ep_p / tail_split + 1)) : target;
     const uint32_t o = out ? off[p] : 0u;
     for (int64_t jb = 0; jb < k_dst; jb += 32) {
       const int64_t jl = jb + lane;
@@ -219,7 +224,7 @@ __global__ void k_sitems(int64_t k_src, int64_t k_dst, const uint32_t* __restric
       for (int t = 0; t < nt; ++t) {
         acc += __shfl_sync(0xffffffffu, sz, t);
         const uint32_t jj = (uint32_t)(jb + t);
-        if (acc >= target || jj + 1 - j0 >= (uint32_t)maxg) {      // item offsets fit in smem
+        if (acc >= tgt || jj + 1 - j0 >= (uint32_t)maxg) {         // item offsets fit in smem
           if (out && lane == 0) out[o + n] = ScatterItem{(uint32_t)p, j0, jj + 1, (uint32_t)acc};
           ++n;
           acc = 0;
@@ -526,11 +531,15 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   // ---- host-side work lists (small copies)
   // scatter items (p, [j0, j1)) holding ~E' / (2 SMs) updates each, counted on the device
   const int64_t target = std::max<int64_t>(8192, ep / (2 * h->num_sms) + 1);
+  int tail_split = 4;                                   // PCPM_SCATTER_TAIL=1: no tail split (A/B)
+  if (const char* e = getenv("PCPM_SCATTER_TAIL")) tail_split = std::max(1, atoi(e));
+  const int64_t p_tail = std::max<int64_t>(0, k_src - h->num_sms);
   uint32_t *si_cnt, *si_off;
   TK(tmp.alloc(&si_cnt, k_src + 1));
   TK(tmp.alloc(&si_off, k_src + 1));
   TK(cudaMemsetAsync(si_cnt + k_src, 0, 4, s));
-  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, nullptr, si_cnt, nullptr);
+  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, p_tail, tail_split, nullptr,
+                                               si_cnt, nullptr);
   TK(cudaGetLastError());
   {
     size_t bytes = 0;
@@ -549,7 +558,8 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   h->n_dangling = (int64_t)hdang;
   h->n_sitems = (int)n_si;
   if ((rc = dev_alloc_t(h, &h->sitems, std::max<size_t>(n_si, 1)))) return rc;
-  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, si_off, nullptr,
+  k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, p_tail, tail_split, si_off,
+                                               nullptr,
                                                h->sitems);
   TK(cudaGetLastError());
   if (h->opt_scatter_lpt && (rc = order_scatter_items(h, s))) return rc;
