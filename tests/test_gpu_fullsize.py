@@ -101,3 +101,46 @@ def test_fullsize_spmv(pcpm):
     err = np.abs(got.astype(np.float64) - ref)
     print(f"{key}: nnz={gn.m} F={fb} max_abs_err={err.max():.3e} worst err/tol={np.max(err / tol):.3e}")
     assert np.all(err <= tol), f"worst {np.max(err / tol):.3f}x tol at {np.argmax(err / tol)}"
+
+
+@pytest.mark.parametrize("key", ["c4", "c5"])
+def test_fullsize_host_build_equals_device_build(pcpm, key):
+    """The e2e path (host CSR in pinned memory: chunks copied on a second stream while
+    earlier chunks sort) builds the same layout, bit for bit, as the device-input
+    build, and the same PageRank / SpMV output, at full size."""
+    from tests.gpu_util import d2h
+    cfg = graphs.CONFIGS[key]
+    g = graphs.make_config(key, backend="torch", device="cuda")
+    pin = lambda t: t.cpu().pin_memory() if t is not None else None     # noqa: E731
+    rp_h, col_h, val_h = pin(g.row_ptr), pin(g.col), pin(g.values)
+    hd = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values), cfg["bits"], 0, None)
+    hh = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, rp_h, col_h, val_h), cfg["bits"], 0, None)
+    try:
+        ia, ib = pcpm.pcpm_get_info(hd), pcpm.pcpm_get_info(hh)
+        assert (ia.nnz, ia.e_prime, ia.k_src, ia.k_dst, ia.n_dangling) == (ib.nnz, ib.e_prime, ib.k_src, ib.k_dst,
+                                                                           ib.n_dangling)
+        va, vb = pcpm.pcpm_export_layout(hd), pcpm.pcpm_export_layout(hh)
+        m, ep, ks, kd = ia.nnz, ia.e_prime, ia.k_src, ia.k_dst
+        for name, count, dt in [("ids16", m, np.uint16), ("png_src16", ep, np.uint16),
+                                ("png_off", ks * (kd + 1), np.uint32), ("upd_off", ks * kd, np.uint32),
+                                ("bin_id_start", kd + 1, np.uint32), ("bin_upd_start", kd + 1, np.uint32),
+                                ("chunk_base", m // 128 + 1, np.uint32), ("out_degree", ia.n_src, np.uint32)] + \
+                               ([("w", m, np.float32)] if g.values is not None else []):
+            a, b = d2h(getattr(va, name), count, dt), d2h(getattr(vb, name), count, dt)
+            assert np.array_equal(a.view(np.uint8), b.view(np.uint8)), name
+        if g.values is None:
+            oa = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            ob = torch.zeros_like(oa)
+            pcpm.pcpm_pagerank(hd, 0.85, 3, oa)
+            pcpm.pcpm_pagerank(hh, 0.85, 3, ob)
+        else:
+            x = graphs.make_x(g.n_src, cfg["seed"], backend="torch", device="cuda")
+            oa = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
+            ob = torch.zeros_like(oa)
+            pcpm.pcpm_spmv(hd, x, oa)
+            pcpm.pcpm_spmv(hh, x, ob)
+        torch.cuda.synchronize()
+        assert torch.equal(oa, ob)
+    finally:
+        pcpm.pcpm_destroy(hd)
+        pcpm.pcpm_destroy(hh)
