@@ -247,6 +247,8 @@ def run_pcpm(args, world, rank, local):
     ms_iter = ms_per_step / iters
     hbm_gbs = iter_bytes / (ms_iter * 1e-3) / 1e9
     traffic = ncu_traffic(key, dom)
+    sm_clk = float(peaks().get("sm_max_mhz", 1965.0))
+    smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
@@ -268,6 +270,7 @@ def run_pcpm(args, world, rank, local):
                      "unit": "GB/s", "frac": round(kernels[dom]["frac"], 4), "traffic": traffic,
                      "alg_bytes_per_launch": kernels[dom]["bytes"],
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if not pk.get("_fallback") else "fallback"},
+        "roofline_smem": smem,
         "kernels": {k: {kk: (round(vv, 5) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                     for k, v in kernels.items()},
         "model_bytes_per_iter": {
@@ -487,6 +490,26 @@ def ncu_traffic(key, kernel):
         return d[key][kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
+
+
+def smem_roofline(key, kernel, ms, clk_mhz):
+    """Secondary ceiling of the gather: the shared-memory data pipe (one 128-byte
+    wavefront per SM-cycle).  Wavefronts per launch come from the committed ncu capture,
+    the time from this run's CUDA events; null when no capture exists for the config."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))[key][kernel]
+        wf = float(d["smem_wavefronts_per_launch"])
+    except Exception:
+        return None
+    peak = 148 * clk_mhz * 1e6                      # wavefronts / s
+    ach = wf / (ms * 1e-3)
+    out = {"bound": "smem", "unit": "wavefronts/s", "achieved": round(ach / 1e9, 2), "peak": round(peak / 1e9, 2),
+           "scale": "1e9", "frac": round(ach / peak, 4), "wavefronts_per_launch": wf}
+    for k in ("smem_atom_wavefronts", "smem_atom_bank_conflicts", "smem_atom_instructions"):
+        if d.get(k) is not None:
+            out[k] = d[k]
+    return out
 
 
 def cpu_baseline(g, key, op, iters, budget_s=20.0):

@@ -14,7 +14,12 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_active.avg",
-        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active"]
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "smsp__inst_executed_op_shared_atom.sum"]
 
 
 def main():
@@ -64,7 +69,13 @@ def main():
                 1e6 if d.get("dram__bytes_read.sum_unit") == "Mbyte" else 1.0)
             allj[key]["gather_apply" if k == "gather" else k] = {
                 "dram_bytes_per_launch": gb * scale, "report": rep,
-                "time_ms": d.get("gpu__time_duration.sum")}
+                "time_ms": d.get("gpu__time_duration.sum"),
+                "smem_wavefronts_per_launch": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                "smem_pipe_pct_of_peak": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                "smem_atom_wavefronts": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"),
+                "smem_atom_bank_conflicts": d.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_atom.sum"),
+                "smem_atom_instructions": d.get("smsp__inst_executed_op_shared_atom.sum"),
+                "sm_cycles_active": d.get("sm__cycles_active.avg")}
         json.dump(allj, open(path, "w"), indent=1)
 
 
