@@ -109,3 +109,76 @@ def test_sharded_pagerank_gloo_matches_oracle(world):
     prs = [oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, t) for t in range(13)]
     want = [np.abs(prs[t + 1] - prs[t]).sum() for t in range(12)]
     np.testing.assert_allclose(out[0][4], want, rtol=1e-4, atol=1e-7)
+
+
+class FakeIpc:
+    """Stand-in for the CUDA IPC calls of libpcpm (pcpm_ipc_*): integer 'pointers'."""
+
+    def __init__(self, rank, fail_open):
+        self.rank, self.fail_open = rank, fail_open
+        self.freed, self.closed, self.next = [], [], (rank + 1) << 40
+
+    def pcpm_ipc_alloc(self, nbytes):
+        self.next += 1 << 30
+        return self.next
+
+    def pcpm_ipc_get_handle(self, ptr):
+        return ptr.to_bytes(8, "little") * 8
+
+    def pcpm_ipc_open(self, handle):
+        if self.fail_open:
+            raise RuntimeError("no peer access")
+        return int.from_bytes(handle[:8], "little") + 7      # a mapping in this process
+
+    def pcpm_ipc_close(self, ptr):
+        self.closed.append(ptr)
+
+    def pcpm_ipc_free(self, ptr):
+        self.freed.append(ptr)
+
+
+def _p2p_worker(rank, world, port, q, fail_rank):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sh = object.__new__(pdist.ShardedPageRank)
+    sh.torch, sh.dist, sh.group, sh.device = torch, dist, None, "cpu"
+    sh.world, sh.rank = world, rank
+    sh.plan = pdist.shard_plan(5000, 8, world)
+    sh.exchange, sh.exchange_note, sh.own, sh.peers = "p2p", "", None, None
+    sh.pcpm = FakeIpc(rank, fail_open=(rank == fail_rank))
+    sh._setup_p2p()
+    res = {"exchange": sh.exchange, "note": sh.exchange_note, "freed": len(sh.pcpm.freed),
+           "closed": len(sh.pcpm.closed)}
+    if sh.exchange == "p2p":
+        outs = sh._outs(1)
+        off = rank * sh.plan.per * 4
+        res["outs_ok"] = outs[0] == sh.own[1] + off and len(outs) == world and \
+            all(o == sh.peers[r][1] + off for o, r in zip(outs[1:], sorted(sh.peers)))
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, res))
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_p2p_exchange_setup_is_consistent_across_ranks(fail_rank):
+    """The fused-exchange setup (IPC handles exchanged once, peers mapped) either
+    succeeds on every rank or falls back to the NCCL all-gather on every rank (a
+    rank that cannot map a peer must not leave the others waiting)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, fail_rank)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r, res in out.items():
+        if fail_rank < 0:
+            assert res["exchange"] == "p2p" and res["outs_ok"] and res["freed"] == 0
+        else:
+            assert res["exchange"] == "allgather" and "p2p setup failed" in res["note"]
+            assert res["freed"] == 2                       # own exchange buffers released
+            assert res["closed"] == (0 if r == fail_rank else 2 * (world - 1))
