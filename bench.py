@@ -252,9 +252,12 @@ def run_pcpm(args, world, rank, local):
     iter_bytes = sb + gb
     ms_iter = ms_per_step / iters
     hbm_gbs = iter_bytes / (ms_iter * 1e-3) / 1e9
-    traffic = ncu_traffic(key, dom)
+    # the committed ncu capture is of the default build (compact, compressed, the
+    # config's partition bits, default options); other variants report null
+    default_variant = not (args.no_compress or args.wide or args.bits or args.opt)
+    traffic = ncu_traffic(key, dom) if default_variant else None
     sm_clk = float(peaks().get("sm_max_mhz", 1965.0))
-    smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk)
+    smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk) if default_variant else None
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
