@@ -44,12 +44,14 @@ def _load():
         lib.oracle_transpose.argtypes = [I64, P, P, P, P]
         lib.oracle_pagerank_pull.argtypes = [I64, P, P, P, ctypes.c_double, ctypes.c_int, P]
         lib.oracle_pagerank.argtypes = [I64, P, P, ctypes.c_double, ctypes.c_int, P]
+        lib.oracle_pagerank_weighted.argtypes = [I64, P, P, P, ctypes.c_double, ctypes.c_int, P]
         lib.oracle_spmv_t.argtypes = [I64, I64, P, P, P, P, P]
         lib.oracle_layout_sizes.argtypes = [I64, I64, P, P, ctypes.c_int, P, P, P]
         lib.oracle_layout.argtypes = [I64, I64, P, P, P, ctypes.c_int, P, P, P, P, P, P, P]
         lib.oracle_scatter.argtypes = [I64, I64, P, P, P, P, P]
         lib.oracle_gather.argtypes = [I64, I64, P, P, P, P, P, P]
-        for f in ("oracle_transpose", "oracle_pagerank_pull", "oracle_pagerank", "oracle_spmv_t",
+        for f in ("oracle_transpose", "oracle_pagerank_pull", "oracle_pagerank", "oracle_pagerank_weighted",
+                  "oracle_spmv_t",
                   "oracle_layout_sizes", "oracle_layout", "oracle_scatter", "oracle_gather"):
             getattr(lib, f).restype = ctypes.c_int
         _lib = lib
@@ -106,6 +108,19 @@ def pagerank(n, row_ptr, col, d=0.85, iters=20):
     rc = _load().oracle_pagerank(n, _p(row_ptr), _p(colp), float(d), int(iters), _p(pr))
     if rc:
         raise ValueError(f"oracle_pagerank failed ({rc})")
+    return pr
+
+
+def pagerank_weighted(n, row_ptr, col, w, d=0.85, iters=20):
+    """Weighted PageRank (reading R24): u passes PR(u) w(u,v)/W(u) to v; float64[n]."""
+    row_ptr, col = _csr(row_ptr, col)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    pr = np.zeros(n, dtype=np.float64)
+    colp = col if col.size else np.zeros(1, dtype=np.uint32)
+    wp = w if w.size else np.zeros(1, dtype=np.float32)
+    rc = _load().oracle_pagerank_weighted(n, _p(row_ptr), _p(colp), _p(wp), float(d), int(iters), _p(pr))
+    if rc:
+        raise ValueError(f"oracle_pagerank_weighted failed ({rc})")
     return pr
 
 

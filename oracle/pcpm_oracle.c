@@ -18,6 +18,9 @@
  *                     n=1 self-loop, 2-cycle, out-star / in-star closed forms
  *                     at every t, dense brute-force power iteration (n<=64),
  *                     stationary vector by linear solve, sum(PR)=1.
+ *   oracle_pagerank_weighted  pinned: uniform weights = oracle_pagerank, per-source
+ *                     scaling invariance, zero weights = removed edges, dense
+ *                     brute-force power iteration of the weighted chain (n<=48).
  *   oracle_spmv_t     pinned: identity, zero, 2x2 hand product, dense numpy
  *                     product on random matrices, Eq. 2 consistency.
  *   oracle_layout     pinned: G_toy hand derivation (tests/golden)
@@ -129,6 +132,47 @@ int oracle_pagerank_pull(int64_t n, const int64_t* row_ptr, const int64_t* in_pt
     memcpy(pr, next, sizeof(double) * (size_t)n);
   }
   free(spr); free(dang); free(next);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Weighted PageRank (§3.5: edge weights stored with the destination IDs
+ * "applied to the source node value before updating the destination node"; the
+ * normalisation is reading R24): u passes PR(u) * w(u,v) / W(u) to v, with
+ * W(u) = sum_v w(u,v) and w >= 0.  Vertices with W(u) = 0 (out-degree 0, or only
+ * zero weights) are dangling and their mass is spread uniformly (R1):
+ *   PR_{t+1}(v) = (1-d)/n + d * ( sum_{u->v} PR_t(u) w(u,v) / W(u) + D_t/n ).
+ * With every w = 1 this is oracle_pagerank.  Push form, plain loops, fp64.
+ * Returns 0, -1 on bad arguments, -3 on a negative weight.
+ * ------------------------------------------------------------------------- */
+int oracle_pagerank_weighted(int64_t n, const int64_t* row_ptr, const uint32_t* col, const float* w,
+                             double d, int iters, double* pr) {
+  if (n <= 0 || iters < 0 || !(d > 0.0 && d < 1.0)) return -1;
+  int64_t m = row_ptr[n];
+  for (int64_t e = 0; e < m; ++e) if (w[e] < 0.0f) return -3;
+  double* W = (double*)malloc(sizeof(double) * (size_t)n);
+  double* dang = (double*)malloc(sizeof(double) * (size_t)n);
+  double* next = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!W || !dang || !next) { free(W); free(dang); free(next); return -2; }
+  for (int64_t u = 0; u < n; ++u) {
+    double s = 0.0;
+    for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e) s += (double)w[e];
+    W[u] = s;
+  }
+  for (int64_t v = 0; v < n; ++v) pr[v] = 1.0 / (double)n;           /* R2 */
+  for (int it = 0; it < iters; ++it) {
+    for (int64_t u = 0; u < n; ++u) dang[u] = W[u] > 0.0 ? 0.0 : pr[u];
+    double D = oracle_sum(dang, n);                                   /* R1 */
+    for (int64_t v = 0; v < n; ++v) next[v] = 0.0;
+    for (int64_t u = 0; u < n; ++u) {
+      if (!(W[u] > 0.0)) continue;
+      for (int64_t e = row_ptr[u]; e < row_ptr[u + 1]; ++e)
+        next[col[e]] += pr[u] * (double)w[e] / W[u];
+    }
+    for (int64_t v = 0; v < n; ++v) next[v] = (1.0 - d) / (double)n + d * (next[v] + D / (double)n);
+    memcpy(pr, next, sizeof(double) * (size_t)n);
+  }
+  free(W); free(dang); free(next);
   return 0;
 }
 

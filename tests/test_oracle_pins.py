@@ -123,6 +123,62 @@ def test_dense_brute_force_power_iteration(seed):
         np.testing.assert_allclose(oracle.pagerank(n, rp, c, d, t), x, rtol=0, atol=1e-14)
 
 
+def weighted_dense_google(n, row_ptr, col, w, d):
+    """The Markov matrix of weighted PageRank (R24): column u = w(u, .)/W(u), or 1/n if W(u) = 0."""
+    M = np.zeros((n, n))
+    for u in range(n):
+        W = sum(float(w[e]) for e in range(row_ptr[u], row_ptr[u + 1]))
+        if W <= 0.0:
+            M[:, u] = 1.0 / n
+            continue
+        for e in range(row_ptr[u], row_ptr[u + 1]):
+            M[col[e], u] += float(w[e]) / W
+    return d * M + (1 - d) / n * np.ones((n, n))
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_weighted_pagerank_dense_brute_force(seed):
+    """Weighted PageRank (R24) against powers of its dense Markov matrix,
+    with zero-weight rows (dangling) and zero-weight edges mixed in."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(2, 49))
+    rp, c = random_small_graph(rng, n, float(rng.uniform(0.05, 0.35)))
+    w = rng.uniform(0.0, 2.0, len(c)).astype(np.float32)
+    w[rng.random(len(c)) < 0.15] = 0.0
+    G = weighted_dense_google(n, rp, c, w, 0.85)
+    x = np.full(n, 1.0 / n)
+    for t in range(1, 13):
+        x = G @ x
+        np.testing.assert_allclose(oracle.pagerank_weighted(n, rp, c, w, 0.85, t), x, rtol=0, atol=1e-14)
+
+
+def test_weighted_pagerank_reduces_and_is_scale_invariant():
+    g = graphs.make_graph("rmat", 41, scale=10, permute=True)
+    n, rp, c = g.n_src, g.row_ptr, g.col
+    rng = np.random.default_rng(7)
+    # uniform weights: the unweighted chain (w/W = 1/outdeg)
+    for cst in (1.0, 0.37, 3.0):
+        np.testing.assert_allclose(oracle.pagerank_weighted(n, rp, c, np.full(len(c), cst, np.float32), 0.85, 15),
+                                   oracle.pagerank(n, rp, c, 0.85, 15), rtol=1e-12, atol=0)
+    # scaling all out-weights of a source by s_u > 0 leaves w/W, hence PR, unchanged
+    w = rng.uniform(0.1, 1.0, len(c)).astype(np.float32)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    s_u = (2.0 ** rng.integers(-3, 4, n)).astype(np.float32)          # exact in fp32
+    np.testing.assert_allclose(oracle.pagerank_weighted(n, rp, c, w * s_u[rows], 0.85, 15),
+                               oracle.pagerank_weighted(n, rp, c, w, 0.85, 15), rtol=1e-12, atol=0)
+    # a zero-weight edge is an absent edge (a source with only zero weights is dangling)
+    w0 = w.copy()
+    w0[rng.random(len(c)) < 0.3] = 0.0
+    keep = w0 > 0
+    rp2 = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=rp2[1:])
+    np.testing.assert_allclose(oracle.pagerank_weighted(n, rp, c, w0, 0.85, 15),
+                               oracle.pagerank_weighted(n, rp2, c[keep], w0[keep], 0.85, 15), rtol=1e-12, atol=0)
+    assert abs(oracle.pagerank_weighted(n, rp, c, w0, 0.85, 15).sum() - 1.0) < 1e-12
+    with pytest.raises(ValueError):
+        oracle.pagerank_weighted(n, rp, c, -w, 0.85, 3)
+
+
 def test_g_toy_against_dense_and_stationary():
     g = json.load(open(os.path.join(GOLDEN, "g_toy_layout.json")))
     n, rp, c = g["n"], np.array(g["row_ptr"]), np.array(g["col"], dtype=np.uint32)
