@@ -65,7 +65,8 @@ typedef struct {
   int64_t nnz;              /* nonzeros / edges, after deduplication (R10) */
   const int64_t* row_ptr;   /* n_src+1 entries, row_ptr[0] = 0, monotone, row_ptr[n_src] = nnz */
   const uint32_t* col_idx;  /* nnz entries, < n_dst, strictly increasing within each row */
-  const float* values;      /* nnz entries or NULL (= all ones; PageRank ignores values) */
+  const float* values;      /* nnz entries or NULL (= all ones); PageRank uses them only with the
+                               "weighted_pagerank" option (R24) */
 } pcpm_csr;
 
 typedef struct pcpm_handle pcpm_handle;
@@ -210,7 +211,11 @@ int pcpm_get_residuals(pcpm_handle* h, double* host, int cap);
 int pcpm_scatter(pcpm_handle* h, const float* x);
 /* Select a kernel variant for A/B experiments.
  * Keys: "phase_timing", "use_graph", "scatter_variant" (0|1), "scatter_lpt",
- * "scatter_prefetch", "gather_prefetch", "epilogue_prefetch".  Every variant
+ * "scatter_prefetch", "gather_prefetch", "epilogue_prefetch" (kernel variants:
+ * every one computes the same result) and "weighted_pagerank" (1: pcpm_pagerank
+ * uses the edge values as weights, u passing PR(u) w(u,v) / W(u) to v with
+ * W(u) = sum of u's weights (reading R24); needs a non-shard handle
+ * built with non-negative values, else PCPM_ESTATE / PCPM_EINVAL).  Every variant
  * computes the same result.  Returns PCPM_EINVAL for unknown keys or
  * out-of-range values. */
 int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value);

@@ -151,7 +151,12 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
   h->last_was_spmv = false;
   h->n_events_used = 0;
   if ((rc = mark(h, s))) return rc;
-  if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0, fbits), s))) return rc;
+  const bool wpr = h->opt_weighted_pr && h->inv_wdeg && h->w;      // weighted PageRank (R24)
+  if (wpr) {
+    if ((rc = launch_pr_init_weighted(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0f, fbits), s))) return rc;
+  } else if ((rc = launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0, fbits), s))) {
+    return rc;
+  }
   if ((rc = mark(h, s))) return rc;
   if (iters == 0) {
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
@@ -169,7 +174,8 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
     a.pr_old = h->pr[t & 1];
     a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
     a.spr_new = h->spr;
-    if ((rc = launch_gather(h, a, false, true, s))) return rc;  // Alg. 5 + apply
+    if (wpr) a.inv_deg = h->inv_wdeg;                          // 1/W(u): the weights' normalisation
+    if ((rc = launch_gather(h, a, wpr, true, s))) return rc;    // Alg. 5 (+ weights) + apply
     if ((rc = mark(h, s))) return rc;
   }
   return PCPM_OK;
@@ -722,7 +728,20 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     free_graph(h);
     return PCPM_OK;
   }
-  if (!strcmp(key, "epilogue_prefetch")) {
+  if (!strcmp(key, "weighted_pagerank")) {
+    if (value && (!h->inv_wdeg || !h->w || h->shard)) {
+      set_error(PCPM_ESTATE, "weighted_pagerank needs a (non-shard) handle built with edge values");
+      return PCPM_ESTATE;
+    }
+    if (value && h->neg_weights) {
+      set_error(PCPM_EINVAL, "weighted_pagerank needs non-negative edge values (R24)");
+      return PCPM_EINVAL;
+    }
+    h->opt_weighted_pr = value ? 1 : 0;
+    free_graph(h);
+    return PCPM_OK;
+  }
+    if (!strcmp(key, "epilogue_prefetch")) {
     if (value < 0 || value > 64) {
       set_error(PCPM_EINVAL, "epilogue_prefetch must be in [0, 64] (tiles before the item's end)");
       return PCPM_EINVAL;

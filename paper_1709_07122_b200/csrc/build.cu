@@ -490,6 +490,53 @@ cudaError_t radix_sort_pairs(Temp& tmp, const KeyT* kin, KeyT* kout, const ValT*
 }
 
 
+// Weighted out-degrees W(u) = sum of row u's weights (fp64, lanes then a fixed shuffle
+// tree: deterministic), 1/W(u) in fp32 (0 when W(u) = 0: dangling under R24), the
+// count of such vertices and whether any weight is negative.  One warp per row.
+__global__ void k_row_wsum(int64_t n, const int64_t* __restrict__ row_ptr, const float* __restrict__ val,
+                           float* inv_w, unsigned long long* n_zero, uint32_t* neg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = w0; u < n; u += nw) {
+    double sum = 0.0;
+    bool ng = false;
+    for (int64_t e = row_ptr[u] + lane; e < row_ptr[u + 1]; e += 32) {
+      const float x = val[e];
+      sum += (double)x;
+      ng = ng || x < 0.0f;
+    }
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (__any_sync(0xffffffffu, ng) && lane == 0) atomicOr(neg, 1u);
+    if (lane == 0) {
+      inv_w[u] = sum > 0.0 ? (float)(1.0 / sum) : 0.0f;
+      if (!(sum > 0.0)) atomicAdd(n_zero, 1ull);
+    }
+  }
+}
+
+int weighted_degrees(pcpm_handle* h, Temp& tmp, const int64_t* d_row_ptr, const float* d_val) {
+  cudaStream_t s = h->stream;
+  int rc;
+  if ((rc = dev_alloc_t(h, &h->inv_wdeg, h->n_src + 4))) return rc;
+  unsigned long long* cnt;
+  uint32_t* neg;
+  TK(tmp.alloc(&cnt, 1));
+  TK(tmp.alloc(&neg, 1));
+  TK(cudaMemsetAsync(cnt, 0, 8, s));
+  TK(cudaMemsetAsync(neg, 0, 4, s));
+  k_row_wsum<<<grid_for(h->n_src * 32), kT, 0, s>>>(h->n_src, d_row_ptr, d_val, h->inv_wdeg, cnt, neg);
+  TK(cudaGetLastError());
+  unsigned long long hc = 0;
+  uint32_t hn = 0;
+  TK(cudaMemcpyAsync(&hc, cnt, 8, cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(&hn, neg, 4, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  h->n_wdangling = (int64_t)hc;
+  h->neg_weights = hn ? 1 : 0;
+  return PCPM_OK;
+}
+
 // Offsets, decode anchors, work lists and iteration state: the part of the
 // build shared by both layout constructions.  G = flat (p, j) PNG group starts.
 int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsigned long long* d_dang) {
@@ -868,6 +915,7 @@ int build_layout_legacy(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       int ex = 0;
       if (hmx > 0.f) frexpf(hmx, &ex);
       h->wexp = ex;
+      if ((rc2 = weighted_degrees(h, tmp, row_ptr, values))) return rc2;
     }
   } else {
     h->e_prime = 0;
@@ -1183,6 +1231,7 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     int ex = 0;
     if (hmx > 0.f) frexpf(hmx, &ex);
     h->wexp = ex;
+    if ((rc2 = weighted_degrees(h, tmp, d_rp, d_val))) return rc2;
   }
   return finish_layout(h, tmp, pt, G, d_dang);
 }

@@ -368,7 +368,9 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             uint32_t tlo[P], thi[P], old[P];
 #pragma unroll
             for (int c = 0; c < P; ++c) {
-              const unsigned long long T = __float2ull_rn(val[c]);   // SPR is stored as SPR * 2^F
+              // SPR is stored as SPR * 2^F; weighted PageRank (R24) applies w(u,v) here
+              const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+              const unsigned long long T = __float2ull_rn(tv);
               tlo[c] = (uint32_t)T;
               thi[c] = (uint32_t)(T >> 32);
             }

@@ -84,6 +84,10 @@ struct pcpm_handle {
   uint32_t* chunk_base = nullptr;   // [m_pad/kChunkIds + 1]
   uint32_t* outdeg = nullptr;       // [n_src]
   float* inv_deg = nullptr;         // [n_src] 1/|N_o(u)| (0 for dangling u), read by the apply
+  float* inv_wdeg = nullptr;        // [n_src] 1/W(u), W(u) = sum of u's edge weights (0 if W(u) = 0); weighted
+                                    // PageRank (R24), built when values are given
+  int64_t n_wdangling = 0;          // #{u : W(u) = 0}
+  int neg_weights = 0;              // some weight < 0 (SpMV only)
   float* upd = nullptr;             // [E' + 8]
   int wexp = 0;                     // max|w| <= 2^wexp (SpMV fixed-point scale)
   float* xmax = nullptr;            // [1] device max|x| of the last pcpm_spmv
@@ -127,6 +131,7 @@ struct pcpm_handle {
   int opt_scatter_lpt = 0;          // scatter claim order: 0 ascending p, 1 largest first
   int opt_scatter_pf = 0;           // scatter: PNG stages prefetched into L2 ahead of the ring
   int opt_phase_timing = 0;
+  int opt_weighted_pr = 0;          // pcpm_pagerank uses the edge weights (R24)
   std::vector<cudaEvent_t> events;  // phase-timing events (created on demand)
   int n_events_used = 0;
 
@@ -277,6 +282,8 @@ int read_debug_counters(unsigned long long* out, int cap, bool reset);
 int prepare_gather(pcpm_handle* h);
 int prepare_scatter(pcpm_handle* h);
 int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, double spr_scale, cudaStream_t s);
+int launch_pr_init_weighted(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, float spr_scale,
+                            cudaStream_t s);
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
                           float* spr_out, double* red_t, float d, cudaStream_t s);
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);

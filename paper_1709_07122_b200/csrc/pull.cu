@@ -74,6 +74,32 @@ __global__ void __launch_bounds__(256) k_pull(int64_t n, const uint32_t* __restr
 
 }  // namespace
 
+// Weighted PageRank (R24): PR_0 = 1/n, SPR_0 = f32(PR_0) * 1/W(u) * 2^F (the apply's
+// form, R23), D_0 = #{W(u) = 0} / n.
+__global__ void k_pr_init_w(int64_t n, const float* __restrict__ inv_w, int64_t n_zero, float* pr0, float* spr,
+                            double* red, int red_n, float spr_scale) {
+  const double inv_n = 1.0 / (double)n;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    pr0[v] = (float)inv_n;
+    spr[v] = (float)inv_n * inv_w[v] * spr_scale;
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < red_n; i += blockDim.x) red[i] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) red[0] = (double)n_zero * inv_n;   // D_0
+  }
+}
+
+int launch_pr_init_weighted(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, float spr_scale,
+                            cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((h->n_src + 255) / 256, h->num_sms * 8);
+  k_pr_init_w<<<std::max(grid, 1), 256, 0, s>>>(h->n_src, h->inv_wdeg, h->n_wdangling, pr0, spr, red, red_n,
+                                                spr_scale);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 1;
+  return PCPM_OK;
+}
+
 int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, double spr_scale, cudaStream_t s) {
   int grid = (int)std::min<int64_t>((h->n_src + 255) / 256, h->num_sms * 8);
   k_pr_init<<<std::max(grid, 1), 256, 0, s>>>(h->n_src, h->outdeg, h->n_dangling, pr0, spr, red, red_n,

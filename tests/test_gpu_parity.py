@@ -424,3 +424,60 @@ def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, chunk
             assert_layout_equal(g, lay, b)
     finally:
         pcpm.pcpm_destroy(h)
+
+
+def weighted(g, seed, zero_frac=0.1):
+    """g with non-negative fp32 edge weights (some exactly zero) for weighted PageRank."""
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(0.0, 1.0, g.m).astype(np.float32)
+    w[rng.random(g.m) < zero_frac] = 0.0
+    return graphs.GraphCSR(g.name + "_w", g.n_src, g.n_dst, g.row_ptr, g.col, w)
+
+
+WPR_CASES = [
+    ("rmat12_b8", lambda: weighted(graphs.make_graph("rmat", 12, scale=12, permute=True), 1), 8, True),
+    ("rmat14_b10_host", lambda: weighted(graphs.make_graph("rmat", 13, scale=14, permute=True), 2), 10, False),
+    ("rmat15_b15_split", lambda: weighted(graphs.make_graph("rmat", 13, scale=15, permute=False), 3), 15, True),
+    ("er_ragged_b9", lambda: weighted(graphs.make_graph("er", 6, n=70001, m_raw=600000), 4, 0.3), 9, True),
+]
+
+
+@pytest.mark.parametrize("name,mk,b,device", WPR_CASES, ids=[c[0] for c in WPR_CASES])
+def test_weighted_pagerank_parity(pcpm, name, mk, b, device):
+    """Weighted PageRank (R24): the gather applies w(u,v) to the source value,
+    the apply normalises by W(u); oracle bounds as for Eq. 1, bit-reproducible."""
+    g = mk()
+    h = build(pcpm, g, b, device=device)
+    try:
+        pcpm.pcpm_set_option(h, "weighted_pagerank", 1)
+        ref = oracle.pagerank_weighted(g.n_src, g.row_ptr, g.col, g.values, 0.85, 15)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 15, out)
+        pr_check(out.cpu().numpy(), ref, name)
+        out2 = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(h, 0.85, 15, out2)
+        assert torch.equal(out, out2)
+        pcpm.pcpm_set_option(h, "weighted_pagerank", 0)     # back to Eq. 1 on the structure
+        pcpm.pcpm_pagerank(h, 0.85, 15, out)
+        pr_check(out.cpu().numpy(), oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 15), name + "/unweighted")
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_weighted_pagerank_rejected_without_usable_weights(pcpm):
+    g = graphs.make_graph("rmat", 12, scale=10, permute=True)
+    h = build(pcpm, g, 6)
+    try:
+        with pytest.raises(pcpm.PcpmError) as e:
+            pcpm.pcpm_set_option(h, "weighted_pagerank", 1)        # no values
+        assert e.value.code == pcpm.PCPM_ESTATE
+    finally:
+        pcpm.pcpm_destroy(h)
+    gs = graphs.make_graph("rmat", 5, scale=10, permute=True, values=True)   # values in [-1, 1)
+    h = build(pcpm, gs, 6)
+    try:
+        with pytest.raises(pcpm.PcpmError) as e:
+            pcpm.pcpm_set_option(h, "weighted_pagerank", 1)
+        assert e.value.code == pcpm.PCPM_EINVAL
+    finally:
+        pcpm.pcpm_destroy(h)
