@@ -495,8 +495,8 @@ def ncu_traffic(key, kernel):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))
-        return d[key][kernel]["dram_bytes_per_launch"]
+        d = json.load(open(p))[key]
+        return (d.get(kernel) or d["gather_apply"])["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -507,7 +507,8 @@ def smem_roofline(key, kernel, ms, clk_mhz):
     the time from this run's CUDA events; null when no capture exists for the config."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        d = json.load(open(p))[key][kernel]
+        dk = json.load(open(p))[key]
+        d = dk.get(kernel) or dk["gather_apply"]
         wf = float(d["smem_wavefronts_per_launch"])
     except Exception:
         return None

@@ -63,13 +63,17 @@ def main():
         except Exception:
             allj = {}
         allj.setdefault(key, {})
+        byte_scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        time_scale = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+                      "second": 1e3, "s": 1e3}
         for k, d in res.items():
-            gb = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-            scale = 1e9 if d.get("dram__bytes_read.sum_unit") == "Gbyte" else (
-                1e6 if d.get("dram__bytes_read.sum_unit") == "Mbyte" else 1.0)
+            gb = sum(d.get(mn, 0) * byte_scale.get(d.get(mn + "_unit"), 1.0)
+                     for mn in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            tm = d.get("gpu__time_duration.sum")
+            tm = tm * time_scale.get(d.get("gpu__time_duration.sum_unit"), 1.0) if tm is not None else None
             allj[key]["gather_apply" if k == "gather" else k] = {
-                "dram_bytes_per_launch": gb * scale, "report": rep,
-                "time_ms": d.get("gpu__time_duration.sum"),
+                "dram_bytes_per_launch": gb, "report": rep,
+                "time_ms": tm,
                 "smem_wavefronts_per_launch": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
                 "smem_pipe_pct_of_peak": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
                 "smem_atom_wavefronts": d.get("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum"),
