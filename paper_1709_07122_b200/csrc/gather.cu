@@ -316,12 +316,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   uint32_t phase = 0;
   unsigned long long pt[4] = {0, 0, 0, 0};
   long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
-#ifndef PCPM_GATHER_WAIT_HINT
-#define PCPM_GATHER_WAIT_HINT 0
-#endif
   for (;;) {
-    if (PCPM_GATHER_WAIT_HINT) mbar_wait_sleep(&full[stage], phase, PCPM_GATHER_WAIT_HINT);
-    else mbar_wait(&full[stage], phase);
+    mbar_wait(&full[stage], phase);
     if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[0] += t - tc; tc = t; }
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;

@@ -188,17 +188,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// try_wait with a suspend-time hint (ns): the waiting warp sleeps in hardware until
-// the phase completes or the hint expires, instead of re-issuing the test.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(hint_ns)
-      : "memory");
-}
 // 1-D bulk async copy global -> shared (TMA engine, UBLKCP), completion on mbarrier.
 // dst, src 16 B aligned; bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
