@@ -71,3 +71,29 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "pcpm_oracle" not in txt, f
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    exe = tmp_path / "pagerank_c"
+    libdir = os.path.join(ROOT, "paper_1709_07122_b200")
+    subprocess.run(["gcc", "-O2", "-Wall", "-Werror", "-std=c99", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "pagerank_c.c"), "-L", libdir, "-lpcpm",
+                    "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_example_compiles_against_the_header(tmp_path):
+    """include/pcpm.h is plain C99 and libpcpm.so links from C (no CUDA or Python)."""
+    assert _build_c_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    import subprocess
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([str(_build_c_example(tmp_path)), "200000"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "sum_pr=" in r.stdout
