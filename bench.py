@@ -263,7 +263,8 @@ def run_pcpm(args, world, rank, local):
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
         "ms_per_iter": round(ms_iter, 5), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 values, i64 fixed-point accumulation, f64 apply", "data": "synthetic (seeded RMAT/ER, inputs/)",
+        "dtype": "f32", "arithmetic": "f32 values, i64 fixed-point accumulation, f64 apply",
+        "data": "synthetic (seeded RMAT/ER, inputs/)",
         "hbm_gbs": round(hbm_gbs, 1), "hbm_frac_of_measured": round(hbm_gbs / peak, 4),
         "hbm_frac_of_8tbs_spec": round(hbm_gbs / 8000.0, 4),
         "config": {"workload": WORKLOADS[key], "n": n, "m": m, "k": info.k_dst, "q": info.q,
@@ -399,7 +400,8 @@ def run_sharded(args, world, rank, local):
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "ms_per_iter": round(ms_per_step / iters, 5),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 values, i64 fixed-point accumulation, f64 apply", "data": "synthetic (seeded RMAT/ER, inputs/)",
+        "dtype": "f32", "arithmetic": "f32 values, i64 fixed-point accumulation, f64 apply",
+        "data": "synthetic (seeded RMAT/ER, inputs/)",
         "config": {"workload": WORKLOADS[key], "n": n, "m": m, "iters": iters, "partition_bits": b,
                    "l2": "inputs larger than L2 (no flush)",
                    "parallelism": f"destination shards x{world}, {exchange_desc}"},
