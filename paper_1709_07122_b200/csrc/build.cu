@@ -618,7 +618,9 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   std::vector<GatherItem> gi;
   std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
   uint32_t nslots = 0;
-  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (2 * h->num_sms)) / kTileAlign + 1) * kTileAlign);
+  int slice_div = 2;                                   // PCPM_GATHER_SLICE_DIV: items per SM the cut aims at
+  if (const char* e = getenv("PCPM_GATHER_SLICE_DIV")) slice_div = std::max(1, atoi(e));
+  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (slice_div * h->num_sms)) / kTileAlign + 1) * kTileAlign);
   for (int64_t j = 0; j < k_dst; ++j) {
     int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
     int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
