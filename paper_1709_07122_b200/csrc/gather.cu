@@ -12,8 +12,11 @@
 //    engine, cp.async.bulk) into a 4-stage ring: the IDs (4096 2-byte IDs in
 //    the compact layout), the window of update values they reference, and
 //    the decode anchors.
-//  * 16 consumer warps each decode one sub-chunk of the tile in steps of 32
-//    consecutive IDs (lane l takes ID 32 c + l).  The update pointer of Alg. 5
+//  * 31 consumer warps in two groups that take alternate stages; each warp
+//    decodes two 128-ID sub-chunks of a stage (the group of 15 rotates the
+//    remaining two) in steps of 32 consecutive IDs (lane l takes ID 32 c + l).
+//    The producer also prefetches the tiles (and, near an item's end, the
+//    apply's vertex arrays) into L2 ahead of the ring.  The update pointer of Alg. 5
 //    becomes a warp prefix count of MSB flags:
 //    ptr = anchor + (flags of earlier steps) + popc(ballot & lanemask_le) - 1
 //    (reading R5's -1 start), with no data-dependent branch; all loads and
@@ -27,9 +30,14 @@
 //    fp32 smem atomics are CAS loops on sm_100a).  SpMV uses the signed
 //    ("balanced") variant of the same accumulator.
 //  * Epilogue: PR' = (1-d)/n + d (acc + D/n) in fp64, stored fp32; SPR' =
-//    fp32(PR') * fp32(1/outdeg) (<= 3 fp32 roundings, R23); per-item dangling mass and L1 residual, reduced in fixed
-//    order by the last CTA.  Slices of split bins store their low words to a
-//    slot buffer and the last-arriving slice sums the slots and runs the epilogue.
+//    fp32(PR') * fp32(1/outdeg) (<= 3 fp32 roundings, R23); per-item
+//    dangling mass and L1 residual, reduced in fixed order by the last CTA.
+//    Slices of split (heavy) bins store their low words to per-slice slot
+//    buffers; k_apply_split sums the slots and applies those bins afterwards.
+//  * Weighted PageRank (R24) and SpMV multiply each update by the edge weight
+//    (staged with the IDs) before the fixed-point add.
+//  * The decode is bound by the shared-memory pipe (one random ATOMS per ID,
+//    ~4.4 wavefronts per warp instruction), see DESIGN.md §6.
 #include <type_traits>
 
 #include "pcpm_internal.cuh"

@@ -10,13 +10,16 @@
 // the same x.
 //
 // k_scatter_tma (default):
-//  * Persistent CTAs claim items (largest first) from an atomic counter.
+//  * Persistent CTAs claim items from an atomic counter in source-partition
+//    order (neighbouring groups of an update bin are written at about the same
+//    time, so their shared sectors complete in L2); the last 148 partitions'
+//    items are cut finer so the final wave is short.
 //  * Warp 0 is a TMA producer.  Per item it bulk-copies the partition's source
 //    values x[p q .. p q + q) (128 KB at q = 2^15 -- "cache the vertex data of
 //    p") and the item's rows of png_off / upd_off into shared memory,
-//    then streams the item's PNG entries through a 3-stage ring of 16 KB
-//    bulk copies, with an L2 prefetch running further ahead.
-//  * 16 consumer warps take 512-entry sub-ranges of each stage.  Lane l
+//    then streams the item's PNG entries through a 5-stage ring of 16 KB
+//    bulk copies with the grp_at anchors of each 256-entry chunk.
+//  * 31 consumer warps take 256-entry sub-ranges of each stage.  Lane l
 //    handles entries e = base + l + 32 i: consecutive lanes read consecutive
 //    PNG entries from smem and write consecutive update slots of the group
 //    containing e (dst = upd_off[g] + e - png_off[g]), so global stores are
