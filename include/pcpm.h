@@ -127,6 +127,13 @@ pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned fla
  * the unscaled PR_iters (R4).  iters = 0 returns 1/n.  PCPM_ESTATE if the
  * handle is not square. */
 int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out);
+/* PageRank iterated to convergence: the same iterations as pcpm_pagerank, run
+ * until the L1 residual sum_v |PR_t(v) - PR_{t-1}(v)| (computed by the fused apply
+ * of every iteration) is <= tol, or max_iters iterations.  out receives PR_t for
+ * that t (host or device, n floats); *iters_done = t.  The host reads one residual
+ * per iteration while the next iteration already runs (kernels launched directly,
+ * no graph).  tol >= 0, max_iters >= 1; returns 0 or PCPM_E*. */
+int pcpm_pagerank_tol(pcpm_handle* h, float d, double tol, int max_iters, float* out, int* iters_done);
 
 /* y = M^T x (§3.5): y[v] = sum over CSR entries (u -> v) of
  * w(u,v) * x[u], with w = values given at build (1 if none).  x: n_src floats,

@@ -144,6 +144,27 @@ int mark(pcpm_handle* h, cudaStream_t s) {
   return PCPM_OK;
 }
 
+// Iteration t of Eq. 1: scatter (Alg. 4) then gather (Alg. 5) + apply, PR_t in
+// pr[t & 1] -> PR_{t+1} in pr_new; red[2t] = D_t in, red[2t+1] = residual, red[2t+2] = D_{t+1}.
+int enqueue_iteration(pcpm_handle* h, float d, int t, float* pr_new, cudaStream_t s) {
+  int rc;
+  const bool wpr = h->opt_weighted_pr && h->inv_wdeg && h->w;      // weighted PageRank (R24)
+  if ((rc = launch_scatter(h, h->spr, s))) return rc;              // Alg. 4
+  if ((rc = mark(h, s))) return rc;
+  GatherArgs a = base_args(h, h->fixed_bits);
+  a.d = d;
+  a.n = (double)h->n_src;
+  a.red_in = h->red + 2 * t;
+  a.res_out = h->red + 2 * t + 1;
+  a.dang_out = h->red + 2 * t + 2;
+  a.pr_old = h->pr[t & 1];
+  a.pr_new = pr_new;
+  a.spr_new = h->spr;
+  if (wpr) a.inv_deg = h->inv_wdeg;                              // 1/W(u): the weights' normalisation
+  if ((rc = launch_gather(h, a, wpr, true, s))) return rc;        // Alg. 5 (+ weights) + apply
+  return mark(h, s);
+}
+
 int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
   int rc;
   const int fbits = pr_fixed_bits(h->n_src);
@@ -162,22 +183,8 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
     return PCPM_OK;
   }
-  for (int t = 0; t < iters; ++t) {
-    if ((rc = launch_scatter(h, h->spr, s))) return rc;          // Alg. 4
-    if ((rc = mark(h, s))) return rc;
-    GatherArgs a = base_args(h, fbits);
-    a.d = d;
-    a.n = (double)h->n_src;
-    a.red_in = h->red + 2 * t;
-    a.res_out = h->red + 2 * t + 1;
-    a.dang_out = h->red + 2 * t + 2;
-    a.pr_old = h->pr[t & 1];
-    a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
-    a.spr_new = h->spr;
-    if (wpr) a.inv_deg = h->inv_wdeg;                          // 1/W(u): the weights' normalisation
-    if ((rc = launch_gather(h, a, wpr, true, s))) return rc;    // Alg. 5 (+ weights) + apply
-    if ((rc = mark(h, s))) return rc;
-  }
+  for (int t = 0; t < iters; ++t)
+    if ((rc = enqueue_iteration(h, d, t, (t == iters - 1) ? dst : h->pr[(t + 1) & 1], s))) return rc;
   return PCPM_OK;
 }
 
@@ -525,6 +532,70 @@ pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits) {
 
 int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out) { return pagerank_common(h, d, iters, out, 0); }
 
+int pcpm_pagerank_tol(pcpm_handle* h, float d, double tol, int max_iters, float* out, int* iters_done) {
+  if (!h || !out || !iters_done) {
+    set_error(PCPM_EINVAL, "NULL handle, output or iters_done");
+    return PCPM_EINVAL;
+  }
+  if (!(d > 0.f && d < 1.f) || max_iters < 1 || !(tol >= 0.0)) {
+    set_error(PCPM_EINVAL, "d must be in (0,1), max_iters >= 1, tol >= 0");
+    return PCPM_EINVAL;
+  }
+  if (h->n_src != h->n_dst) {
+    set_error(PCPM_ESTATE, "PageRank needs a square matrix (n_src == n_dst)");
+    return PCPM_ESTATE;
+  }
+  int rc = ensure_red(h, max_iters);
+  if (rc) return rc;
+  if (!h->res_host) PCPM_CK(cudaMallocHost(reinterpret_cast<void**>(&h->res_host), sizeof(double) * 2));
+  cudaStream_t s = h->stream;
+  h->launches = 0;
+  h->opt_phase_timing_saved = h->opt_phase_timing;
+  h->opt_phase_timing = 0;                     // no event bookkeeping on this path
+  const int fbits = pr_fixed_bits(h->n_src);
+  h->fixed_bits = fbits;
+  h->last_was_spmv = false;
+  h->n_events_used = 0;
+  const bool wpr = h->opt_weighted_pr && h->inv_wdeg && h->w;
+  rc = wpr ? launch_pr_init_weighted(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0f, fbits), s)
+           : launch_pr_init(h, h->pr[0], h->spr, h->red, h->red_cap, std::ldexp(1.0, fbits), s);
+  // One iteration in flight: iteration t is enqueued before the host looks at the
+  // residual of iteration t - 1 (copied to pinned memory behind an event).  If that
+  // residual is <= tol the result is PR_t, in pr[t & 1], which iteration t only reads.
+  int done = max_iters;
+  cudaEvent_t ev = nullptr;
+  if (!rc && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) rc = PCPM_ECUDA;
+  for (int t = 0; t < max_iters && !rc; ++t) {
+    if ((rc = enqueue_iteration(h, d, t, h->pr[(t + 1) & 1], s))) break;
+    if (t > 0) {
+      if (cudaEventSynchronize(ev) != cudaSuccess) { rc = PCPM_ECUDA; break; }
+      if (h->res_host[0] <= tol) {               // sum |PR_t - PR_{t-1}| <= tol
+        done = t;
+        break;
+      }
+    }
+    if (cudaMemcpyAsync(h->res_host, h->red + 2 * t + 1, sizeof(double), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaEventRecord(ev, s) != cudaSuccess) {
+      rc = PCPM_ECUDA;
+      break;
+    }
+  }
+  if (ev) cudaEventDestroy(ev);
+  h->opt_phase_timing = h->opt_phase_timing_saved;
+  if (rc) {
+    if (rc == PCPM_ECUDA) set_error(PCPM_ECUDA, "CUDA error in pcpm_pagerank_tol");
+    return rc;
+  }
+  if (done == max_iters) {                       // the last iteration's residual
+    PCPM_CK(cudaStreamSynchronize(s));
+  }
+  h->last_iters = done;
+  *iters_done = done;
+  PCPM_CK(cudaMemcpyAsync(out, h->pr[done & 1], sizeof(float) * h->n_src, cudaMemcpyDefault, s));
+  PCPM_CK(cudaStreamSynchronize(s));
+  return PCPM_OK;
+}
+
 int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out) {
   return pagerank_common(h, d, iters, out, 1);
 }
@@ -583,6 +654,7 @@ void pcpm_destroy(pcpm_handle* h) {
   for (cudaEvent_t e : h->events) cudaEventDestroy(e);
   for (void* p : h->allocs)
     if (p) cudaFreeAsync(p, h->stream);
+  if (h->res_host) cudaFreeHost(h->res_host);
   delete h;
 }
 

@@ -131,6 +131,8 @@ struct pcpm_handle {
   int opt_scatter_lpt = 0;          // scatter claim order: 0 ascending p, 1 largest first
   int opt_scatter_pf = 0;           // scatter: PNG stages prefetched into L2 ahead of the ring
   int opt_phase_timing = 0;
+  int opt_phase_timing_saved = 0;
+  double* res_host = nullptr;       // pinned: the residual read back by pcpm_pagerank_tol
   int opt_weighted_pr = 0;          // pcpm_pagerank uses the edge weights (R24)
   std::vector<cudaEvent_t> events;  // phase-timing events (created on demand)
   int n_events_used = 0;

@@ -31,7 +31,7 @@ EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_p
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
             "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters",
-            "pcpm_shard_step_peers", "pcpm_shard_init_peers", "pcpm_ipc_handle_bytes", "pcpm_ipc_alloc", "pcpm_ipc_free", "pcpm_ipc_get_handle",
+            "pcpm_shard_step_peers", "pcpm_pagerank_tol", "pcpm_shard_init_peers", "pcpm_ipc_handle_bytes", "pcpm_ipc_alloc", "pcpm_ipc_free", "pcpm_ipc_get_handle",
             "pcpm_ipc_open", "pcpm_ipc_close"]
 
 
@@ -97,6 +97,7 @@ def _load():
         "pcpm_shard_step_peers": (I, [P, ctypes.c_float, P, P, P, P, ctypes.POINTER(P), I, P]),
         "pcpm_shard_init_peers": (I, [P, P, ctypes.POINTER(P), I, P]),
         "pcpm_ipc_handle_bytes": (I, []),
+        "pcpm_pagerank_tol": (I, [P, ctypes.c_float, ctypes.c_double, I, P, ctypes.POINTER(I)]),
         "pcpm_ipc_alloc": (I, [I64, ctypes.POINTER(P)]),
         "pcpm_ipc_free": (I, [P]),
         "pcpm_ipc_get_handle": (I, [P, P]),
@@ -267,6 +268,13 @@ def pcpm_shard_step_peers(h, d: float, spr_in, D_in, pr_old, pr_new, spr_outs, r
 def pcpm_shard_init_peers(h, pr0, spr_outs, dang0):
     outs = (ctypes.c_void_p * len(spr_outs))(*[_ptr(o).value for o in spr_outs])
     return _check(_lib.pcpm_shard_init_peers(h, _ptr(pr0), outs, len(spr_outs), _ptr(dang0)))
+
+
+def pcpm_pagerank_tol(h, d: float, tol: float, max_iters: int, out) -> int:
+    """PageRank until the L1 residual <= tol (or max_iters); returns the iteration count."""
+    done = ctypes.c_int(0)
+    _check(_lib.pcpm_pagerank_tol(h, float(d), float(tol), int(max_iters), _ptr(out), ctypes.byref(done)))
+    return done.value
 
 
 def pcpm_ipc_alloc(nbytes: int) -> int:

@@ -481,3 +481,33 @@ def test_weighted_pagerank_rejected_without_usable_weights(pcpm):
         assert e.value.code == pcpm.PCPM_EINVAL
     finally:
         pcpm.pcpm_destroy(h)
+
+
+@pytest.mark.parametrize("tol", [1e-4, 1e-6])
+def test_pagerank_to_tolerance(pcpm, tol):
+    """pcpm_pagerank_tol stops at the first t whose L1 residual sum|PR_t - PR_{t-1}| <= tol
+    and returns exactly pcpm_pagerank's PR_t (the same kernels)."""
+    g = graphs.make_graph("rmat", 12, scale=14, permute=True)
+    h = build(pcpm, g, 10)
+    try:
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        t = pcpm.pcpm_pagerank_tol(h, 0.85, tol, 200, out)
+        assert 1 <= t < 200
+        prs = [oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, k) for k in (t - 1, t)]
+        pr_check(out.cpu().numpy(), prs[1], "tol")
+        res = np.abs(prs[1] - prs[0]).sum()
+        assert res <= tol * 1.01 + 1e-7                  # fp32 vs fp64 residual
+        if t >= 2:
+            prev = np.abs(prs[0] - oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, t - 2)).sum()
+            assert prev >= tol * 0.99 - 1e-7               # it did not stop early
+        ref = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(h, 0.85, t, ref)
+        assert torch.equal(out, ref)
+        host = np.zeros(g.n_src, np.float32)
+        assert pcpm.pcpm_pagerank_tol(h, 0.85, 0.0, 7, host) == 7      # tol 0: runs max_iters
+        pcpm.pcpm_pagerank(h, 0.85, 7, ref)
+        np.testing.assert_array_equal(host, ref.cpu().numpy())
+        with pytest.raises(pcpm.PcpmError):
+            pcpm.pcpm_pagerank_tol(h, 0.85, -1.0, 5, out)
+    finally:
+        pcpm.pcpm_destroy(h)
