@@ -36,6 +36,11 @@ namespace {
 // ------------------------------------------------------------------ TMA variant
 // consumer warps: 31 for the compact (2-byte) PNG -- 32 sub-ranges of 256 entries per
 // 16 KB stage, the extra one rotating -- and 16 for the 4-byte PNG (16 sub-ranges)
+#ifndef PCPM_SCATTER_UNROLL
+#define PCPM_SCATTER_UNROLL 8
+#endif
+#define PCPM_STR_(x) #x
+#define PCPM_UNROLL(n) _Pragma(PCPM_STR_(unroll n))
 #ifndef PCPM_SCATTER_WARPS16
 #define PCPM_SCATTER_WARPS16 31
 #endif
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
           uint32_t g = ga > 0 ? (uint32_t)ga : 0u;
           uint32_t gend = offs[g + 1];
           uint32_t delta = uos[g] - offs[g];                 // dst = e + delta within group g
-#pragma unroll 4
+          PCPM_UNROLL(PCPM_SCATTER_UNROLL)
           for (uint32_t e = wlo + lane; e < whi; e += 32) {
             if (e >= gend) {
               do {
