@@ -81,7 +81,10 @@ struct Cfg {
 #ifndef PCPM_GATHER_COLD_WARPS
 #define PCPM_GATHER_COLD_WARPS 31
 #endif
-  static constexpr int kWarps = kHot ? 31 : PCPM_GATHER_COLD_WARPS;
+#ifndef PCPM_GATHER_HOT_WARPS
+#define PCPM_GATHER_HOT_WARPS 31
+#endif
+  static constexpr int kWarps = kHot ? PCPM_GATHER_HOT_WARPS : PCPM_GATHER_COLD_WARPS;
   static constexpr int kThreads = 32 * (kWarps + 1);
   static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kChunkIds;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
