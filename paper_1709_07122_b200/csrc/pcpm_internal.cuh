@@ -12,6 +12,10 @@
 
 #include "pcpm.h"
 
+// #pragma unroll with a macro argument (A/B build knobs)
+#define PCPM_STR_(x) #x
+#define PCPM_UNROLL(n) _Pragma(PCPM_STR_(unroll n))
+
 namespace pcpm {
 
 // ---------------------------------------------------------------- constants

@@ -39,8 +39,6 @@ namespace {
 #ifndef PCPM_SCATTER_UNROLL
 #define PCPM_SCATTER_UNROLL 8
 #endif
-#define PCPM_STR_(x) #x
-#define PCPM_UNROLL(n) _Pragma(PCPM_STR_(unroll n))
 #ifndef PCPM_SCATTER_WARPS16
 #define PCPM_SCATTER_WARPS16 31
 #endif
