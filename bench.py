@@ -488,9 +488,99 @@ def e2e(args, g, b, iters, op, world):
     d2h = res.numel() * 4 if op == "pagerank" else res.numel() * 4 * iters
     if op != "pagerank":
         h2d += x.numel() * 4 * iters
-    return {"value": round(m * iters * world / t / 1e9, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
-            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "seconds_per_step": round(t, 4), "includes": "H2D CSR + GPU build + iterations + D2H result"}
+    unit = "GTEPS" if op == "pagerank" else "G-nnz/s"
+    serial = {"value": round(m * iters * world / t / 1e9, 3), "unit": unit,
+              "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+              "seconds_per_step": round(t, 4), "includes": "H2D CSR + GPU build + iterations + D2H result"}
+    flags = (pcpm.PCPM_WIDE_IDS if args.wide else 0) | (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0)
+    try:
+        tp, np_ = e2e_pipelined((rp, col, val), (g.n_src, g.n_dst), b, flags, iters, op, x, max(g.n_src, g.n_dst),
+                                 max(8, min(args.steps, 10)), world)
+    except Exception as ex:                  # e.g. two layouts do not fit: report the serial figure only
+        serial["pipelined_error"] = str(ex)[:200]
+        return serial
+    tp = max_over_ranks(tp, world)
+    out = dict(serial)
+    out.update({"value": round(m * iters * world / tp / 1e9, 3), "seconds_per_step": round(tp, 4),
+                "pipelined": True, "steps": np_,
+                "includes": "every step: H2D of the CSR (pinned host -> device) + GPU build (C ABI) + iterations "
+                            "+ D2H of the result; step k+1's CSR upload runs on the copy engine while step k "
+                            "builds and iterates; the timed window spans all steps, pipeline fill and drain included",
+                "serial": {"value": serial["value"], "seconds_per_step": serial["seconds_per_step"]}})
+    return out
+
+
+def e2e_pipelined(g_host, dims, b, flags, iters, op, x, n_out, nsteps, world):
+    """Back-to-back independent jobs, each: H2D of the CSR from pinned host memory, pcpm_build
+    (C ABI) from that device copy, the iterations, D2H of the result.  The copy engines move
+    job k+1's CSR in and job k-1's result out while the SMs build and iterate job k; builds
+    and iterations share one compute stream (they never compete for the SMs).  One untimed
+    two-job pass first sizes the memory pool for two resident layouts.
+    Returns (seconds per job, jobs)."""
+    import torch
+    from paper_1709_07122_b200 import pcpm
+    rp, col, val = g_host
+    n_src, n_dst = dims
+    nnz = int(rp[-1])                          # host copy: the device one may still be uploading
+    comp, h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    stage = [(torch.empty_like(rp, device="cuda"), torch.empty_like(col, device="cuda"),
+              None if val is None else torch.empty_like(val, device="cuda")) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    out_read = [torch.cuda.Event() for _ in range(2)]
+    dev = [torch.empty(n_out, dtype=torch.float32, device="cuda") for _ in range(2)]
+    host = [torch.empty(n_out, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    xd = torch.empty(x.numel(), dtype=torch.float32, device="cuda") if x is not None else None
+
+    def upload(k):
+        h2d.wait_stream(comp)                  # the build that read this staging buffer is done
+        with torch.cuda.stream(h2d):
+            d = stage[k & 1]
+            d[0].copy_(rp, non_blocking=True)
+            d[1].copy_(col, non_blocking=True)
+            if val is not None:
+                d[2].copy_(val, non_blocking=True)
+            ready[k & 1].record(h2d)
+
+    def run(jobs):
+        prev = None
+        try:
+            upload(0)
+            for k in range(jobs):
+                comp.wait_event(ready[k & 1])
+                if k + 1 < jobs:
+                    upload(k + 1)              # staging buffer of job k-1, whose build is done
+                d = stage[k & 1]
+                h = pcpm.pcpm_build_ex(pcpm.make_csr(n_src, n_dst, d[0], d[1], d[2], nnz=nnz), b, flags, comp)
+                if prev is not None:
+                    pcpm.pcpm_destroy(prev)    # job k-1's iterations ran before this build
+                if k >= 2:
+                    comp.wait_event(out_read[k & 1])   # job k-2's result has left dev[k & 1]
+                with torch.cuda.stream(comp):
+                    if op == "pagerank":
+                        pcpm.pcpm_pagerank(h, 0.85, iters, dev[k & 1])
+                        done[k & 1].record(comp)
+                        d2h.wait_event(done[k & 1])
+                        with torch.cuda.stream(d2h):
+                            host[k & 1].copy_(dev[k & 1], non_blocking=True)
+                            out_read[k & 1].record(d2h)
+                    else:
+                        for _ in range(iters):
+                            xd.copy_(x, non_blocking=True)
+                            pcpm.pcpm_spmv(h, xd, dev[k & 1])
+                            host[k & 1].copy_(dev[k & 1], non_blocking=True)
+                        out_read[k & 1].record(comp)
+                prev = h
+        finally:
+            if prev is not None:
+                pcpm.pcpm_destroy(prev)
+        torch.cuda.synchronize()
+
+    run(2)                                     # untimed: pool grows to two resident layouts
+    barrier(world)
+    t0 = time.perf_counter()
+    run(nsteps)
+    return (time.perf_counter() - t0) / nsteps, nsteps
 
 
 def ncu_traffic(key, kernel):

@@ -148,9 +148,12 @@ def pcpm_last_status() -> int:
     return _lib.pcpm_last_status()
 
 
-def make_csr(n_src, n_dst, row_ptr, col_idx, values=None):
-    """pcpm_csr over caller-owned arrays (keep them alive for the pcpm_build call)."""
-    nnz = int(row_ptr[-1]) if not hasattr(row_ptr, "data_ptr") else int(row_ptr[-1].item())
+def make_csr(n_src, n_dst, row_ptr, col_idx, values=None, nnz=None):
+    """pcpm_csr over caller-owned arrays (keep them alive for the pcpm_build call).
+    ``nnz`` defaults to row_ptr[-1] (read from the array: pass it when row_ptr is a device
+    buffer still being written on another stream)."""
+    if nnz is None:
+        nnz = int(row_ptr[-1]) if not hasattr(row_ptr, "data_ptr") else int(row_ptr[-1].item())
     return pcpm_csr(int(n_src), int(n_dst), nnz, _ptr(row_ptr), _ptr(col_idx), _ptr(values))
 
 
