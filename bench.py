@@ -473,6 +473,7 @@ def e2e(args, g, b, iters, op, world):
         t0 = time.perf_counter()
         h = pcpm.pcpm_build_ex(csr, b, (pcpm.PCPM_WIDE_IDS if args.wide else 0) |
                                (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0), None)
+        layout_bytes = pcpm.pcpm_get_info(h).device_bytes
         if op == "pagerank":
             pcpm.pcpm_pagerank(h, 0.85, iters, res)
         else:
@@ -493,8 +494,18 @@ def e2e(args, g, b, iters, op, world):
               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
               "seconds_per_step": round(t, 4), "includes": "H2D CSR + GPU build + iterations + D2H result"}
     flags = (pcpm.PCPM_WIDE_IDS if args.wide else 0) | (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0)
+    if op != "pagerank":
+        # SpMV jobs move x in and y out on every multiply (13.4 GB per c5 job): PCIe-bound in
+        # both directions, so overlapping the next CSR upload only adds contention (measured
+        # 25.7 vs 59.8 G-nnz/s on c5); the serial schedule is the e2e figure
+        return serial
     try:
-        tp, np_ = e2e_pipelined((rp, col, val), (g.n_src, g.n_dst), b, flags, iters, op, x, max(g.n_src, g.n_dst),
+        # one layout + a device-input build's sort buffers (~1.3x the CSR), cached in the pool
+        # up front so no job maps new memory inside the timed window
+        csr_bytes = rp.numel() * 8 + col.numel() * 4 + (0 if val is None else val.numel() * 4)
+        free = torch.cuda.mem_get_info()[0]
+        pcpm.pcpm_pool_reserve(int(min(1.2 * (layout_bytes + 2 * csr_bytes), 0.5 * free)))
+        tp, np_ = e2e_pipelined((rp, col, val), (g.n_src, g.n_dst), b, flags, iters, max(g.n_src, g.n_dst),
                                  max(8, min(args.steps, 10)), world)
     except Exception as ex:                  # e.g. two layouts do not fit: report the serial figure only
         serial["pipelined_error"] = str(ex)[:200]
@@ -510,12 +521,13 @@ def e2e(args, g, b, iters, op, world):
     return out
 
 
-def e2e_pipelined(g_host, dims, b, flags, iters, op, x, n_out, nsteps, world):
-    """Back-to-back independent jobs, each: H2D of the CSR from pinned host memory, pcpm_build
+def e2e_pipelined(g_host, dims, b, flags, iters, n_out, nsteps, world):
+    """Back-to-back independent PageRank jobs, each: H2D of the CSR from pinned host memory, pcpm_build
     (C ABI) from that device copy, the iterations, D2H of the result.  The copy engines move
     job k+1's CSR in and job k-1's result out while the SMs build and iterate job k; builds
-    and iterations share one compute stream (they never compete for the SMs).  One untimed
-    two-job pass first sizes the memory pool for two resident layouts.
+    and iterations share one compute stream (they never compete for the SMs), so job k-1's
+    layout is freed before job k's build and one layout is resident at a time.  One untimed
+    two-job pass comes first.
     Returns (seconds per job, jobs)."""
     import torch
     from paper_1709_07122_b200 import pcpm
@@ -530,7 +542,6 @@ def e2e_pipelined(g_host, dims, b, flags, iters, op, x, n_out, nsteps, world):
     out_read = [torch.cuda.Event() for _ in range(2)]
     dev = [torch.empty(n_out, dtype=torch.float32, device="cuda") for _ in range(2)]
     host = [torch.empty(n_out, dtype=torch.float32, pin_memory=True) for _ in range(2)]
-    xd = torch.empty(x.numel(), dtype=torch.float32, device="cuda") if x is not None else None
 
     def upload(k):
         h2d.wait_stream(comp)                  # the build that read this staging buffer is done
@@ -542,41 +553,48 @@ def e2e_pipelined(g_host, dims, b, flags, iters, op, x, n_out, nsteps, world):
                 d[2].copy_(val, non_blocking=True)
             ready[k & 1].record(h2d)
 
+    dbg = bool(os.environ.get("PCPM_E2E_DEBUG"))
+
     def run(jobs):
         prev = None
+        t_run = time.perf_counter()
         try:
             upload(0)
             for k in range(jobs):
                 comp.wait_event(ready[k & 1])
                 if k + 1 < jobs:
                     upload(k + 1)              # staging buffer of job k-1, whose build is done
+                if prev is not None:
+                    # job k-1's iterations run before this build on the same stream anyway:
+                    # freeing its layout first keeps one layout resident (steady pool reuse)
+                    pcpm.pcpm_destroy(prev)
+                    prev = None
                 d = stage[k & 1]
                 h = pcpm.pcpm_build_ex(pcpm.make_csr(n_src, n_dst, d[0], d[1], d[2], nnz=nnz), b, flags, comp)
-                if prev is not None:
-                    pcpm.pcpm_destroy(prev)    # job k-1's iterations ran before this build
                 if k >= 2:
                     comp.wait_event(out_read[k & 1])   # job k-2's result has left dev[k & 1]
                 with torch.cuda.stream(comp):
-                    if op == "pagerank":
-                        pcpm.pcpm_pagerank(h, 0.85, iters, dev[k & 1])
-                        done[k & 1].record(comp)
-                        d2h.wait_event(done[k & 1])
-                        with torch.cuda.stream(d2h):
-                            host[k & 1].copy_(dev[k & 1], non_blocking=True)
-                            out_read[k & 1].record(d2h)
-                    else:
-                        for _ in range(iters):
-                            xd.copy_(x, non_blocking=True)
-                            pcpm.pcpm_spmv(h, xd, dev[k & 1])
-                            host[k & 1].copy_(dev[k & 1], non_blocking=True)
-                        out_read[k & 1].record(comp)
+                    pcpm.pcpm_pagerank(h, 0.85, iters, dev[k & 1])
+                    done[k & 1].record(comp)
+                d2h.wait_event(done[k & 1])
+                with torch.cuda.stream(d2h):
+                    host[k & 1].copy_(dev[k & 1], non_blocking=True)
+                    out_read[k & 1].record(d2h)
                 prev = h
+                if dbg:
+                    from cuda.bindings import runtime as rt
+                    _, pool = rt.cudaDeviceGetDefaultMemPool(torch.cuda.current_device())
+                    _, res = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrReservedMemCurrent)
+                    _, used = rt.cudaMemPoolGetAttribute(pool, rt.cudaMemPoolAttr.cudaMemPoolAttrUsedMemCurrent)
+                    sys.stderr.write(f"e2e job {k}: build returned at {(time.perf_counter() - t_run) * 1e3:.1f} ms "
+                                     f"pool reserved {int(res) / 1e9:.1f} GB used {int(used) / 1e9:.1f} GB "
+                                     f"free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB\n")
         finally:
             if prev is not None:
                 pcpm.pcpm_destroy(prev)
         torch.cuda.synchronize()
 
-    run(2)                                     # untimed: pool grows to two resident layouts
+    run(2)                                     # untimed warm-up
     barrier(world)
     t0 = time.perf_counter()
     run(nsteps)

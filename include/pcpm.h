@@ -204,6 +204,12 @@ int pcpm_ipc_close(void* dev_ptr);
 void pcpm_destroy(pcpm_handle* h);
 
 /* Support: stream, errors, introspection. */
+/* Memory: handles take their device memory from the current device's stream-ordered
+ * default pool (cudaMallocAsync), which keeps freed memory cached.  pcpm_pool_reserve
+ * maps `bytes` into that pool once (allocate + free, synchronous), so later builds and
+ * two layouts alive at once (pipelined jobs) carve from cached memory instead of
+ * mapping new memory mid-run.  0, PCPM_EINVAL (bytes < 0), PCPM_ENOMEM, PCPM_ECUDA. */
+int pcpm_pool_reserve(int64_t bytes);
 int pcpm_set_stream(pcpm_handle* h, void* cuda_stream);
 int pcpm_last_error(char* buf, int cap);   /* copies the message, returns its length */
 int pcpm_last_status(void);                /* code of the last failure on this thread */

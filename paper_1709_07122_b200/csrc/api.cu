@@ -49,6 +49,37 @@ void pool_setup(int device) {
   done[device] = true;
 }
 
+}  // namespace pcpm
+
+extern "C" int pcpm_pool_reserve(int64_t bytes) {
+  using namespace pcpm;
+  if (bytes < 0) {
+    set_error(PCPM_EINVAL, "bytes < 0");
+    return PCPM_EINVAL;
+  }
+  if (bytes == 0) return PCPM_OK;
+  int dev = 0;
+  PCPM_CK(cudaGetDevice(&dev));
+  pool_setup(dev);
+  cudaStream_t s;
+  PCPM_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  void* p = nullptr;
+  const cudaError_t e = cudaMallocAsync(&p, (size_t)bytes, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaStreamDestroy(s);
+    set_error(PCPM_ENOMEM, "pool reserve of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    return PCPM_ENOMEM;
+  }
+  cudaFreeAsync(p, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  PCPM_CK(e2);
+  return PCPM_OK;
+}
+
+namespace pcpm {
+
 int dev_alloc(pcpm_handle* h, void** p, size_t bytes) {
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMallocAsync(p, bytes, h->stream);

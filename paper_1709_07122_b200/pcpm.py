@@ -32,7 +32,7 @@ EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_p
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
             "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters",
             "pcpm_shard_step_peers", "pcpm_pagerank_tol", "pcpm_shard_init_peers", "pcpm_ipc_handle_bytes", "pcpm_ipc_alloc", "pcpm_ipc_free", "pcpm_ipc_get_handle",
-            "pcpm_ipc_open", "pcpm_ipc_close"]
+            "pcpm_ipc_open", "pcpm_ipc_close", "pcpm_pool_reserve"]
 
 
 class PcpmError(RuntimeError):
@@ -103,6 +103,7 @@ def _load():
         "pcpm_ipc_get_handle": (I, [P, P]),
         "pcpm_ipc_open": (I, [P, ctypes.POINTER(P)]),
         "pcpm_ipc_close": (I, [P]),
+        "pcpm_pool_reserve": (I, [I64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -198,6 +199,10 @@ def pcpm_scatter(h, x):
 def pcpm_destroy(h):
     if h:
         _lib.pcpm_destroy(h)
+
+
+def pcpm_pool_reserve(nbytes: int):
+    return _check(_lib.pcpm_pool_reserve(int(nbytes)))
 
 
 def pcpm_set_stream(h, stream):

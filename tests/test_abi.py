@@ -62,6 +62,10 @@ def test_invalid_arguments_rejected_without_gpu():
     with pytest.raises(pcpm.PcpmError) as e:
         pcpm.pcpm_pagerank(None, 0.85, 1, np.zeros(2, np.float32))
     assert e.value.code == pcpm.PCPM_EINVAL
+    with pytest.raises(pcpm.PcpmError) as e:
+        pcpm.pcpm_pool_reserve(-1)
+    assert e.value.code == pcpm.PCPM_EINVAL
+    assert pcpm.pcpm_pool_reserve(0) == pcpm.PCPM_OK      # nothing to map: no CUDA call
 
 
 def test_product_never_imports_the_oracle():

@@ -511,3 +511,49 @@ def test_pagerank_to_tolerance(pcpm, tol):
             pcpm.pcpm_pagerank_tol(h, 0.85, -1.0, 5, out)
     finally:
         pcpm.pcpm_destroy(h)
+
+
+def test_pipelined_jobs_match_single_build(pcpm):
+    """bench.py's e2e schedule: CSR uploaded on a copy stream while the previous job
+    iterates, built from the device copy on a compute stream (nnz passed from the host),
+    result downloaded on a third stream -- every job's PR is bit-identical to a plain
+    build + pcpm_pagerank; pcpm_pool_reserve leaves the pool usable."""
+    g = graphs.make_graph("rmat", 21, scale=13, permute=True)
+    assert pcpm.pcpm_pool_reserve(64 << 20) == pcpm.PCPM_OK
+    h = build(pcpm, g, 10)
+    try:
+        ref = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 12, ref)
+        ref = ref.cpu()
+    finally:
+        pcpm.pcpm_destroy(h)
+    rp = torch.from_numpy(np.ascontiguousarray(g.row_ptr)).pin_memory()
+    col = torch.from_numpy(np.ascontiguousarray(g.col).view(np.int32)).pin_memory()
+    comp, h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    stage = [(torch.empty_like(rp, device="cuda"), torch.empty_like(col, device="cuda")) for _ in range(2)]
+    ready = [torch.cuda.Event() for _ in range(2)]
+    dev = [torch.zeros(g.n_src, device="cuda") for _ in range(2)]
+    outs = []
+    prev = None
+    for k in range(3):
+        h2d.wait_stream(comp)
+        with torch.cuda.stream(h2d):
+            stage[k & 1][0].copy_(rp, non_blocking=True)
+            stage[k & 1][1].copy_(col, non_blocking=True)
+            ready[k & 1].record(h2d)
+        comp.wait_event(ready[k & 1])
+        if prev is not None:
+            pcpm.pcpm_destroy(prev)
+        csr = pcpm.make_csr(g.n_src, g.n_dst, stage[k & 1][0], stage[k & 1][1], None, nnz=int(rp[-1]))
+        prev = pcpm.pcpm_build_ex(csr, 10, 0, comp)
+        with torch.cuda.stream(comp):
+            pcpm.pcpm_pagerank(prev, 0.85, 12, dev[k & 1])
+        d2h.wait_stream(comp)
+        host = torch.empty(g.n_src, pin_memory=True)
+        with torch.cuda.stream(d2h):
+            host.copy_(dev[k & 1], non_blocking=True)
+        outs.append(host)
+    pcpm.pcpm_destroy(prev)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref)
