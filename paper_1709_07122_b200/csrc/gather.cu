@@ -664,7 +664,48 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
     sp_inv = ldexp(1.0, -spmv_fbits(*a.xmax, a.wexp));
   }
   double dang = 0.0, res = 0.0;
-  for (int64_t i = c0 + threadIdx.x; i < min(cnt, c0 + kSplitChunk); i += kSplitThreads) {
+  const int64_t c1 = min(cnt, c0 + kSplitChunk);
+  bool vec = PR && (c1 & 3) == 0 && (q & 3) == 0 && aligned16(a.hi + v0) && aligned16(a.pr_new + v0) && aligned16(a.spr_new + v0) &&
+             aligned16(a.inv_deg + v0) && aligned16(a.pr_old + v0) && aligned16(sb);
+  for (int r = 0; r < a.n_peer; ++r) vec = vec && aligned16(a.spr_peer[r] + v0);
+  if (vec) {
+    // 4 consecutive vertices per thread: one 16-byte load per slot, all slots' loads
+    // independent (the sums are exact integers, so the order is free)
+    for (int64_t i4 = c0 / 4 + threadIdx.x; i4 < c1 / 4; i4 += kSplitThreads) {
+      const uint32_t v = v0 + (uint32_t)(4 * i4);
+      const uint4 h4 = __ldcg(reinterpret_cast<const uint4*>(a.hi + v));
+      uint64_t t0 = (uint64_t)h4.x << 32, t1 = (uint64_t)h4.y << 32, t2 = (uint64_t)h4.z << 32,
+               t3 = (uint64_t)h4.w << 32;
+#pragma unroll 4
+      for (uint32_t sl = 0; sl < nsl; ++sl) {
+        const uint4 w = __ldcg(reinterpret_cast<const uint4*>(sb + (size_t)sl * (size_t)q) + i4);
+        t0 += w.x;
+        t1 += w.y;
+        t2 += w.z;
+        t3 += w.w;
+      }
+      *reinterpret_cast<uint4*>(a.hi + v) = make_uint4(0u, 0u, 0u, 0u);
+      const float4 idg = __ldg(reinterpret_cast<const float4*>(a.inv_deg + v));
+      const float4 po = __ldg(reinterpret_cast<const float4*>(a.pr_old + v));
+      const uint64_t tv[4] = {t0, t1, t2, t3};
+      const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
+      const float pov[4] = {po.x, po.y, po.z, po.w};
+      float pn[4], sp[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double prn = base_pr + a.d * ((double)(long long)tv[c] * inv_scale);
+        pn[c] = (float)prn;
+        sp[c] = pn[c] * idv[c] * fscale;
+        if (idv[c] == 0.0f) dang += prn;
+        res += fabs(prn - (double)pov[c]);
+      }
+      *reinterpret_cast<float4*>(a.pr_new + v) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+      *reinterpret_cast<float4*>(a.spr_new + v) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+      for (int r = 0; r < a.n_peer; ++r)
+        *reinterpret_cast<float4*>(a.spr_peer[r] + v) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+    }
+  }
+  for (int64_t i = c0 + threadIdx.x; !vec && i < c1; i += kSplitThreads) {
     const uint32_t v = v0 + (uint32_t)i;
     uint64_t tot = (uint64_t)__ldcg(&a.hi[v]) << 32;
     for (uint32_t sl = 0; sl < nsl; ++sl) {
