@@ -618,7 +618,12 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   std::vector<GatherItem> gi;
   std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
   uint32_t nslots = 0;
-  int slice_div = 2;                                   // PCPM_GATHER_SLICE_DIV: items per SM the cut aims at
+  // items per SM the cut aims at: 2 when bin sizes are skewed (the LPT order then has
+  // small slices to fill the tail), 1 when every bin is within 2x of the mean (cutting
+  // finer only adds slot traffic); PCPM_GATHER_SLICE_DIV overrides (A/B)
+  int64_t max_bin = 0;
+  for (int64_t j = 0; j < k_dst; ++j) max_bin = std::max<int64_t>(max_bin, (int64_t)hbin[j + 1] - (int64_t)hbin[j]);
+  int slice_div = (k_dst > 0 && max_bin * k_dst <= 2 * m) ? 1 : 2;
   if (const char* e = getenv("PCPM_GATHER_SLICE_DIV")) slice_div = std::max(1, atoi(e));
   int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (slice_div * h->num_sms)) / kTileAlign + 1) * kTileAlign);
   for (int64_t j = 0; j < k_dst; ++j) {
