@@ -145,6 +145,8 @@ def layout_bytes(info, iters_kind="pagerank", wide=False):
         gather = di * m + 4 * ep + 4 * n * 4      # ids, updates; outdeg + PR_old read, PR + SPR written
     else:
         gather = di * m + 4 * m + 4 * ep + 4 * info.n_dst   # ids, weights, updates; y written
+    if getattr(info, "compact_slots", 0):
+        gather += 2 * info.n_dst                   # the apply reads each vertex's accumulator slot
     return scatter, gather
 
 
@@ -170,6 +172,8 @@ def run_pcpm(args, world, rank, local):
         flags |= pcpm.PCPM_WIDE_IDS
     if args.no_compress:
         flags |= pcpm.PCPM_NO_COMPRESS
+    if args.slots:
+        flags |= pcpm.PCPM_COMPACT_SLOTS
     # the first build grows the stream-ordered memory pool; build_ms is the second one
     h = pcpm.pcpm_build_ex(csr, b, flags, stream)
     build_ms_cold = pcpm.pcpm_get_info(h).build_ms
@@ -292,7 +296,7 @@ def run_pcpm(args, world, rank, local):
             "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
             "paper_eq4_bvgas": round(model.bvgas_comm(n, m)),
         },
-        "options": args.opt,
+        "options": args.opt, "compact_slots": int(info.compact_slots) if hasattr(info, "compact_slots") else 0,
         "clocks": clk,
         "gpu_launches": int(launches),
     }
@@ -472,7 +476,8 @@ def e2e(args, g, b, iters, op, world):
         barrier(world)
         t0 = time.perf_counter()
         h = pcpm.pcpm_build_ex(csr, b, (pcpm.PCPM_WIDE_IDS if args.wide else 0) |
-                               (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0), None)
+                               (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0) |
+                               (pcpm.PCPM_COMPACT_SLOTS if args.slots else 0), None)
         layout_bytes = pcpm.pcpm_get_info(h).device_bytes
         if op == "pagerank":
             pcpm.pcpm_pagerank(h, 0.85, iters, res)
@@ -493,7 +498,8 @@ def e2e(args, g, b, iters, op, world):
     serial = {"value": round(m * iters * world / t / 1e9, 3), "unit": unit,
               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
               "seconds_per_step": round(t, 4), "includes": "H2D CSR + GPU build + iterations + D2H result"}
-    flags = (pcpm.PCPM_WIDE_IDS if args.wide else 0) | (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0)
+    flags = (pcpm.PCPM_WIDE_IDS if args.wide else 0) | (pcpm.PCPM_NO_COMPRESS if args.no_compress else 0) | \
+        (pcpm.PCPM_COMPACT_SLOTS if args.slots else 0)
     if op != "pagerank":
         # SpMV jobs move x in and y out on every multiply (13.4 GB per c5 job): PCIe-bound in
         # both directions, so overlapping the next CSR upload only adds contention (measured
@@ -745,6 +751,7 @@ def main():
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: run N independent replicas instead of one destination-sharded graph")
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
+    ap.add_argument("--slots", type=int, default=0, help="1: build with PCPM_COMPACT_SLOTS (accumulator slots)")
     args = ap.parse_args()
     if args.lib:                                   # A/B variant build of libpcpm.so
         os.environ["PCPM_LIB"] = os.path.abspath(args.lib)

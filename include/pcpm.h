@@ -49,6 +49,13 @@ extern "C" {
                                   the BVGAS-like traffic baseline of P:342-345, measured with our layout */
 #define PCPM_BUILD_PULL 0x2u   /* also build the in-adjacency (CSC) for pcpm_pull_pagerank */
 #define PCPM_KEEP_VALUES 0x4u  /* keep weight bins even if values == NULL (all ones) */
+#define PCPM_COMPACT_SLOTS 0x10u /* accumulator slots: when every destination partition has <= ~20K
+                                  vertices with in-edges (and no bin is split), the 2-byte IDs hold the
+                                  vertex's rank among its partition's vertices with in-edges, so the
+                                  gather's shared-memory accumulator shrinks and its TMA ring gets 6
+                                  stages instead of 4.  Results are identical; ignored (layout as
+                                  without the flag) for weighted / shard / wide handles or when the
+                                  condition fails (pcpm_get_info().compact_slots says which). */
 #define PCPM_WIDE_IDS 0x8u     /* iterate on the paper's 4-byte layout (global 31-bit IDs + MSB flag in
                                   destID bins, 4-byte PNG sources) instead of the default
                                   compact one (2-byte partition-local IDs: 15-bit offset + MSB flag,
@@ -84,7 +91,8 @@ typedef struct {
   int64_t device_bytes;     /* device memory held by the handle */
   double build_ms;          /* device time of the build (event-timed) */
   int64_t gather_items, scatter_items;  /* work-list sizes of the two kernels */
-  int32_t fixed_point_bits; /* F of the last pcpm_pagerank / pcpm_spmv call */
+  int32_t fixed_point_bits;
+  int32_t compact_slots;      /* 1: built with accumulator slots (PCPM_COMPACT_SLOTS applied) */ /* F of the last pcpm_pagerank / pcpm_spmv call */
 } pcpm_info;
 
 /* Device pointers to the built layout, for bit-exact tests (read-only).

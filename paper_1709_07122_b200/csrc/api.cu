@@ -138,6 +138,8 @@ int pr_fixed_bits(int64_t n) {
 GatherArgs base_args(pcpm_handle* h, int fbits) {
   GatherArgs a{};
   a.ids = h->wide ? static_cast<const void*>(h->ids) : static_cast<const void*>(h->ids16);
+  a.slot16 = h->wide ? nullptr : h->slot16;
+  a.acc_words = h->slot16 ? h->acc_words : (int)h->q;
   a.w = h->w;
   a.upd = h->upd;
   a.chunk_base = h->chunk_base;
@@ -733,6 +735,7 @@ int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
   i.gather_items = h->n_gitems;
   i.scatter_items = h->n_sitems;
   i.fixed_point_bits = h->fixed_bits;
+  i.compact_slots = h->slot16 ? 1 : 0;
   if (h->last_was_spmv && h->xmax) {   // same rule as spmv_fbits() in gather.cu
     float xm = 0.f;
     if (cudaMemcpy(&xm, h->xmax, 4, cudaMemcpyDeviceToHost) == cudaSuccess) {

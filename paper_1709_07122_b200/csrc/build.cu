@@ -113,6 +113,34 @@ __global__ void k_gather_ids(int64_t m, const uint32_t* __restrict__ perm, const
   }
 }
 
+// PCPM_COMPACT_SLOTS: one block per destination bin j.  has_in[j q + l] = 1 for every
+// local ID l in bin j; then (after a scan) ids16 local indices become slots.
+__global__ void k_mark_in(const uint32_t* __restrict__ bin_start, const uint16_t* __restrict__ ids16, int b,
+                          uint32_t* has_in) {
+  const uint32_t j = blockIdx.x;
+  const uint32_t s0 = bin_start[j], s1 = bin_start[j + 1];
+  const size_t base = (size_t)j << b;
+  for (uint32_t x = s0 + threadIdx.x; x < s1; x += blockDim.x) has_in[base + (ids16[x] & 0x7FFFu)] = 1u;
+}
+// slot16[v] = rank of v among its partition's vertices with in-edges (0xFFFF: none)
+__global__ void k_slots(int64_t n, int b, const uint32_t* __restrict__ has_in, const uint32_t* __restrict__ scan,
+                        uint16_t* slot16) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v0 = (v >> b) << b;
+    slot16[v] = has_in[v] ? (uint16_t)(scan[v] - scan[v0]) : (uint16_t)0xFFFFu;
+  }
+}
+__global__ void k_remap_ids(const uint32_t* __restrict__ bin_start, int b, const uint16_t* __restrict__ slot16,
+                            uint16_t* ids16) {
+  const uint32_t j = blockIdx.x;
+  const uint32_t s0 = bin_start[j], s1 = bin_start[j + 1];
+  const uint16_t* sl = slot16 + ((size_t)j << b);
+  for (uint32_t x = s0 + threadIdx.x; x < s1; x += blockDim.x) {
+    const uint16_t id = ids16[x];
+    ids16[x] = (uint16_t)((id & 0x8000u) | sl[id & 0x7FFFu]);
+  }
+}
+
 __global__ void k_ids16(int64_t m, const uint32_t* __restrict__ ids, uint32_t qmask, uint16_t* ids16) {
   GRID_STRIDE(x, m) {
     const uint32_t id = ids[x];
@@ -694,6 +722,37 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   TK(cudaMemsetAsync(h->xbuf, 0, sizeof(float) * (n_src + 8), s));
   TK(cudaStreamSynchronize(s));
   pt.mark("work lists + iteration state");
+  // ---- PCPM_COMPACT_SLOTS: accumulator slots (unweighted, unsplit, compact, non-shard layouts)
+  if (h->want_slots && !h->wide && !h->w && !h->shard && h->n_split_bins == 0 && k_dst > 0 && q >= 64) {
+    uint32_t *has_in, *scan;
+    TK(tmp.alloc(&has_in, k_dst * q + 1));
+    TK(tmp.alloc(&scan, k_dst * q + 1));
+    TK(cudaMemsetAsync(has_in, 0, sizeof(uint32_t) * (k_dst * q + 1), s));
+    k_mark_in<<<(unsigned)k_dst, 256, 0, s>>>(h->bin_id_start, h->ids16, h->b, has_in);
+    TK(cudaGetLastError());
+    size_t bytes = 0;
+    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, has_in, scan, k_dst * q + 1, s));
+    uint8_t* t;
+    TK(tmp.alloc(&t, bytes));
+    TK(cub::DeviceScan::ExclusiveSum(t, bytes, has_in, scan, k_dst * q + 1, s));
+    std::vector<uint32_t> pc(k_dst + 1);
+    TK(cudaMemcpy2DAsync(pc.data(), sizeof(uint32_t), scan, sizeof(uint32_t) * q, sizeof(uint32_t), k_dst + 1,
+                         cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+    uint32_t mx = 0;
+    for (int64_t j = 0; j < k_dst; ++j) mx = std::max(mx, pc[j + 1] - pc[j]);
+    const int words = (int)(((mx + 31) / 32) * 32);
+    if (words < q && gather_slots_fit(h->b, words)) {
+      const int64_t nd = k_dst * q;
+      if ((rc = dev_alloc_t(h, &h->slot16, nd))) return rc;
+      k_slots<<<grid_for(nd), kT, 0, s>>>(nd, h->b, has_in, scan, h->slot16);
+      k_remap_ids<<<(unsigned)k_dst, 256, 0, s>>>(h->bin_id_start, h->b, h->slot16, h->ids16);
+      TK(cudaGetLastError());
+      h->acc_words = words;
+      TK(cudaStreamSynchronize(s));
+    }
+    pt.mark("accumulator slots");
+  }
   return PCPM_OK;
 }
 
@@ -714,6 +773,7 @@ int build_layout_legacy(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   h->compressed = !(flags & PCPM_NO_COMPRESS);
   h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
   h->wide = (flags & PCPM_WIDE_IDS) != 0;
+  h->want_slots = (flags & PCPM_COMPACT_SLOTS) != 0;
   h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
   if (h->m_pad == 0) h->m_pad = kTileAlign;
 
@@ -963,6 +1023,7 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   h->compressed = !(flags & PCPM_NO_COMPRESS);
   h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
   h->wide = (flags & PCPM_WIDE_IDS) != 0;
+  h->want_slots = (flags & PCPM_COMPACT_SLOTS) != 0;
   h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
   if (h->m_pad == 0) h->m_pad = kTileAlign;
   const int64_t ng = k_src * k_dst;             // groups (p, j)

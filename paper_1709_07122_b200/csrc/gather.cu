@@ -60,7 +60,7 @@ struct StageMeta {
 #ifndef PCPM_GATHER_TILE_MODE
 #define PCPM_GATHER_TILE_MODE 0     // 0: 4096 x 4 stages, 1: 8192 x 2, 2: 2048 x 8 (compact PageRank)
 #endif
-template <typename IdT, bool W>
+template <typename IdT, bool W, bool SL = false>
 struct Cfg {
   static constexpr bool kCompact = sizeof(IdT) == 2;
   // compact PageRank (the hot configuration): 4096-ID tiles in a 4-stage ring,
@@ -74,7 +74,8 @@ struct Cfg {
 #ifndef PCPM_GATHER_STAGES
 #define PCPM_GATHER_STAGES 4
 #endif
-  static constexpr int kStages = kMode == 1 ? 2 : (kMode == 2 ? 8 : (kHot ? PCPM_GATHER_STAGES : 4));
+  // SL (accumulator slots, PCPM_COMPACT_SLOTS): the smaller accumulator leaves room for 6 stages
+  static constexpr int kStages = SL ? 6 : (kMode == 1 ? 2 : (kMode == 2 ? 8 : (kHot ? PCPM_GATHER_STAGES : 4)));
   // Consumer warps form two groups that take alternate stages (group g: stages
   // g, g+2, ...), so each warp decodes two sub-chunks per stage it sees and the
   // per-stage bookkeeping is paid once per 2 sub-chunks; both groups run at once.
@@ -144,16 +145,17 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
 // MULTI (PageRank shards with a fused exchange, pcpm_shard_step_peers): the apply
 // also stores each SPR group to a.spr_peer[0 .. n_peer) -- other ranks' buffers,
 // NVLink P2P -- and the kernel ends with a system-scope fence.
-template <typename IdT, bool W, bool PR, bool MULTI = false>
-__global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const GatherArgs a) {
-  using C = Cfg<IdT, W>;
+template <typename IdT, bool W, bool PR, bool MULTI = false, bool SL = false>
+__global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const GatherArgs a) {
+  using C = Cfg<IdT, W, SL>;
   constexpr int S = C::kStages;
   constexpr int P = C::kPer;
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t q = int64_t(1) << a.b;
-  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // q words (128 B rounded)
-  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;                           // 1 bit per 32 vertices
-  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
+  const int64_t aw = SL ? (int64_t)a.acc_words : q;                         // accumulator words (slots)
+  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // aw words (128 B rounded)
+  uint32_t* bitmap = acc + ((aw + 31) / 32) * 32;                          // 1 bit per 32 words
+  const int bm_words = (int)((aw + 1023) / 1024) < 4 ? 4 : (int)((aw + 1023) / 1024);
   uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + ((bm_words + 31) / 32) * 32);
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
                 if (vb) {
                   bulk_prefetch_l2(a.inv_deg + v0, vb);
                   bulk_prefetch_l2(a.pr_old + v0, vb);
+                  if (SL) bulk_prefetch_l2(a.slot16 + v0, vb / 2);
                 }
               }
             }
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
   const uint32_t qmask = (uint32_t)(q - 1);
   const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F (PageRank)
   const double inv_scale = 1.0 / (double)fscale;
-  for (int64_t i = ctid; i < q; i += kCons) acc[i] = 0u;
+  for (int64_t i = ctid; i < aw; i += kCons) acc[i] = 0u;
   for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
   double base_pr = 0.0;
   if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
@@ -514,6 +517,67 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
       };
       double dang = 0.0, res = 0.0;
       if (PCPM_GATHER_NO_EPI) run_apply = false;
+      if constexpr (SL) {
+        // accumulator slots: vertex v reads slot16[v] (bins are never split with slots);
+        // a vertex without in-edges has a zero sum.  4 consecutive vertices per thread when
+        // the partition length and the output pointers allow 16-byte accesses
+        run_apply = false;
+        auto slot_total = [&](uint32_t sl) -> uint64_t {
+          if (sl == 0xFFFFu) return 0;
+          uint64_t tot = PR ? (uint64_t)acc[sl] : (uint64_t)(long long)(int32_t)acc[sl];
+          if ((bitmap[sl >> 10] >> ((sl >> 5) & 31)) & 1u) {
+            tot += (uint64_t)ldcg_u32(&a.hi[v0 + sl]) << 32;
+            a.hi[v0 + sl] = 0u;
+          }
+          acc[sl] = 0u;
+          return tot;
+        };
+        const bool vec4 = (cnt & 3) == 0 &&
+                          (PR ? aligned16(a.pr_new + v0) && aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0) &&
+                                    aligned16(a.pr_old + v0)
+                              : aligned16(a.y + v0));
+        for (int64_t i = ctid; !vec4 && i < cnt; i += kCons) {      // unaligned output / short partition
+          const uint32_t v = v0 + (uint32_t)i;
+          const uint64_t tot = slot_total(a.slot16[v]);
+          if constexpr (PR) {
+            const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
+            a.pr_new[v] = (float)prn;
+            const float idg = __ldg(a.inv_deg + v);
+            a.spr_new[v] = (float)prn * idg * fscale;
+            if (idg == 0.0f) dang += prn;
+            res += fabs(prn - (double)a.pr_old[v]);
+          } else {
+            a.y[v] = (float)((double)(long long)tot * sp_inv);
+          }
+        }
+        for (int64_t i4 = ctid; vec4 && i4 < cnt / 4; i4 += kCons) {
+          const uint32_t v = v0 + (uint32_t)(4 * i4);
+          const uint2 s2 = __ldg(reinterpret_cast<const uint2*>(a.slot16 + v));
+          const uint32_t sl[4] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu, s2.y >> 16};
+          if constexpr (PR) {
+            const float4 idg = __ldg(reinterpret_cast<const float4*>(a.inv_deg + v));
+            const float4 po = __ldg(reinterpret_cast<const float4*>(a.pr_old + v));
+            const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
+            const float pov[4] = {po.x, po.y, po.z, po.w};
+            float pn[4], sp[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double prn = base_pr + a.d * ((double)(long long)slot_total(sl[c]) * inv_scale);
+              pn[c] = (float)prn;
+              sp[c] = pn[c] * idv[c] * fscale;
+              dang += idv[c] != 0.0f ? 0.0 : prn;
+              res += fabs(prn - (double)pov[c]);
+            }
+            *reinterpret_cast<float4*>(a.pr_new + v) = make_float4(pn[0], pn[1], pn[2], pn[3]);
+            *reinterpret_cast<float4*>(a.spr_new + v) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+          } else {
+            float yv[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) yv[c] = (float)((double)(long long)slot_total(sl[c]) * sp_inv);
+            *reinterpret_cast<float4*>(a.y + v) = make_float4(yv[0], yv[1], yv[2], yv[3]);
+          }
+        }
+      }
       if (run_apply) {
         if constexpr (PR) {
           bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
@@ -566,7 +630,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather(const Gathe
             a.y[v0 + (uint32_t)i] = (float)((double)(long long)total(i) * sp_inv);
         }
       }
-      for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
+      if (!SL)
+        for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
       if constexpr (PR) {
         for (int o = 16; o; o >>= 1) {
           dang += __shfl_xor_sync(0xffffffffu, dang, o);
@@ -772,10 +837,10 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
   }
 }
 
-template <typename IdT, bool W>
-int smem_bytes_for(int b) {
-  using C = Cfg<IdT, W>;
-  const int64_t q = int64_t(1) << b;
+template <typename IdT, bool W, bool SL = false>
+int smem_bytes_for(int b, int64_t aw = 0) {
+  using C = Cfg<IdT, W, SL>;
+  const int64_t q = aw > 0 ? aw : int64_t(1) << b;
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
@@ -784,7 +849,8 @@ int smem_bytes_for(int b) {
 
 using GatherFn = void (*)(const GatherArgs);
 
-GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false) {
+GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false, bool slots = false) {
+  if (slots) return pagerank ? k_gather<uint16_t, false, true, false, true> : k_gather<uint16_t, false, false, false, true>;
   if (multi) return wide ? k_gather<uint32_t, false, true, true> : k_gather<uint16_t, false, true, true>;
   if (wide)
     return weighted ? (pagerank ? k_gather<uint32_t, true, true> : k_gather<uint32_t, true, false>)
@@ -800,6 +866,16 @@ int gather_smem_bytes(int b, bool wide, bool weighted) {
   return weighted ? smem_bytes_for<uint16_t, true>(b) : smem_bytes_for<uint16_t, false>(b);
 }
 
+bool gather_slots_fit(int b, int acc_words) {
+  int dev = 0, maxsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return smem_bytes_for<uint16_t, false, true>(b, acc_words) <= maxsm;
+}
+
 int prepare_gather(pcpm_handle* h) {
   int maxsm = 0;
   PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
@@ -813,6 +889,9 @@ int prepare_gather(pcpm_handle* h) {
         PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   for (int wd = 0; wd < 2; ++wd)
     PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, false, true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  for (int p = 0; p < 2; ++p)
+    PCPM_CK(cudaFuncSetAttribute(gather_fn(false, false, p, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 maxsm));
       }
   return PCPM_OK;
 }
@@ -856,10 +935,11 @@ int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaS
 }
 
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi) {
-  const int smem = gather_smem_bytes(a.b, h->wide, weighted);
+  const bool slots = a.slot16 != nullptr && !weighted && !multi;
+  const int smem = slots ? smem_bytes_for<uint16_t, false, true>(a.b, a.acc_words) : gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
-  gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted)<<<grid, gather_threads(h->wide, weighted), smem,
-                                                                        s>>>(a);
+  gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted, slots)<<<grid, gather_threads(h->wide, weighted),
+                                                                                smem, s>>>(a);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return launch_apply_split(h, a, pagerank, s);     // split bins (small k), if any

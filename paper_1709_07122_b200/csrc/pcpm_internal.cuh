@@ -77,6 +77,9 @@ struct pcpm_handle {
   bool wide = false;                // iterate on the 4-byte arrays (PCPM_WIDE_IDS)
   uint32_t* ids = nullptr;          // [m_pad] 4-byte IDs (wide handles only)
   uint16_t* ids16 = nullptr;        // [m_pad] compact IDs: local | flag << 15
+  uint16_t* slot16 = nullptr;       // [n_dst] PCPM_COMPACT_SLOTS: accumulator slot of v (0xFFFF: no in-edges)
+  int acc_words = 0;                // slots per partition (rounded up), 0 = q (no slots)
+  bool want_slots = false;
   float* w = nullptr;               // [m_pad] or null
   uint32_t* png_src = nullptr;      // [E' (+pad)] 4-byte PNG sources (wide handles only)
   uint16_t* png16 = nullptr;        // [E' (+pad)] compact PNG sources: u & (q-1)
@@ -230,6 +233,8 @@ __device__ __forceinline__ uint32_t lanemask_le() {
 // ---------------------------------------------------------------- launchers
 struct GatherArgs {
   const void* ids;         // uint16_t* (compact) or uint32_t* (wide)
+  const uint16_t* slot16;  // accumulator slots (PCPM_COMPACT_SLOTS) or null
+  int acc_words;           // accumulator words (q without slots)
   const float* w;
   const float* upd;
   const uint32_t* chunk_base;
@@ -271,6 +276,7 @@ int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStr
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s,
                   bool multi = false);
 int gather_smem_bytes(int b, bool wide, bool weighted);
+bool gather_slots_fit(int b, int acc_words);   // the 6-stage slot kernel fits in shared memory
 
 int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
 int read_debug_counters(unsigned long long* out, int cap, bool reset);

@@ -557,3 +557,61 @@ def test_pipelined_jobs_match_single_build(pcpm):
     torch.cuda.synchronize()
     for o in outs:
         assert torch.equal(o, ref)
+
+
+@pytest.mark.parametrize("scale,b", [(16, 8), (17, 9)])
+def test_compact_slots_match(pcpm, scale, b):
+    """PCPM_COMPACT_SLOTS (accumulator slots = rank among the partition's vertices with
+    in-edges, 6-stage gather ring): PageRank and SpMV bit-identical to the default layout
+    and within the oracle bounds; the remapped IDs equal the oracle's local IDs mapped
+    through the per-partition ranks computed here from the oracle layout."""
+    g = graphs.make_graph("rmat", 31, scale=scale, permute=True)
+    h0 = build(pcpm, g, b)
+    h1 = build(pcpm, g, b, pcpm.PCPM_COMPACT_SLOTS)
+    try:
+        assert pcpm.pcpm_get_info(h1).compact_slots == 1, "slots not applied"
+        outs = []
+        for h in (h0, h1):
+            o = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, 15, o)
+            outs.append(o.cpu())
+        assert torch.equal(outs[0], outs[1])
+        pr_check(outs[1].numpy(), oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 15), "slots")
+        x = torch.from_numpy(graphs.make_x(g.n_src, 31)).cuda()
+        ys = []
+        for h in (h0, h1):
+            y = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_spmv(h, x, y)
+            ys.append(y.cpu())
+        assert torch.equal(ys[0], ys[1])
+        # IDs: slot = rank of the local ID among vertices with in-edges in its partition
+        ref = oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, b)
+        q = 1 << b
+        has_in = np.zeros(((g.n_dst + q - 1) // q) * q, dtype=bool)
+        has_in[np.asarray(g.col, dtype=np.int64)] = True
+        rank = (np.cumsum(has_in.reshape(-1, q), axis=1) - 1).reshape(-1)
+        ids_o = np.asarray(ref.ids, dtype=np.uint32)
+        v = (ids_o & np.uint32(0x7FFFFFFF)).astype(np.int64)
+        want = (rank[v].astype(np.uint32) | ((ids_o >> np.uint32(31)) << np.uint32(15))).astype(np.uint16)
+        np.testing.assert_array_equal(export(pcpm, h1)["ids16"], want)
+    finally:
+        pcpm.pcpm_destroy(h0)
+        pcpm.pcpm_destroy(h1)
+
+
+def test_compact_slots_ragged_partition(pcpm):
+    """Slots with a short last partition (n not a multiple of q or of 4): the scalar apply
+    path; PageRank identical to the default layout."""
+    g = graphs.make_graph("er", 33, n=3 * 4096 * 8 + 3, m_raw=400000)
+    h0 = build(pcpm, g, 8)
+    h1 = build(pcpm, g, 8, pcpm.PCPM_COMPACT_SLOTS)
+    try:
+        outs = []
+        for h in (h0, h1):
+            o = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, 9, o)
+            outs.append(o.cpu())
+        assert torch.equal(outs[0], outs[1])
+    finally:
+        pcpm.pcpm_destroy(h0)
+        pcpm.pcpm_destroy(h1)
