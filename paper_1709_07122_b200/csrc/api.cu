@@ -140,6 +140,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.ids = h->wide ? static_cast<const void*>(h->ids) : static_cast<const void*>(h->ids16);
   a.slot16 = h->wide ? nullptr : h->slot16;
   a.acc_words = h->slot16 ? h->acc_words : (int)h->q;
+  a.slotmap = h->wide ? nullptr : h->slotmap;
   a.w = h->w;
   a.upd = h->upd;
   a.chunk_base = h->chunk_base;

@@ -130,6 +130,15 @@ __global__ void k_slots(int64_t n, int b, const uint32_t* __restrict__ has_in, c
     slot16[v] = has_in[v] ? (uint16_t)(scan[v] - scan[v0]) : (uint16_t)0xFFFFu;
   }
 }
+__global__ void k_slotmap(int64_t nw, const uint32_t* __restrict__ has_in, const uint32_t* __restrict__ scan, int b,
+                          uint2* slotmap) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = w * 32, v0 = (v >> b) << b;
+    uint32_t bits = 0;
+    for (int i = 0; i < 32; ++i) bits |= (has_in[v + i] ? 1u : 0u) << i;
+    slotmap[w] = make_uint2(bits, scan[v] - scan[v0]);
+  }
+}
 __global__ void k_remap_ids(const uint32_t* __restrict__ bin_start, int b, const uint16_t* __restrict__ slot16,
                             uint16_t* ids16) {
   const uint32_t j = blockIdx.x;
@@ -747,6 +756,8 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
       if ((rc = dev_alloc_t(h, &h->slot16, nd))) return rc;
       k_slots<<<grid_for(nd), kT, 0, s>>>(nd, h->b, has_in, scan, h->slot16);
       k_remap_ids<<<(unsigned)k_dst, 256, 0, s>>>(h->bin_id_start, h->b, h->slot16, h->ids16);
+      if ((rc = dev_alloc_t(h, &h->slotmap, nd / 32))) return rc;
+      k_slotmap<<<grid_for(nd / 32), kT, 0, s>>>(nd / 32, has_in, scan, h->b, h->slotmap);
       TK(cudaGetLastError());
       h->acc_words = words;
       TK(cudaStreamSynchronize(s));

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // aw words (128 B rounded)
   uint32_t* bitmap = acc + ((aw + 31) / 32) * 32;                          // 1 bit per 32 words
   const int bm_words = (int)((aw + 1023) / 1024) < 4 ? 4 : (int)((aw + 1023) / 1024);
-  uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + ((bm_words + 31) / 32) * 32);
+  uint2* smap = reinterpret_cast<uint2*>(bitmap + ((bm_words + 31) / 32) * 32);  // slots: q/32 words
+  uint8_t* stage_base = reinterpret_cast<uint8_t*>(smap + (SL ? q / 32 : 0));
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
   uint64_t* empty = full + S;
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
                 if (vb) {
                   bulk_prefetch_l2(a.inv_deg + v0, vb);
                   bulk_prefetch_l2(a.pr_old + v0, vb);
-                  if (SL) bulk_prefetch_l2(a.slot16 + v0, vb / 2);
+                  if (SL) bulk_prefetch_l2(a.slotmap + v0 / 32, vb / 16);   // q/32 uint2 = q/4 bytes
                 }
               }
             }
@@ -522,6 +523,14 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
         // a vertex without in-edges has a zero sum.  4 consecutive vertices per thread when
         // the partition length and the output pointers allow 16-byte accesses
         run_apply = false;
+        const uint2* gmap = a.slotmap + ((size_t)m.j << a.b) / 32;
+        for (int64_t w = ctid; w < q / 32; w += kCons) smap[w] = __ldg(gmap + w);
+        named_bar_sync(1, kCons);
+        auto slot_of = [&](uint32_t i) -> uint32_t {   // local vertex i -> slot (0xFFFF: no in-edges)
+          const uint2 e = smap[i >> 5];
+          const uint32_t bit = 1u << (i & 31);
+          return (e.x & bit) ? e.y + __popc(e.x & (bit - 1u)) : 0xFFFFu;
+        };
         auto slot_total = [&](uint32_t sl) -> uint64_t {
           if (sl == 0xFFFFu) return 0;
           uint64_t tot = PR ? (uint64_t)acc[sl] : (uint64_t)(long long)(int32_t)acc[sl];
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
                               : aligned16(a.y + v0));
         for (int64_t i = ctid; !vec4 && i < cnt; i += kCons) {      // unaligned output / short partition
           const uint32_t v = v0 + (uint32_t)i;
-          const uint64_t tot = slot_total(a.slot16[v]);
+          const uint64_t tot = slot_total(slot_of((uint32_t)i));
           if constexpr (PR) {
             const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
             a.pr_new[v] = (float)prn;
@@ -552,8 +561,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
         }
         for (int64_t i4 = ctid; vec4 && i4 < cnt / 4; i4 += kCons) {
           const uint32_t v = v0 + (uint32_t)(4 * i4);
-          const uint2 s2 = __ldg(reinterpret_cast<const uint2*>(a.slot16 + v));
-          const uint32_t sl[4] = {s2.x & 0xFFFFu, s2.x >> 16, s2.y & 0xFFFFu, s2.y >> 16};
+          const uint32_t il = (uint32_t)(4 * i4);
+          const uint32_t sl[4] = {slot_of(il), slot_of(il + 1), slot_of(il + 2), slot_of(il + 3)};
           if constexpr (PR) {
             const float4 idg = __ldg(reinterpret_cast<const float4*>(a.inv_deg + v));
             const float4 po = __ldg(reinterpret_cast<const float4*>(a.pr_old + v));
@@ -842,7 +851,7 @@ int smem_bytes_for(int b, int64_t aw = 0) {
   using C = Cfg<IdT, W, SL>;
   const int64_t q = aw > 0 ? aw : int64_t(1) << b;
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
-  const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
+  const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4 + (SL ? ((int64_t(1) << b) / 32) * 8 : 0);
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
                2 * C::kWarps * 8 + 16);
 }

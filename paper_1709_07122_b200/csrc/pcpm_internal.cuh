@@ -79,6 +79,7 @@ struct pcpm_handle {
   uint16_t* ids16 = nullptr;        // [m_pad] compact IDs: local | flag << 15
   uint16_t* slot16 = nullptr;       // [n_dst] PCPM_COMPACT_SLOTS: accumulator slot of v (0xFFFF: no in-edges)
   int acc_words = 0;                // slots per partition (rounded up), 0 = q (no slots)
+  uint2* slotmap = nullptr;         // [k_dst * q/32] per 32 vertices: (in-edge bits, slots before the word)
   bool want_slots = false;
   float* w = nullptr;               // [m_pad] or null
   uint32_t* png_src = nullptr;      // [E' (+pad)] 4-byte PNG sources (wide handles only)
@@ -235,6 +236,7 @@ struct GatherArgs {
   const void* ids;         // uint16_t* (compact) or uint32_t* (wide)
   const uint16_t* slot16;  // accumulator slots (PCPM_COMPACT_SLOTS) or null
   int acc_words;           // accumulator words (q without slots)
+  const uint2* slotmap;    // slots: (in-edge bits, slot prefix) per 32 vertices
   const float* w;
   const float* upd;
   const uint32_t* chunk_base;

@@ -17,7 +17,7 @@ key = sys.argv[1] if len(sys.argv) > 1 else "c4"
 g = graphs.make_config(key, backend="torch", device="cuda")
 cfg = graphs.CONFIGS[key]
 bits = int(os.environ.get("PCPM_BITS", cfg["bits"]))
-h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values), bits, 0,
+h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, g.values), bits, int(os.environ.get("PCPM_FLAGS", "0")),
                        torch.cuda.current_stream())
 for kv in sys.argv[2:]:
     k, v = kv.split("=")
