@@ -60,7 +60,7 @@ int main(int argc, char** argv) {
     return 1;
   }
   pcpm_info info;
-  if (pcpm_get_info(h, &info) || pcpm_pagerank(h, 0.85f, 20, pr)) {
+  if (pcpm_get_info(h, &info) || pcpm_pagerank(h, 0.85, 20, pr)) {
     char msg[256];
     pcpm_last_error(msg, (int)sizeof msg);
     fprintf(stderr, "pcpm_pagerank failed: %s\n", msg);

@@ -91,8 +91,8 @@ typedef struct {
   int64_t device_bytes;     /* device memory held by the handle */
   double build_ms;          /* device time of the build (event-timed) */
   int64_t gather_items, scatter_items;  /* work-list sizes of the two kernels */
-  int32_t fixed_point_bits;
-  int32_t compact_slots;      /* 1: built with accumulator slots (PCPM_COMPACT_SLOTS applied) */ /* F of the last pcpm_pagerank / pcpm_spmv call */
+  int32_t fixed_point_bits;   /* F of the last pcpm_pagerank / pcpm_spmv call */
+  int32_t compact_slots;      /* 1: built with accumulator slots (PCPM_COMPACT_SLOTS applied) */
 } pcpm_info;
 
 /* Device pointers to the built layout, for bit-exact tests (read-only).
@@ -134,14 +134,14 @@ pcpm_handle* pcpm_build_ex(const pcpm_csr* csr, int partition_bits, unsigned fla
  * -> apply, captured in a CUDA graph.  out: n floats (host or device) receive
  * the unscaled PR_iters (R4).  iters = 0 returns 1/n.  PCPM_ESTATE if the
  * handle is not square. */
-int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out);
+int pcpm_pagerank(pcpm_handle* h, double d, int iters, float* out);
 /* PageRank iterated to convergence: the same iterations as pcpm_pagerank, run
  * until the L1 residual sum_v |PR_t(v) - PR_{t-1}(v)| (computed by the fused apply
  * of every iteration) is <= tol, or max_iters iterations.  out receives PR_t for
  * that t (host or device, n floats); *iters_done = t.  The host reads one residual
  * per iteration while the next iteration already runs (kernels launched directly,
  * no graph).  tol >= 0, max_iters >= 1; returns 0 or PCPM_E*. */
-int pcpm_pagerank_tol(pcpm_handle* h, float d, double tol, int max_iters, float* out, int* iters_done);
+int pcpm_pagerank_tol(pcpm_handle* h, double d, double tol, int max_iters, float* out, int* iters_done);
 
 /* y = M^T x (§3.5): y[v] = sum over CSR entries (u -> v) of
  * w(u,v) * x[u], with w = values given at build (1 if none).  x: n_src floats,
@@ -150,7 +150,7 @@ int pcpm_spmv(pcpm_handle* h, const float* x, float* y);
 
 /* Same PageRank computed by the naive pull-direction kernel (Alg. 1, P:86-99;
  * the in-house comparison of BASELINE.json).  Needs PCPM_BUILD_PULL. */
-int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out);
+int pcpm_pull_pagerank(pcpm_handle* h, double d, int iters, float* out);
 
 /* ---- Multi-GPU: destination shards.
  * Rank r owns the destination vertices [v_lo, v_hi) (v_lo a multiple of q = 2^b,
@@ -164,7 +164,7 @@ int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out);
  * local columns v - v_lo), keeping the GLOBAL out-degrees |N_o(u)| of all
  * sources (P:65's SPR divides by the full out-degree).  csr is borrowed, host or
  * device; only the slice's columns are validated.  flags: PCPM_WIDE_IDS,
- * PCPM_KEEP_VALUES.  NULL on error.
+ * PCPM_KEEP_VALUES.  NULL on error (PCPM_ESTATE if csr is not square).
  * pcpm_shard_init: PR_0 = 1/n_global on the slice (pr0, spr0: DEVICE f32[v_hi-v_lo])
  * and dang0 (DEVICE f64[1]) = the slice's share of D_0.
  * pcpm_shard_step: one iteration of Eq. 1 with rule R1 for the slice:
@@ -177,7 +177,7 @@ int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out);
 pcpm_handle* pcpm_build_shard(const pcpm_csr* csr, int partition_bits, int64_t v_lo, int64_t v_hi,
                               unsigned flags, void* cuda_stream);
 int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0);
-int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+int pcpm_shard_step(pcpm_handle* h, double d, const float* spr_in, const double* D_in, const float* pr_old,
                     float* pr_new, float* spr_out, double* red_out);
 
 /* pcpm_shard_step_peers: pcpm_shard_step with the SPR exchange fused into the apply
@@ -187,7 +187,8 @@ int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* 
  * full-SPR buffers -- peer device memory opened with pcpm_ipc_open, written over
  * NVLink / NVSwitch as the tiles finish -- so no all-gather follows.  spr_outs is a
  * HOST array of n_outs (1 .. PCPM_MAX_PEERS + 1) DEVICE pointers, each 16-byte
- * aligned for the vector path.  The gather ends with a system-scope fence: once the
+ * aligned for the vector path (n_outs > 1 is PCPM_ESTATE for handles built with
+ * PCPM_COMPACT_SLOTS).  The gather ends with a system-scope fence: once the
  * kernel completes its stores are visible to the peers; the caller orders each
  * peer's next iteration after a collective (dist.py: the all-reduce of red_out).
  * Returns 0 or PCPM_E*. */
@@ -195,7 +196,7 @@ int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* 
 /* pcpm_shard_init_peers: pcpm_shard_init writing SPR_0 of the slice to spr_outs[0]
  * and copying it to spr_outs[1..] (same layout as pcpm_shard_step_peers). */
 int pcpm_shard_init_peers(pcpm_handle* h, float* pr0, float* const* spr_outs, int n_outs, double* dang0);
-int pcpm_shard_step_peers(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+int pcpm_shard_step_peers(pcpm_handle* h, double d, const float* spr_in, const double* D_in, const float* pr_old,
                           float* pr_new, float* const* spr_outs, int n_outs, double* red_out);
 /* CUDA IPC plumbing for the fused exchange (one process per GPU).
  * pcpm_ipc_alloc / _free: a plain cudaMalloc'ed, zeroed exchange buffer (IPC handles
@@ -218,6 +219,10 @@ void pcpm_destroy(pcpm_handle* h);
  * two layouts alive at once (pipelined jobs) carve from cached memory instead of
  * mapping new memory mid-run.  0, PCPM_EINVAL (bytes < 0), PCPM_ENOMEM, PCPM_ECUDA. */
 int pcpm_pool_reserve(int64_t bytes);
+/* pcpm_set_stream: later calls order their device work on cuda_stream (NULL = the
+ * legacy default stream).  The handle's scratch is shared by all calls, so the call
+ * first synchronises the previous stream: work queued there completes before any
+ * work on the new one.  0, PCPM_EINVAL, PCPM_ECUDA. */
 int pcpm_set_stream(pcpm_handle* h, void* cuda_stream);
 int pcpm_last_error(char* buf, int cap);   /* copies the message, returns its length */
 int pcpm_last_status(void);                /* code of the last failure on this thread */

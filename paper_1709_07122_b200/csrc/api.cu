@@ -180,7 +180,7 @@ int mark(pcpm_handle* h, cudaStream_t s) {
 
 // Iteration t of Eq. 1: scatter (Alg. 4) then gather (Alg. 5) + apply, PR_t in
 // pr[t & 1] -> PR_{t+1} in pr_new; red[2t] = D_t in, red[2t+1] = residual, red[2t+2] = D_{t+1}.
-int enqueue_iteration(pcpm_handle* h, float d, int t, float* pr_new, cudaStream_t s) {
+int enqueue_iteration(pcpm_handle* h, double d, int t, float* pr_new, cudaStream_t s) {
   int rc;
   const bool wpr = h->opt_weighted_pr && h->inv_wdeg && h->w;      // weighted PageRank (R24)
   if ((rc = launch_scatter(h, h->spr, s))) return rc;              // Alg. 4
@@ -199,7 +199,7 @@ int enqueue_iteration(pcpm_handle* h, float d, int t, float* pr_new, cudaStream_
   return mark(h, s);
 }
 
-int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
+int enqueue_pagerank(pcpm_handle* h, double d, int iters, float* dst, cudaStream_t s) {
   int rc;
   const int fbits = pr_fixed_bits(h->n_src);
   h->fixed_bits = fbits;
@@ -222,7 +222,7 @@ int enqueue_pagerank(pcpm_handle* h, float d, int iters, float* dst, cudaStream_
   return PCPM_OK;
 }
 
-int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s) {
+int enqueue_pull(pcpm_handle* h, double d, int iters, float* dst, cudaStream_t s) {
   int rc;
   float* sprb[2] = {h->spr, h->xbuf};
   h->n_events_used = 0;
@@ -242,7 +242,7 @@ int enqueue_pull(pcpm_handle* h, float d, int iters, float* dst, cudaStream_t s)
   return PCPM_OK;
 }
 
-int run_captured(pcpm_handle* h, int kind, float d, int iters, float* dst) {
+int run_captured(pcpm_handle* h, int kind, double d, int iters, float* dst) {
   cudaStream_t s = h->stream;
   auto enq = [&](cudaStream_t st) { return kind == 0 ? enqueue_pagerank(h, d, iters, dst, st)
                                                       : enqueue_pull(h, d, iters, dst, st); };
@@ -281,12 +281,12 @@ int run_captured(pcpm_handle* h, int kind, float d, int iters, float* dst) {
   return PCPM_OK;
 }
 
-int pagerank_common(pcpm_handle* h, float d, int iters, float* out, int kind) {
+int pagerank_common(pcpm_handle* h, double d, int iters, float* out, int kind) {
   if (!h || !out) {
     set_error(PCPM_EINVAL, "NULL handle or output");
     return PCPM_EINVAL;
   }
-  if (!(d > 0.f && d < 1.f) || iters < 0) {
+  if (!(d > 0.0 && d < 1.0) || iters < 0) {
     set_error(PCPM_EINVAL, "d must be in (0,1) and iters >= 0");
     return PCPM_EINVAL;
   }
@@ -300,6 +300,9 @@ int pagerank_common(pcpm_handle* h, float d, int iters, float* out, int kind) {
   }
   int rc = ensure_red(h, iters);
   if (rc) return rc;
+  // refreshed on every call: a cached graph skips enqueue_pagerank, which also sets them
+  h->fixed_bits = kind == 0 ? pr_fixed_bits(h->n_src) : 0;
+  h->last_was_spmv = false;
   const bool dev_out = is_device_ptr(out);
   float* dst = dev_out ? out : h->ybuf;
   rc = run_captured(h, kind, d, iters, dst);
@@ -418,6 +421,12 @@ pcpm_handle* pcpm_build_shard(const pcpm_csr* csr, int partition_bits, int64_t v
     set_error(PCPM_ETOOBIG, "n >= 2^31: the MSB of a 4-byte ID is the run flag (P:172-173)");
     return nullptr;
   }
+  if (csr->n_src != csr->n_dst) {
+    // the apply reads the global out-degrees of the slice's vertices (outdeg + v_lo): the
+    // graph must be square (PageRank, Eq. 1)
+    set_error(PCPM_ESTATE, "pcpm_build_shard needs a square graph (n_src == n_dst)");
+    return nullptr;
+  }
   return build_common(csr, partition_bits, flags, cuda_stream, v_lo, v_hi);
 }
 
@@ -434,7 +443,7 @@ int pcpm_shard_init(pcpm_handle* h, float* pr0, float* spr0, double* dang0) {
   return launch_pr_init_slice(h, pr0, spr0, dang0, std::ldexp(1.0, pr_fixed_bits(h->n_global)), h->stream);
 }
 
-static int shard_step_common(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+static int shard_step_common(pcpm_handle* h, double d, const float* spr_in, const double* D_in, const float* pr_old,
                              float* pr_new, float* const* outs, int n_outs, double* red_out, const char* fn) {
   if (!h || !spr_in || !D_in || !pr_old || !pr_new || !outs || !red_out) {
     set_error(PCPM_EINVAL, "NULL handle or argument");
@@ -444,7 +453,7 @@ static int shard_step_common(pcpm_handle* h, float d, const float* spr_in, const
     set_error(PCPM_EINVAL, "n_outs must be in [1, PCPM_MAX_PEERS + 1]");
     return PCPM_EINVAL;
   }
-  if (!(d > 0.f && d < 1.f)) {
+  if (!(d > 0.0 && d < 1.0)) {
     set_error(PCPM_EINVAL, "d must be in (0,1)");
     return PCPM_EINVAL;
   }
@@ -457,6 +466,11 @@ static int shard_step_common(pcpm_handle* h, float d, const float* spr_in, const
   }
   if (!h->shard && h->n_src != h->n_dst) {
     set_error(PCPM_ESTATE, std::string(fn) + " needs a shard handle or a square matrix");
+    return PCPM_ESTATE;
+  }
+  if (n_outs > 1 && h->slot16) {
+    // the fused-exchange gather indexes its accumulator by vertex, not by slot
+    set_error(PCPM_ESTATE, std::string(fn) + ": handles built with PCPM_COMPACT_SLOTS take n_outs == 1");
     return PCPM_ESTATE;
   }
   cudaStream_t s = h->stream;
@@ -480,14 +494,14 @@ static int shard_step_common(pcpm_handle* h, float d, const float* spr_in, const
   return launch_gather(h, a, false, true, s, n_outs > 1);   // Alg. 5 + apply on the shard's vertices
 }
 
-int pcpm_shard_step(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+int pcpm_shard_step(pcpm_handle* h, double d, const float* spr_in, const double* D_in, const float* pr_old,
                     float* pr_new, float* spr_out, double* red_out) {
   float* outs[1] = {spr_out};
   return shard_step_common(h, d, spr_in, D_in, pr_old, pr_new, spr_out ? outs : nullptr, 1, red_out,
                            "pcpm_shard_step");
 }
 
-int pcpm_shard_step_peers(pcpm_handle* h, float d, const float* spr_in, const double* D_in, const float* pr_old,
+int pcpm_shard_step_peers(pcpm_handle* h, double d, const float* spr_in, const double* D_in, const float* pr_old,
                           float* pr_new, float* const* spr_outs, int n_outs, double* red_out) {
   return shard_step_common(h, d, spr_in, D_in, pr_old, pr_new, spr_outs, n_outs, red_out, "pcpm_shard_step_peers");
 }
@@ -564,14 +578,14 @@ pcpm_handle* pcpm_build(const pcpm_csr* csr, int partition_bits) {
   return pcpm_build_ex(csr, partition_bits, 0u, nullptr);
 }
 
-int pcpm_pagerank(pcpm_handle* h, float d, int iters, float* out) { return pagerank_common(h, d, iters, out, 0); }
+int pcpm_pagerank(pcpm_handle* h, double d, int iters, float* out) { return pagerank_common(h, d, iters, out, 0); }
 
-int pcpm_pagerank_tol(pcpm_handle* h, float d, double tol, int max_iters, float* out, int* iters_done) {
+int pcpm_pagerank_tol(pcpm_handle* h, double d, double tol, int max_iters, float* out, int* iters_done) {
   if (!h || !out || !iters_done) {
     set_error(PCPM_EINVAL, "NULL handle, output or iters_done");
     return PCPM_EINVAL;
   }
-  if (!(d > 0.f && d < 1.f) || max_iters < 1 || !(tol >= 0.0)) {
+  if (!(d > 0.0 && d < 1.0) || max_iters < 1 || !(tol >= 0.0)) {
     set_error(PCPM_EINVAL, "d must be in (0,1), max_iters >= 1, tol >= 0");
     return PCPM_EINVAL;
   }
@@ -630,7 +644,7 @@ int pcpm_pagerank_tol(pcpm_handle* h, float d, double tol, int max_iters, float*
   return PCPM_OK;
 }
 
-int pcpm_pull_pagerank(pcpm_handle* h, float d, int iters, float* out) {
+int pcpm_pull_pagerank(pcpm_handle* h, double d, int iters, float* out) {
   return pagerank_common(h, d, iters, out, 1);
 }
 
@@ -697,6 +711,9 @@ int pcpm_set_stream(pcpm_handle* h, void* cuda_stream) {
     set_error(PCPM_EINVAL, "NULL handle");
     return PCPM_EINVAL;
   }
+  // the handle's scratch (counters, carries, update bins, reductions) is shared by
+  // every call: work queued on the old stream completes before the new stream is used
+  PCPM_CK(cudaStreamSynchronize(h->stream));
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   return PCPM_OK;
 }

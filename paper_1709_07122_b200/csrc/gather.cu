@@ -889,19 +889,19 @@ int prepare_gather(pcpm_handle* h) {
   int maxsm = 0;
   PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   for (int wd = 0; wd < 2; ++wd)
-    for (int w = 0; w < 2; ++w)
-      for (int p = 0; p < 2; ++p) {
-        if (gather_smem_bytes(h->b, wd, w) > maxsm) {
-          set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit for this partition size");
-          return PCPM_ECUDA;
-        }
+    for (int w = 0; w < 2; ++w) {
+      if (gather_smem_bytes(h->b, wd, w) > maxsm) {
+        set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit for this partition size");
+        return PCPM_ECUDA;
+      }
+      for (int p = 0; p < 2; ++p)
         PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    }
   for (int wd = 0; wd < 2; ++wd)
     PCPM_CK(cudaFuncSetAttribute(gather_fn(wd, false, true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   for (int p = 0; p < 2; ++p)
     PCPM_CK(cudaFuncSetAttribute(gather_fn(false, false, p, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  maxsm));
-      }
   return PCPM_OK;
 }
 

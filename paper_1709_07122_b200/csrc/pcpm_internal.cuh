@@ -47,7 +47,7 @@ struct ScatterItem {       // source partition p, destination groups [j0, j1)
 struct Graph {             // cached CUDA graph of one pcpm_pagerank configuration
   cudaGraphExec_t exec = nullptr;
   int iters = -1;
-  float d = 0.f;
+  double d = 0.0;
   float* out = nullptr;
   int kind = 0;
   int64_t launches = 0;
@@ -288,7 +288,7 @@ int launch_pr_init(pcpm_handle* h, float* pr0, float* spr, double* red, int red_
 int launch_pr_init_weighted(pcpm_handle* h, float* pr0, float* spr, double* red, int red_n, float spr_scale,
                             cudaStream_t s);
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new,
-                          float* spr_out, double* red_t, float d, cudaStream_t s);
+                          float* spr_out, double* red_t, double d, cudaStream_t s);
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags);
 int order_scatter_items(pcpm_handle* h, cudaStream_t s);
 int build_shard_layout(pcpm_handle* h, const pcpm_csr* csr, int64_t lo, int64_t hi, unsigned flags);

@@ -125,7 +125,7 @@ int launch_pr_init_slice(pcpm_handle* h, float* pr0, float* spr, double* dang0, 
 }
 
 int launch_pull_iteration(pcpm_handle* h, const float* spr_in, const float* pr_old, float* pr_new, float* spr_out,
-                          double* red_t, float d, cudaStream_t s) {
+                          double* red_t, double d, cudaStream_t s) {
   const int grid = h->num_sms * 8;
   k_pull<<<grid, 256, 0, s>>>(h->n_dst, h->in_ptr, h->in_src, spr_in, h->outdeg, pr_old, pr_new, spr_out, red_t,
                               red_t, (double)d);

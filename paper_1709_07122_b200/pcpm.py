@@ -77,8 +77,8 @@ def _load():
     sig = {
         "pcpm_build": (P, [ctypes.POINTER(pcpm_csr), I]),
         "pcpm_build_ex": (P, [ctypes.POINTER(pcpm_csr), I, ctypes.c_uint, P]),
-        "pcpm_pagerank": (I, [P, ctypes.c_float, I, P]),
-        "pcpm_pull_pagerank": (I, [P, ctypes.c_float, I, P]),
+        "pcpm_pagerank": (I, [P, ctypes.c_double, I, P]),
+        "pcpm_pull_pagerank": (I, [P, ctypes.c_double, I, P]),
         "pcpm_spmv": (I, [P, P, P]),
         "pcpm_destroy": (None, [P]),
         "pcpm_set_stream": (I, [P, P]),
@@ -93,12 +93,12 @@ def _load():
         "pcpm_get_phase_times": (I, [P, P, I]),
         "pcpm_build_shard": (P, [ctypes.POINTER(pcpm_csr), I, I64, I64, ctypes.c_uint, P]),
         "pcpm_shard_init": (I, [P, P, P, P]),
-        "pcpm_shard_step": (I, [P, ctypes.c_float, P, P, P, P, P, P]),
+        "pcpm_shard_step": (I, [P, ctypes.c_double, P, P, P, P, P, P]),
         "pcpm_get_debug_counters": (I, [P, I, I]),
-        "pcpm_shard_step_peers": (I, [P, ctypes.c_float, P, P, P, P, ctypes.POINTER(P), I, P]),
+        "pcpm_shard_step_peers": (I, [P, ctypes.c_double, P, P, P, P, ctypes.POINTER(P), I, P]),
         "pcpm_shard_init_peers": (I, [P, P, ctypes.POINTER(P), I, P]),
         "pcpm_ipc_handle_bytes": (I, []),
-        "pcpm_pagerank_tol": (I, [P, ctypes.c_float, ctypes.c_double, I, P, ctypes.POINTER(I)]),
+        "pcpm_pagerank_tol": (I, [P, ctypes.c_double, ctypes.c_double, I, P, ctypes.POINTER(I)]),
         "pcpm_ipc_alloc": (I, [I64, ctypes.POINTER(P)]),
         "pcpm_ipc_free": (I, [P]),
         "pcpm_ipc_get_handle": (I, [P, P]),

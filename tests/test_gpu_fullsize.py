@@ -19,6 +19,7 @@ import pytest
 
 import oracle
 from inputs import graphs
+from tests.gpu_util import spmv_fbits
 
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
@@ -86,9 +87,10 @@ def test_fullsize_spmv(pcpm):
         for _ in range(3):                       # repeated multiplies (bench steps several)
             pcpm.pcpm_spmv(h, x, y)
         torch.cuda.synchronize()
-        fb = pcpm.pcpm_get_info(h).fixed_point_bits
         got = y.cpu().numpy()
         xh = x.cpu().numpy()
+        fb = spmv_fbits(g.values.cpu().numpy(), xh)     # from the inputs (R22), not from the library
+        assert pcpm.pcpm_get_info(h).fixed_point_bits == fb
     finally:
         pcpm.pcpm_destroy(h)
     gn = g.to_numpy()
@@ -144,3 +146,112 @@ def test_fullsize_host_build_equals_device_build(pcpm, key):
     finally:
         pcpm.pcpm_destroy(hd)
         pcpm.pcpm_destroy(hh)
+
+
+def _hash64(arrs):
+    """64-bit digest (blake2b) of the concatenated bytes of a sequence of arrays."""
+    import hashlib
+    hs = hashlib.blake2b(digest_size=8)
+    for a in arrs:
+        hs.update(np.ascontiguousarray(a).view(np.uint8))
+    return hs.hexdigest()
+
+
+def _compare_chunked(name, ptr, count, dtype, want, digests, step=1 << 26):
+    """GPU array at device `ptr` (count elements) equals want(lo, hi) chunk by chunk
+    (bounded host memory at c4 size); records both sides' 64-bit digests."""
+    from tests.gpu_util import d2h
+    import hashlib
+    hg, ho = hashlib.blake2b(digest_size=8), hashlib.blake2b(digest_size=8)
+    isz = np.dtype(dtype).itemsize
+    for lo in range(0, count, step):
+        hi = min(count, lo + step)
+        got = d2h(ptr + lo * isz, hi - lo, dtype)
+        exp = np.ascontiguousarray(want(lo, hi), dtype=dtype)
+        hg.update(got.view(np.uint8))
+        ho.update(exp.view(np.uint8))
+        if not np.array_equal(got.view(np.uint8), exp.view(np.uint8)):
+            bad = lo + int(np.argmax(got != exp))
+            raise AssertionError(f"{name}: first difference at element {bad}")
+    digests[name] = (hg.hexdigest(), ho.hexdigest())
+    assert digests[name][0] == digests[name][1]
+
+
+@pytest.mark.parametrize("key", ["c3", "c4", "c4bfs", "c5"])
+def test_fullsize_layout_matches_oracle(pcpm, key):
+    """a0 at the sizes bench.py runs: every layout array of the GPU build (default
+    compact layout, the bench's launch configuration) equals the oracle's plain-definition
+    layout (oracle.layout) bit for bit -- the 2-byte
+    arrays against the oracle's 4-byte bins re-encoded (R20) -- plus the decode anchors
+    by their definition and the out-degrees.  Prints per-array 64-bit digests."""
+    cfg = graphs.CONFIGS[key]
+    b = cfg["bits"]
+    g = graphs.make_config(key, backend="torch", device="cuda")
+    vals = g.values if key == "c5" else None
+    h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, vals), b, 0,
+                           torch.cuda.current_stream())
+    gn = g.to_numpy()
+    del g
+    torch.cuda.empty_cache()
+    digests = {}
+    try:
+        info = pcpm.pcpm_get_info(h)
+        v = pcpm.pcpm_export_layout(h)
+        ref = oracle.layout(gn.n_src, gn.n_dst, gn.row_ptr, gn.col, b, val=gn.values if key == "c5" else None)
+        m, ep, ks, kd = info.nnz, info.e_prime, info.k_src, info.k_dst
+        assert (m, ep, ks, kd) == (int(gn.row_ptr[-1]), ref.e_prime, ref.k_src, ref.k_dst)
+        qmask = np.uint32((1 << b) - 1)
+
+        def ids16(lo, hi):
+            x = ref.ids[lo:hi]
+            return ((x & qmask) | ((x >> np.uint32(31)) << np.uint32(15))).astype(np.uint16)
+        _compare_chunked("ids16", v.ids16, m, np.uint16, ids16, digests)
+        _compare_chunked("png_src16", v.png_src16, ep, np.uint16,
+                         lambda lo, hi: (ref.png_src[lo:hi] & qmask).astype(np.uint16), digests)
+        flat = lambda a: a.reshape(-1).astype(np.uint32)      # noqa: E731
+        for name, arr in [("png_off", flat(ref.png_off)), ("upd_off", flat(ref.upd_off)),
+                          ("bin_id_start", flat(ref.bin_id_start)), ("bin_upd_start", flat(ref.bin_upd_start)),
+                          ("out_degree", np.diff(gn.row_ptr).astype(np.uint32))]:
+            _compare_chunked(name, getattr(v, name), len(arr), np.uint32, lambda lo, hi, a=arr: a[lo:hi], digests)
+        if key == "c5":
+            _compare_chunked("w", v.w, m, np.float32, lambda lo, hi: ref.w[lo:hi], digests)
+        # decode anchors by their plain definition: chunk_base[c] = #flags in ids[0 .. 128 c)
+        ncb = m // 128 + 1
+        blk = np.zeros(ncb, dtype=np.uint64)          # blk[c + 1] = #flags in ids[128 c .. 128 c + 128)
+        step = 1 << 26
+        for lo in range(0, (ncb - 1) * 128, step):
+            hi = min((ncb - 1) * 128, lo + step)
+            blk[1 + lo // 128:1 + hi // 128] = (ref.ids[lo:hi] >> np.uint32(31)).reshape(-1, 128).sum(
+                axis=1, dtype=np.uint64)
+        cum = np.cumsum(blk).astype(np.uint32)
+        _compare_chunked("chunk_base", v.chunk_base, ncb, np.uint32, lambda lo, hi: cum[lo:hi], digests)
+    finally:
+        pcpm.pcpm_destroy(h)
+    print(f"{key}: m={m} E'={ep} k={kd} layout digests (gpu == oracle): "
+          + " ".join(f"{k}={d[0]}" for k, d in digests.items()))
+
+
+def test_fullsize_scatter_bit_exact(pcpm):
+    """a1 at c4 size: the scatter of a seeded x through the bench's layout equals the
+    oracle's Alg. 4 copy (oracle.scatter on the oracle layout) bit for bit."""
+    key = "c4"
+    cfg = graphs.CONFIGS[key]
+    g = graphs.make_config(key, backend="torch", device="cuda")
+    h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, None), cfg["bits"], 0,
+                           torch.cuda.current_stream())
+    gn = g.to_numpy()
+    del g
+    torch.cuda.empty_cache()
+    digests = {}
+    try:
+        x = np.random.default_rng(7).random(gn.n_src).astype(np.float32)
+        pcpm.pcpm_scatter(h, torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        info = pcpm.pcpm_get_info(h)
+        v = pcpm.pcpm_export_layout(h)
+        ref = oracle.scatter(oracle.layout(gn.n_src, gn.n_dst, gn.row_ptr, gn.col, cfg["bits"]), x)
+        assert len(ref) == info.e_prime
+        _compare_chunked("upd", v.upd, info.e_prime, np.uint32, lambda lo, hi: ref[lo:hi].view(np.uint32), digests)
+    finally:
+        pcpm.pcpm_destroy(h)
+    print(f"{key}: scatter of E'={info.e_prime} updates bit-exact, digest {digests['upd'][0]}")

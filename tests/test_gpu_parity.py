@@ -14,7 +14,7 @@ import pytest
 
 import oracle
 from inputs import graphs
-from tests.gpu_util import d2h, to_device
+from tests.gpu_util import d2h, spmv_fbits, to_device
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -329,7 +329,8 @@ def test_spmv_parity(pcpm, name, mk, b, wide):
         x = graphs.make_x(g.n_src, 5)
         y = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
         pcpm.pcpm_spmv(h, torch.from_numpy(x).cuda(), y)
-        fb = pcpm.pcpm_get_info(h).fixed_point_bits
+        fb = spmv_fbits(g.values, x)                   # from the inputs (R22), not from the library
+        assert pcpm.pcpm_get_info(h).fixed_point_bits == fb
         spmv_check(g, y.cpu().numpy(), x, fb)
         yh = np.zeros(g.n_dst, dtype=np.float32)
         pcpm.pcpm_spmv(h, x, yh)                       # host pointers (fp32 order may differ: R19)
@@ -353,7 +354,7 @@ def test_spmv_non_square(pcpm):
         x = rng.uniform(-1, 1, ns).astype(np.float32)
         y = np.zeros(nd, dtype=np.float32)
         pcpm.pcpm_spmv(h, x, y)
-        spmv_check(g, y, x, pcpm.pcpm_get_info(h).fixed_point_bits)
+        spmv_check(g, y, x, spmv_fbits(g.values, x))
         with pytest.raises(pcpm.PcpmError) as e:
             pcpm.pcpm_pagerank(h, 0.85, 2, np.zeros(ns, np.float32))
         assert e.value.code == pcpm.PCPM_ESTATE
