@@ -153,7 +153,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.has_split = h->n_split_bins > 0;
   a.bin_arrive = h->bin_arrive;
   a.hi = h->hi;
-  a.item_red = h->item_red;
+  a.red_fx = h->red_fx;
   a.b = h->b;
   a.n_dst = h->n_dst;
   a.fbits = fbits;
@@ -826,6 +826,15 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
       return PCPM_EINVAL;
     }
     h->opt_scatter_variant = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "gather_variant")) {
+    if (value < 1 || value > 2) {
+      set_error(PCPM_EINVAL, "gather_variant must be 1 (in-line epilogue) or 2 (apply through tensor memory)");
+      return PCPM_EINVAL;
+    }
+    h->opt_gather_variant = (int)value;
     free_graph(h);
     return PCPM_OK;
   }

@@ -471,6 +471,88 @@ __global__ void k_png_place_c(const int64_t* __restrict__ n_dev, const int64_t* 
 }
 
 
+// ---------------------------------------------------------------------------
+// Exclusive prefix sum of u32 counts (hand-written; out may alias in): per block of
+// kScanTile elements a sum, one block scans the block sums, then every block scans its
+// tile from its base.  Used for the bin / group / anchor offsets.
+constexpr int kScanThreads = 1024, kScanPer = 4, kScanTile = kScanThreads * kScanPer;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* wsum, uint32_t* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t ws = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+    uint32_t wi = ws;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    wsum[lane] = wi - ws;
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  return wsum[w] + inc - x;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_sums(const uint32_t* __restrict__ in, int64_t n,
+                                                             uint32_t* bsum) {
+  __shared__ uint32_t wsum[32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) x += base + k < n ? in[base + k] : 0u;
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t y = wsum[threadIdx.x];
+    for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = y;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_top(uint32_t* bsum, int64_t nb) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t tot;
+  uint32_t carry = 0;
+  for (int64_t c = 0; c < nb; c += kScanThreads) {
+    const int64_t i = c + threadIdx.x;
+    const uint32_t x = i < nb ? bsum[i] : 0u;
+    const uint32_t e = block_excl_scan(x, wsum, &tot);
+    if (i < nb) bsum[i] = carry + e;
+    carry += tot;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tiles(const uint32_t* in, uint32_t* out, int64_t n,
+                                                              const uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t tot;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanPer;
+  uint32_t v[kScanPer];
+  uint32_t x = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    v[k] = base + k < n ? in[base + k] : 0u;
+    x += v[k];
+  }
+  uint32_t run = bsum[blockIdx.x] + block_excl_scan(x, wsum, &tot);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k)
+    if (base + k < n) {
+      out[base + k] = run;
+      run += v[k];
+    }
+}
+
+
 // PCPM_BUILD_TIMING=1: synchronise and print the wall time of each build phase (stderr).
 struct PhaseTimer {
   bool on = getenv("PCPM_BUILD_TIMING") != nullptr;
@@ -513,6 +595,19 @@ struct Temp {                 // build scratch: stream-ordered pool memory, free
     }                                                                            \
     if (_e != cudaSuccess) return cuda_fail(_e, #call, __FILE__, __LINE__);     \
   } while (0)
+
+// out[i] = sum of in[0 .. i), i < n (out may alias in)
+int scan_excl_u32(Temp& tmp, const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return PCPM_OK;
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  uint32_t* bsum;
+  TK(tmp.alloc(&bsum, nb));
+  k_scan_sums<<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, bsum);
+  k_scan_top<<<1, kScanThreads, 0, s>>>(bsum, nb);
+  k_scan_tiles<<<(unsigned)nb, kScanThreads, 0, s>>>(in, out, n, bsum);
+  TK(cudaGetLastError());
+  return PCPM_OK;
+}
 
 template <typename KeyT, typename ValT>
 cudaError_t radix_sort_pairs(Temp& tmp, const KeyT* kin, KeyT* kout, const ValT* vin, ValT* vout, int64_t n,
@@ -588,13 +683,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   TK(tmp.alloc(&col_tot, k_dst + 1));
   col_scan(k_src, k_dst, G, h->upd_off, col_tot, s);
   TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
-  {
-    size_t bytes = 0;
-    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
-    uint8_t* t;
-    TK(tmp.alloc(&t, bytes));
-    TK(cub::DeviceScan::ExclusiveSum(t, bytes, col_tot, h->bin_upd_start, k_dst + 1, s));
-  }
+  if ((rc = scan_excl_u32(tmp, col_tot, h->bin_upd_start, k_dst + 1, s))) return rc;
   k_add_bin_start<<<grid_for(k_src * k_dst), kT, 0, s>>>(k_src, k_dst, h->bin_upd_start, h->upd_off);
   TK(cudaGetLastError());
 
@@ -604,11 +693,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
     TK(tmp.alloc(&cnt, nchunks + 1));
     k_chunk_counts16<<<grid_for(nchunks * 32), kT, 0, s>>>(nchunks, h->ids16, cnt);
     TK(cudaGetLastError());
-    size_t bytes = 0;
-    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, h->chunk_base, nchunks + 1, s));
-    uint8_t* t;
-    TK(tmp.alloc(&t, bytes));
-    TK(cub::DeviceScan::ExclusiveSum(t, bytes, cnt, h->chunk_base, nchunks + 1, s));
+    if ((rc = scan_excl_u32(tmp, cnt, h->chunk_base, nchunks + 1, s))) return rc;
   }
 
   pt.mark("pull CSC + offsets + anchors");
@@ -625,13 +710,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   k_sitems<<<grid_for(k_src * 32), kT, 0, s>>>(k_src, k_dst, G, target, kScatterMaxGroups, p_tail, tail_split, nullptr,
                                                si_cnt, nullptr);
   TK(cudaGetLastError());
-  {
-    size_t bytes = 0;
-    TK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, si_cnt, si_off, k_src + 1, s));
-    uint8_t* t;
-    TK(tmp.alloc(&t, bytes));
-    TK(cub::DeviceScan::ExclusiveSum(t, bytes, si_cnt, si_off, k_src + 1, s));
-  }
+  if ((rc = scan_excl_u32(tmp, si_cnt, si_off, k_src + 1, s))) return rc;
   std::vector<uint32_t> hbin(k_dst + 1);
   unsigned long long hdang = 0;
   uint32_t n_si = 0;
@@ -705,8 +784,6 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
     if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
     if (!sb.empty())
       TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
-    const int64_t blocks = (int64_t)sb.size() * ((q + 1023) / 1024);
-    if ((rc = dev_alloc_t(h, &h->split_red, std::max<int64_t>(2, 2 * blocks)))) return rc;
   }
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
@@ -724,7 +801,8 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
   TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
   if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
-  if ((rc = dev_alloc_t(h, &h->item_red, 2 * (size_t)h->n_gitems + 2))) return rc;
+  if ((rc = dev_alloc_t(h, &h->red_fx, 2))) return rc;
+  TK(cudaMemsetAsync(h->red_fx, 0, sizeof(unsigned long long) * 2, s));
   TK(cudaMemsetAsync(h->hi, 0, sizeof(uint32_t) * n_dst, s));
   TK(cudaMemsetAsync(h->counters, 0, sizeof(uint32_t) * 8, s));
   TK(cudaMemsetAsync(h->spr, 0, sizeof(float) * (n_src + 8), s));
@@ -1315,6 +1393,445 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   return finish_layout(h, tmp, pt, G, d_dang);
 }
 
+// ---------------------------------------------------------------------------
+// Counting construction (the default for k_dst <= kCountMaxK; DESIGN.md §5 "build").
+// The paper builds bins and PNG with two scans per partition; here the same
+// two passes run warp-per-segment over the CSR, with no sort:
+//   segment = a row range [u0, u1) of one source partition p (heavy partitions are cut
+//   into several), processed by ONE warp in CSR order (u ascending, v ascending);
+//   pass 1 (count): per (segment, j) the number of IDs and of runs (MSB-flagged IDs,
+//     Alg. 2's prev_bin test) -- plus out-degrees and validation;
+//   scans: id_base[s][j] = bin_id_start[j] + IDs of earlier segments in bin j;
+//     PNG group starts G (groups (p, j) in (p, j) order) and each segment's
+//     run offset inside its group;
+//   pass 2 (place): the same walk; an edge's slot = its segment's running base for
+//     bin j + its rank among the same-j edges of the 32-edge step (match_any), so
+//     each bin lists its IDs in (u, v) order and each PNG group its sources in u
+//     order -- exactly the oracle's layout, deterministic, no atomics on the output.
+// The running bases live in shared memory, one k_dst-entry array pair per warp.
+constexpr int kCntWarps = 8;              // warps (segments in flight) per CTA
+constexpr int64_t kCountMaxK = 2048;      // counters: 2 x k_dst u32 per warp (16 KB at k = 2048)
+
+struct BSeg {
+  uint32_t u0, u1, p, pad;
+};
+
+__global__ void k_fill_f32(int64_t n, float v, float* out) {
+  GRID_STRIDE(i, n) out[i] = v;
+}
+
+template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED>
+__global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
+    const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
+    const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst,
+    uint32_t* CI, uint32_t* CR, const uint32_t* __restrict__ G, uint32_t* outdeg, float* inv_deg,
+    unsigned long long* n_dang, uint32_t* err, uint16_t* ids16, uint32_t* ids32, float* w, uint16_t* png16,
+    uint32_t* png32) {
+  extern __shared__ uint32_t csm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* ci = csm + (size_t)warp * 2 * k_dst;    // IDs (count) / running ID slot (place) per bin j
+  uint32_t* cr = ci + k_dst;                         // runs (count) / running PNG slot (place) per bin j
+  const uint32_t qmask = (1u << b) - 1u;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t errs = 0;
+  for (;;) {
+    uint32_t sidx = 0;
+    if (lane == 0) sidx = atomicAdd(seg_ctr, 1u);
+    sidx = __shfl_sync(0xffffffffu, sidx, 0);
+    if (sidx >= (uint32_t)n_seg) break;
+    const BSeg sg = segs[sidx];
+    for (int64_t j = lane; j < k_dst; j += 32) {
+      if (PLACE) {
+        ci[j] = CI[(int64_t)sidx * k_dst + j];
+        cr[j] = CR[(int64_t)sidx * k_dst + j] + G[(int64_t)sg.p * k_dst + j];
+      } else {
+        ci[j] = 0u;
+        cr[j] = 0u;
+      }
+    }
+    __syncwarp();
+    uint32_t dang = 0;
+    for (uint32_t ub = sg.u0; ub < sg.u1; ub += 32) {
+      const uint32_t u = ub + lane;
+      const bool ur = u < sg.u1;
+      const int64_t rs64 = row_ptr[ur ? u : sg.u1];
+      const int64_t re64 = ur ? row_ptr[u + 1] : rs64;
+      if (!PLACE) {
+        if (ur) {
+          const int64_t dg = re64 - rs64;
+          if (dg < 0) errs |= 1u;
+          outdeg[u] = (uint32_t)(dg > 0 ? dg : 0);
+          inv_deg[u] = dg > 0 ? 1.0f / (float)dg : 0.0f;
+        }
+        dang += __popc(__ballot_sync(0xffffffffu, ur && re64 == rs64));
+      }
+      const int64_t bs = __shfl_sync(0xffffffffu, rs64, 0);
+      const int64_t be = __shfl_sync(0xffffffffu, re64, 31);
+      const uint32_t rs = (uint32_t)(rs64 - bs);         // row starts relative to the batch (m < 2^32)
+      uint32_t pv = 0, pj = 0;                           // edge before the step (lane 31 of the previous one)
+      for (int64_t x0 = bs; x0 < be; x0 += 32) {
+        const int64_t x = x0 + lane;
+        const bool valid = x < be;
+        const uint32_t v = valid ? col[x] : 0u;
+        const uint32_t xr = (uint32_t)(x - bs);
+        int r = 0;                                        // row of x: the last lane r with rs_r <= x
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const uint32_t t = __shfl_sync(0xffffffffu, rs, r + st);
+          if (t <= xr) r += st;
+        }
+        const bool first = __shfl_sync(0xffffffffu, rs, r) == xr;
+        uint32_t j = v >> b;
+        const uint32_t upv = __shfl_up_sync(0xffffffffu, v, 1), upj = __shfl_up_sync(0xffffffffu, j, 1);
+        const uint32_t prv = lane ? upv : pv, prj = lane ? upj : pj;
+        if (!PLACE && valid) {
+          if (v >= (uint32_t)n_dst) errs |= 2u;
+          if (!first && prv >= v) errs |= 4u;
+        }
+        if (j >= (uint32_t)k_dst) j = (uint32_t)k_dst - 1;   // invalid input: keep indices in range
+        const bool flag = !COMPRESS || first || prj != j;   // Alg. 2 prev_bin / MSB demarcation
+        const uint32_t F = __ballot_sync(0xffffffffu, valid && flag);
+        const uint32_t me = __match_any_sync(0xffffffffu, valid ? j : 0xFFFFFFFFu);
+        const bool lead = lane == 31 - __clz(me);         // highest lane of the same-j group
+        if (!PLACE) {
+          if (valid && lead) {
+            ci[j] += __popc(me);
+            cr[j] += __popc(me & F);
+          }
+        } else {
+          uint32_t bi = 0, br = 0;
+          if (valid) {
+            bi = ci[j];
+            br = cr[j];
+          }
+          __syncwarp();
+          if (valid) {
+            const uint32_t pos = bi + __popc(me & lt);
+            ids16[pos] = (uint16_t)((v & qmask) | (flag ? 0x8000u : 0u));
+            if (WIDE) ids32[pos] = v | (flag ? 0x80000000u : 0u);
+            if (WEIGHTED) w[pos] = val[x];
+            if (flag) {
+              const uint32_t pp = br + __popc(me & F & lt);
+              const uint32_t uu = ub + (uint32_t)r;
+              png16[pp] = (uint16_t)(uu & qmask);
+              if (WIDE) png32[pp] = uu;
+            }
+            if (lead) {
+              ci[j] = bi + __popc(me);
+              cr[j] = br + __popc(me & F);
+            }
+          }
+          __syncwarp();
+        }
+        pv = __shfl_sync(0xffffffffu, v, 31);
+        pj = __shfl_sync(0xffffffffu, j, 31);
+      }
+    }
+    __syncwarp();
+    if (!PLACE) {
+      for (int64_t j = lane; j < k_dst; j += 32) {
+        CI[(int64_t)sidx * k_dst + j] = ci[j];
+        CR[(int64_t)sidx * k_dst + j] = cr[j];
+      }
+      if (lane == 0 && dang) atomicAdd(n_dang, (unsigned long long)dang);
+    }
+    __syncwarp();
+  }
+  if (!PLACE) {
+    for (int o = 16; o; o >>= 1) errs |= __shfl_xor_sync(0xffffffffu, errs, o);
+    if (lane == 0 && errs) atomicOr(err, errs);
+  }
+}
+
+// Column prefix of a [rows x cols] count matrix, in place: cnt[r][c] <- sum_{r' < r} cnt[r'][c];
+// col_tot[c] = the column total.  Block = 32 columns x 32 row slabs (coalesced over c).
+__global__ void __launch_bounds__(1024) k_col_prefix(int64_t rows, int64_t cols, uint32_t* cnt, uint32_t* col_tot) {
+  __shared__ uint32_t part[32][33];
+  const int64_t c = blockIdx.x * 32 + threadIdx.x;
+  const int y = threadIdx.y;
+  const int64_t per = (rows + 31) / 32;
+  const int64_t r0 = min(rows, y * per), r1 = min(rows, r0 + per);
+  uint32_t sum = 0;
+  if (c < cols)
+    for (int64_t r = r0; r < r1; ++r) sum += cnt[r * cols + c];
+  part[y][threadIdx.x] = sum;
+  __syncthreads();
+  if (y == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t t = part[k][threadIdx.x];
+      part[k][threadIdx.x] = run;
+      run += t;
+    }
+    if (c < cols) col_tot[c] = run;
+  }
+  __syncthreads();
+  uint32_t run = part[y][threadIdx.x];
+  if (c < cols)
+    for (int64_t r = r0; r < r1; ++r) {
+      const uint32_t t = cnt[r * cols + c];
+      cnt[r * cols + c] = run;
+      run += t;
+    }
+}
+
+// Runs of partition p per bin j: RP[p][j] = sum over p's segments of CR[s][j]; CR
+// becomes each segment's run offset inside group (p, j) (segments of p in row order).
+__global__ void k_part_runs(int64_t k_src, int64_t k_dst, const uint32_t* __restrict__ seg_first, uint32_t* CR,
+                            uint32_t* RP) {
+  GRID_STRIDE(i, k_src * k_dst) {
+    const int64_t p = i / k_dst, j = i % k_dst;
+    uint32_t acc = 0;
+    for (uint32_t sg = seg_first[p]; sg < seg_first[p + 1]; ++sg) {
+      const uint32_t t = CR[(int64_t)sg * k_dst + j];
+      CR[(int64_t)sg * k_dst + j] = acc;
+      acc += t;
+    }
+    RP[i] = acc;
+  }
+}
+
+__global__ void k_add_row_base(int64_t rows, int64_t cols, const uint32_t* __restrict__ base, uint32_t* m) {
+  GRID_STRIDE(i, rows * cols) m[i] += base[i % cols];
+}
+
+// grp_at[c] = flat group g of PNG entry kPngChunk * c: the last g with G[g] <= x (empty
+// groups share their start with the next one)
+__global__ void k_grp_at_G(int64_t ep, const uint32_t* __restrict__ G, int64_t ng, int64_t n, uint32_t* grp_at) {
+  GRID_STRIDE(c, n) {
+    int64_t x = c * kPngChunk;
+    if (x >= ep) x = ep - 1;
+    int64_t lo = 0, hi = ng;                    // G[lo] <= x < G[hi] (G[ng] = ep > x)
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)G[mid] <= x) lo = mid;
+      else hi = mid;
+    }
+    grp_at[c] = (uint32_t)lo;
+  }
+}
+
+using SegPassFn = void (*)(const BSeg*, int, uint32_t*, const int64_t*, const uint32_t*, const float*, int, int64_t,
+                           int64_t, uint32_t*, uint32_t*, const uint32_t*, uint32_t*, float*, unsigned long long*,
+                           uint32_t*, uint16_t*, uint32_t*, float*, uint16_t*, uint32_t*);
+
+template <bool PLACE>
+SegPassFn seg_pass_fn(bool compress, bool wide, bool weighted) {
+#define PCPM_SEG_FN(C, WI, WE) \
+  if (compress == C && wide == WI && weighted == WE) return k_seg_pass<PLACE, C, WI, WE>;
+  PCPM_SEG_FN(true, false, false) PCPM_SEG_FN(true, false, true) PCPM_SEG_FN(true, true, false)
+  PCPM_SEG_FN(true, true, true) PCPM_SEG_FN(false, false, false) PCPM_SEG_FN(false, false, true)
+  PCPM_SEG_FN(false, true, false) PCPM_SEG_FN(false, true, true)
+#undef PCPM_SEG_FN
+  return nullptr;
+}
+
+int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+  cudaStream_t s = h->stream;
+  const int64_t n_src = csr->n_src, n_dst = csr->n_dst, m = csr->nnz;
+  const int b = h->b;
+  const int64_t q = int64_t(1) << b;
+  const int64_t k_src = (n_src + q - 1) / q, k_dst = (n_dst + q - 1) / q;
+  h->k_src = k_src;
+  h->k_dst = k_dst;
+  h->q = q;
+  h->n_src = n_src;
+  h->n_dst = n_dst;
+  h->m = m;
+  h->compressed = !(flags & PCPM_NO_COMPRESS);
+  h->weighted = csr->values != nullptr || (flags & PCPM_KEEP_VALUES);
+  h->wide = (flags & PCPM_WIDE_IDS) != 0;
+  h->want_slots = (flags & PCPM_COMPACT_SLOTS) != 0;
+  h->m_pad = ((m + kTileAlign - 1) / kTileAlign) * kTileAlign;
+  if (h->m_pad == 0) h->m_pad = kTileAlign;
+  const int64_t ng = k_src * k_dst;
+  Temp tmp(s);
+  PhaseTimer pt(s);
+  int rc;
+
+  // ---- inputs on the device (host CSR: one copy in, the passes need it twice)
+  const int64_t* row_ptr = csr->row_ptr;
+  const uint32_t* col = csr->col_idx;
+  const float* values = csr->values;
+  if (!is_device_ptr(row_ptr)) {
+    int64_t* d;
+    TK(tmp.alloc(&d, n_src + 1));
+    TK(cudaMemcpyAsync(d, row_ptr, sizeof(int64_t) * (n_src + 1), cudaMemcpyHostToDevice, s));
+    row_ptr = d;
+  }
+  if (!is_device_ptr(col)) {
+    uint32_t* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, col, sizeof(uint32_t) * m, cudaMemcpyHostToDevice, s));
+    col = d;
+  }
+  if (values && !is_device_ptr(values)) {
+    float* d;
+    TK(tmp.alloc(&d, m));
+    TK(cudaMemcpyAsync(d, values, sizeof(float) * m, cudaMemcpyHostToDevice, s));
+    values = d;
+  }
+
+  // ---- partition boundaries (host): global checks and the segment plan
+  std::vector<int64_t> pb(k_src + 1);
+  TK(cudaMemcpy2DAsync(pb.data(), sizeof(int64_t), row_ptr, sizeof(int64_t) * q, sizeof(int64_t), k_src,
+                       cudaMemcpyDeviceToHost, s));
+  TK(cudaMemcpyAsync(&pb[k_src], row_ptr + n_src, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  bool rp_ok = pb[0] == 0 && pb[k_src] == m;
+  for (int64_t p = 0; p < k_src && rp_ok; ++p) rp_ok = pb[p] <= pb[p + 1];
+  if (!rp_ok) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+  int64_t seg_target = std::max<int64_t>(int64_t(1) << 16, m / ((int64_t)h->num_sms * kCntWarps * 3) + 1);
+  if (const char* e = getenv("PCPM_BUILD_SEG_EDGES")) seg_target = std::max<int64_t>(1, atoll(e));   // tests
+  std::vector<BSeg> segs;
+  std::vector<uint32_t> seg_first(k_src + 1);
+  for (int64_t p = 0; p < k_src; ++p) {
+    seg_first[p] = (uint32_t)segs.size();
+    const int64_t u0 = p * q, u1 = std::min(n_src, u0 + q), rows = u1 - u0;
+    int64_t ns = std::max<int64_t>(1, std::min<int64_t>((pb[p + 1] - pb[p] + seg_target - 1) / seg_target,
+                                                        (rows + 31) / 32));
+    const int64_t per = ((rows + ns - 1) / ns + 31) / 32 * 32;      // rows per segment, whole 32-row batches
+    for (int64_t a = u0; a < u1; a += per)
+      segs.push_back(BSeg{(uint32_t)a, (uint32_t)std::min(u1, a + per), (uint32_t)p, 0u});
+  }
+  seg_first[k_src] = (uint32_t)segs.size();
+  const int64_t n_seg = (int64_t)segs.size();
+
+  // ---- layout arrays owned by the handle
+  uint32_t* ids32 = nullptr;
+  if (h->wide) {
+    if ((rc = dev_alloc_t(h, &h->ids, h->m_pad))) return rc;
+    ids32 = h->ids;
+    TK(cudaMemsetAsync(ids32 + m, 0, sizeof(uint32_t) * (h->m_pad - m), s));
+  }
+  if ((rc = dev_alloc_t(h, &h->ids16, h->m_pad))) return rc;
+  TK(cudaMemsetAsync(h->ids16 + m, 0, sizeof(uint16_t) * (h->m_pad - m), s));
+  if (h->weighted) {
+    if ((rc = dev_alloc_t(h, &h->w, h->m_pad))) return rc;
+    TK(cudaMemsetAsync(h->w + m, 0, sizeof(float) * (h->m_pad - m), s));
+  }
+  if ((rc = dev_alloc_t(h, &h->png_off, k_src * (k_dst + 1) + 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->upd_off, ng + 4))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_id_start, k_dst + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_upd_start, k_dst + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->chunk_base, h->m_pad / kChunkIds + 1))) return rc;
+  if ((rc = dev_alloc_t(h, &h->outdeg, n_src))) return rc;
+  if ((rc = dev_alloc_t(h, &h->inv_deg, n_src + 4))) return rc;
+
+  // ---- scratch
+  BSeg* d_segs;
+  uint32_t *d_seg_first, *ctr, *err, *CI, *CR, *RP, *G, *col_tot;
+  unsigned long long* d_dang;
+  TK(tmp.alloc(&d_segs, n_seg));
+  TK(tmp.alloc(&d_seg_first, k_src + 1));
+  TK(tmp.alloc(&ctr, 4));
+  TK(tmp.alloc(&err, 4));
+  TK(tmp.alloc(&d_dang, 1));
+  TK(tmp.alloc(&CI, n_seg * k_dst));
+  TK(tmp.alloc(&CR, n_seg * k_dst));
+  TK(tmp.alloc(&RP, ng + 1));
+  TK(tmp.alloc(&G, ng + 1));
+  TK(tmp.alloc(&col_tot, k_dst + 1));
+  TK(cudaMemcpyAsync(d_segs, segs.data(), sizeof(BSeg) * n_seg, cudaMemcpyHostToDevice, s));
+  TK(cudaMemcpyAsync(d_seg_first, seg_first.data(), sizeof(uint32_t) * (k_src + 1), cudaMemcpyHostToDevice, s));
+  TK(cudaMemsetAsync(ctr, 0, 16, s));
+  TK(cudaMemsetAsync(err, 0, 16, s));
+  TK(cudaMemsetAsync(d_dang, 0, 8, s));
+  pt.mark("count build: plan + allocations");
+
+  const bool weighted_ids = h->weighted && values != nullptr;
+  const size_t smem = (size_t)kCntWarps * 2 * k_dst * sizeof(uint32_t);
+  SegPassFn cnt_fn = seg_pass_fn<false>(h->compressed, h->wide, weighted_ids);
+  SegPassFn place_fn = seg_pass_fn<true>(h->compressed, h->wide, weighted_ids);
+  TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_seg + kCntWarps - 1) / kCntWarps, h->num_sms));
+
+  // ---- pass 1: counts, out-degrees, validation
+  cnt_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI, CR,
+                                            nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr, nullptr,
+                                            nullptr, nullptr);
+  TK(cudaGetLastError());
+  uint32_t herr = 0;
+  TK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  if (herr & 1u) {
+    set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
+    return PCPM_EBADCSR;
+  }
+  if (herr & 2u) {
+    set_error(PCPM_EBADCSR, "col_idx has an entry >= n_dst");
+    return PCPM_EBADCSR;
+  }
+  if (herr & 4u) {
+    set_error(PCPM_EBADCSR, "a row's columns are not strictly increasing (sorted, deduplicated) (R6)");
+    return PCPM_EBADCSR;
+  }
+  pt.mark("count build: pass 1 (count)");
+
+  // ---- scans: ID bases per (segment, bin), PNG groups and run offsets
+  k_col_prefix<<<(unsigned)((k_dst + 31) / 32), dim3(32, 32), 0, s>>>(n_seg, k_dst, CI, col_tot);
+  TK(cudaMemsetAsync(col_tot + k_dst, 0, 4, s));
+  if ((rc = scan_excl_u32(tmp, col_tot, h->bin_id_start, k_dst + 1, s))) return rc;
+  k_add_row_base<<<grid_for(n_seg * k_dst), kT, 0, s>>>(n_seg, k_dst, h->bin_id_start, CI);
+  k_part_runs<<<grid_for(ng), kT, 0, s>>>(k_src, k_dst, d_seg_first, CR, RP);
+  TK(cudaMemsetAsync(RP + ng, 0, 4, s));
+  if ((rc = scan_excl_u32(tmp, RP, G, ng + 1, s))) return rc;
+  TK(cudaGetLastError());
+  uint32_t hep = 0;
+  TK(cudaMemcpyAsync(&hep, G + ng, 4, cudaMemcpyDeviceToHost, s));
+  TK(cudaStreamSynchronize(s));
+  const int64_t ep = (int64_t)hep;
+  h->e_prime = ep;
+  if (h->wide) {
+    if ((rc = dev_alloc_t(h, &h->png_src, ep + 8))) return rc;
+    TK(cudaMemsetAsync(h->png_src + ep, 0, sizeof(uint32_t) * 8, s));
+  }
+  if ((rc = dev_alloc_t(h, &h->png16, ep + 16))) return rc;
+  TK(cudaMemsetAsync(h->png16 + ep, 0, sizeof(uint16_t) * 16, s));
+  pt.mark("count build: scans");
+
+  // ---- pass 2: place IDs (+ weights) and PNG sources
+  TK(cudaMemsetAsync(ctr, 0, 4, s));
+  place_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI, CR, G,
+                                              nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w, h->png16,
+                                              h->wide ? h->png_src : nullptr);
+  TK(cudaGetLastError());
+  if (h->weighted && !values) {
+    // PCPM_KEEP_VALUES without values: every weight is 1
+    k_fill_f32<<<grid_for(m), kT, 0, s>>>(m, 1.0f, h->w);
+    TK(cudaGetLastError());
+  }
+  pt.mark("count build: pass 2 (place)");
+
+  if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
+  TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+  {
+    const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
+    if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;
+    k_grp_at_G<<<grid_for(nga), kT, 0, s>>>(ep > 0 ? ep : 1, G, ng, nga, h->grp_at);
+    TK(cudaGetLastError());
+  }
+  if (values) {
+    float* mx;
+    TK(tmp.alloc(&mx, 1));
+    float hmx = 0.f;
+    int rc2 = launch_absmax(h, values, m, mx, s);
+    if (rc2) return rc2;
+    TK(cudaMemcpyAsync(&hmx, mx, 4, cudaMemcpyDeviceToHost, s));
+    TK(cudaStreamSynchronize(s));
+    int ex = 0;
+    if (hmx > 0.f) frexpf(hmx, &ex);
+    h->wexp = ex;
+    if ((rc2 = weighted_degrees(h, tmp, row_ptr, values))) return rc2;
+  }
+  return finish_layout(h, tmp, pt, G, d_dang);
+}
+
 }  // namespace
 
 // Layout construction: the chunked sort (default) or the two-sort legacy path
@@ -1322,6 +1839,11 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   const bool legacy = getenv("PCPM_BUILD_LEGACY") != nullptr;
   if (legacy || csr->nnz == 0 || csr->n_src <= 0 || csr->n_dst <= 0) return build_layout_legacy(h, csr, flags);
+  // the counting construction (default) unless the pull CSC is wanted or the bins are too many
+  const char* mode = getenv("PCPM_BUILD");                   // "sort": the chunked sort (A/B)
+  const int64_t q = int64_t(1) << h->b, k_dst = (csr->n_dst + q - 1) / q;
+  if (!(mode && !strcmp(mode, "sort")) && !(flags & PCPM_BUILD_PULL) && k_dst <= kCountMaxK)
+    return build_layout_count(h, csr, flags);
   return csr->values ? build_layout_chunked<PayW>(h, csr, flags) : build_layout_chunked<uint32_t>(h, csr, flags);
 }
 

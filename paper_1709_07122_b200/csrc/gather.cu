@@ -134,12 +134,292 @@ __device__ int spmv_fbits(float xmax, int wexp) {
 
 namespace {
 
+// fixed-point (dangling, residual) partials of one warp into the launch's totals (lane 0)
+__device__ __forceinline__ void warp_red_add(unsigned long long* red, unsigned long long dang, unsigned long long res,
+                                             int lane) {
+  for (int o = 16; o; o >>= 1) {
+    dang += __shfl_xor_sync(0xffffffffu, dang, o);
+    res += __shfl_xor_sync(0xffffffffu, res, o);
+  }
+  if (lane == 0) {
+    if (dang) atomicAdd(red, dang);
+    if (res) atomicAdd(red + 1, res);
+    __threadfence();
+  }
+}
+// after every partial is in: D_{t+1} and the residual as doubles, totals reset to zero
+__device__ __forceinline__ void red_finish(const GatherArgs& a) {
+  const unsigned long long dg = __ldcg(a.red_fx), rs = __ldcg(a.red_fx + 1);
+  *a.dang_out = (double)dg / kRedScale;
+  *a.res_out = (double)rs / kRedScale;
+  a.red_fx[0] = 0ull;
+  a.red_fx[1] = 0ull;
+}
+
 __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
   float mx = 0.0f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     mx = fmaxf(mx, fabsf(x[i]));
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
+}
+
+// Warp 0 of a gather CTA: claims work items and streams their tiles (IDs, update
+// window, decode anchors, weights) into the ring of S stages with bulk async copies.
+template <typename C, typename IdT, bool W, bool PR, bool SL>
+__device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* ids, uint8_t* stage_base,
+                                                StageMeta* meta, uint64_t* full, uint64_t* empty, int lane) {
+  constexpr int S = C::kStages;
+  // ================= producer (whole warp; lane 0 issues) =================
+  // The window of tile t is fixed by two decode anchors (chunk_base at the
+  // tile's ends).  Lanes load the anchors of 32 tiles at once, so the issue
+  // loop carries no dependent global load per tile.
+  const uint64_t pol = policy_evict_first();
+  int stage = 0;
+  uint32_t phase = 0;
+  auto claim = [&]() -> uint32_t {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(&a.counters[0], 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  auto push_meta = [&](const StageMeta& m) {      // a stage without data (empty item / stop)
+    if (lane == 0) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      meta[stage] = m;
+      mbar_arrive(&full[stage]);
+    }
+    __syncwarp();
+    if (++stage == S) { stage = 0; phase ^= 1; }
+  };
+  uint32_t it = claim();
+  GatherItem item{};
+  if (it < (uint32_t)a.n_items) item = a.items[it];
+  for (;;) {
+    if (it >= (uint32_t)a.n_items) {
+      StageMeta m{};
+      m.item = -1;
+      m.flags = kFlagStop;
+      push_meta(m);                              // one per consumer group
+      push_meta(m);
+      break;
+    }
+    // claim the next item now so its descriptor load overlaps this item's issue loop
+    const uint32_t it_next = claim();
+    GatherItem item_next{};
+    if (it_next < (uint32_t)a.n_items) item_next = a.items[it_next];
+    if (item.x0 == item.x1) {
+      StageMeta m{};
+      m.item = (int)it;
+      m.j = item.j;
+      m.flags = kFlagLast | kFlagEmpty;
+      push_meta(m);                              // both groups run the item's epilogue
+      push_meta(m);
+    } else {
+      const uint32_t t0 = item.x0 / C::kTile, t1 = (item.x1 - 1) / C::kTile;
+      for (uint32_t tb0 = t0; tb0 <= t1; tb0 += 32) {
+        const uint32_t tl = tb0 + lane;
+        uint32_t fa = 0, fb = 0;                 // #flags before the tile's first / after its last ID
+        if (tl <= t1) {
+          const uint32_t tb = tl * C::kTile;
+          fa = (tl == t0) ? item.fx0 : __ldg(a.chunk_base + tb / kChunkIds);
+          fb = (tl == t1) ? item.fx1 : __ldg(a.chunk_base + (tb + C::kTile) / kChunkIds);
+        }
+        const uint32_t nb = min(32u, t1 - tb0 + 1);
+        const uint32_t pf = (uint32_t)a.pf_tiles;
+        // L2 prefetch of the batch's first pf tiles (the ring then loads them from L2)
+        if (pf && lane < nb && lane < pf) {
+          const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
+          bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
+          if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+        }
+        for (uint32_t k = 0; k < nb; ++k) {
+          const uint32_t flo = __shfl_sync(0xffffffffu, fa, k);
+          const uint32_t fhi = __shfl_sync(0xffffffffu, fb, k);
+          // keep the L2 prefetch pf tiles ahead of the ring (within the batch)
+          if (pf && lane == k + pf && lane < nb) {
+            const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
+            bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
+            if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+          }
+          if constexpr (PR) {
+            // the apply's vertex arrays of partition j into L2 a few tiles before the epilogue
+            if (a.epi_pf && lane == 0 && tb0 + k == (t1 > t0 + (uint32_t)a.epi_pf ? t1 - (uint32_t)a.epi_pf : t0)) {
+              const int64_t v0 = (int64_t)item.j << a.b;
+              const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
+              if (vb) {
+                bulk_prefetch_l2(a.inv_deg + v0, vb);
+                bulk_prefetch_l2(a.pr_old + v0, vb);
+                if (SL) bulk_prefetch_l2(a.slotmap + v0 / 32, vb / 16);   // q/32 uint2 = q/4 bytes
+              }
+            }
+          }
+          if (lane == 0) {
+            const uint32_t t = tb0 + k;
+            const uint32_t tb = t * C::kTile;
+            const uint32_t wlo = flo > 0 ? flo - 1 : 0;   // the first ID may continue the previous run
+            const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
+            mbar_wait(&empty[stage], phase ^ 1);
+            StageMeta m{};
+            m.item = (int)it;
+            m.j = item.j;
+            m.lo = max(tb, item.x0);
+            m.hi = min(tb + C::kTile, item.x1);
+            m.tile_base = tb;
+            m.win_base = alo;
+            // the item's final stage of EACH group is flagged Last: tiles t1 and t1 - 1
+            m.flags = (t + 1 >= t1 + (t1 > t0 ? 0u : 1u)) ? kFlagLast : 0u;
+            meta[stage] = m;
+            uint8_t* sb = stage_base + stage * C::kStageBytes;
+            const uint32_t win_bytes = (ahi - alo) * 4;
+            mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
+            bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
+            bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
+            bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
+                     &full[stage], pol);
+            if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+      if (t1 == t0) {                             // single tile: the other group still needs its Last
+        StageMeta m{};
+        m.item = (int)it;
+        m.j = item.j;
+        m.flags = kFlagLast | kFlagEmpty;
+        push_meta(m);
+      }
+    }
+    it = it_next;
+    item = item_next;
+  }
+}
+
+// Decode of one full stage by one consumer warp (Alg. 5): the
+// warp takes sub-chunks gw, gw + gsz, ... of the stage's tile (plus its turn of the
+// rotating remainder) and adds each ID's update into the shared accumulator.
+template <typename C, typename IdT, bool W, bool PR>
+__device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMeta& m, const uint8_t* sb,
+                                             uint32_t* acc, uint32_t* bitmap, const int gw, const int gsz,
+                                             int& rot, const uint32_t qmask, const uint32_t lemask, const int lane,
+                                             const float sp_scale_f, const uint32_t v0) {
+  constexpr int P = C::kPer;
+  const IdT* ids_s = reinterpret_cast<const IdT*>(sb);
+  const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
+  const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
+  const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
+  auto process = [&](const int sc) {
+  const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
+  if (!PCPM_GATHER_NOOP && xs < m.hi && xs + C::kSub > m.lo) {
+    const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
+    auto body = [&](auto WHOLE) {
+      constexpr bool kWhole = decltype(WHOLE)::value;
+      // lane-strided decode: step c covers the 32 consecutive IDs c*32 .. c*32+31
+      // of the sub-chunk, so the window reads of a step hit ~32/r consecutive
+      // words (one or two smem wavefronts)
+      // IDs are read sign-extended: the run flag (MSB) becomes the sign, one
+      // compare per ID for the ballot
+      using SIdT = typename std::conditional<sizeof(IdT) == 2, int16_t, int32_t>::type;
+      const SIdT* sids = reinterpret_cast<const SIdT*>(ids_s);
+      uint32_t id[P];
+#pragma unroll
+      for (int c = 0; c < P; ++c) id[c] = (uint32_t)(int32_t)sids[sc * C::kSub + c * 32 + lane];
+      // Alg. 5 update_ptr = #flags in ids[0..x] - 1 (R5), from the sub-chunk's
+      // anchor plus a warp prefix count of the MSB flags, step by step
+      uint32_t run = cb_s[(sc * C::kSub) / kChunkIds] - 1u - m.win_base;
+      float val[P];
+      bool ok[P];
+#pragma unroll
+      for (int c = 0; c < P; ++c) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (int32_t)id[c] < 0);
+        const uint32_t ptr = run + __popc(bal & lemask);
+        run += __popc(bal);
+        const uint32_t x = xs + c * 32 + lane;
+        ok[c] = kWhole || (x >= m.lo && x < m.hi);
+        val[c] = ok[c] ? win_s[ptr] : 0.0f;
+      }
+      if constexpr (PR) {
+        // PageRank: the apply stores SPR * 2^F (a power-of-two scaling, exact in fp32),
+        // so one conversion rounds each term to the 2^-F grid
+        uint32_t tlo[P], thi[P], old[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          // SPR is stored as SPR * 2^F; weighted PageRank (R24) applies w(u,v) here
+          const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+          const unsigned long long T = __float2ull_rn(tv);
+          tlo[c] = (uint32_t)T;
+          thi[c] = (uint32_t)(T >> 32);
+        }
+#pragma unroll
+        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+        // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
+        // ok = false have lo = hi = 0 (val = 0) and never carry
+        uint32_t any = 0;
+#pragma unroll
+        for (int c = 0; c < P; ++c) any |= thi[c] | (tlo[c] > ~old[c] ? 1u : 0u);
+        if (any) {                                   // rare: carry into the global high word
+#pragma unroll
+          for (int c = 0; c < P; ++c) {
+            const uint32_t hinc = thi[c] + (tlo[c] > ~old[c] ? 1u : 0u);
+            if (hinc) {
+              const uint32_t li = id[c] & qmask;
+              atomicAdd(&a.hi[v0 + li], hinc);
+              atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+            }
+          }
+        }
+      } else {
+        // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
+        // word is read as a signed int32, so a running sum that hovers
+        // around zero never wraps; only signed overflow of the low word
+        // (|partial| >= 2^31 units) carries +-1 into the global high word.
+        // w*x is rounded once to fp32 (<= 2^-24 |w x|, R22); F keeps
+        // |w x| 2^F <= 2^30, so each term T is an int32 and the high part of the
+        // balanced form is zero: only the low word's signed overflow carries.
+        uint32_t tlo[P], old[P];
+        int32_t thi[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+          tlo[c] = (uint32_t)__float2int_rn(tv * sp_scale_f);
+          thi[c] = 0;
+        }
+#pragma unroll
+        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+        uint32_t any = 0;
+        int32_t hinc[P];
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const uint32_t nw = old[c] + tlo[c];
+          const bool ovf = (int32_t)((old[c] ^ nw) & (tlo[c] ^ nw)) < 0;
+          hinc[c] = ok[c] ? thi[c] + (ovf ? ((int32_t)old[c] < 0 ? -1 : 1) : 0) : 0;
+          any |= (uint32_t)hinc[c];
+        }
+        if (any) {
+#pragma unroll
+          for (int c = 0; c < P; ++c)
+            if (hinc[c]) {
+              const uint32_t li = id[c] & qmask;
+              atomicAdd(&a.hi[v0 + li], (uint32_t)hinc[c]);
+              atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+            }
+        }
+      }
+    };
+    if (whole) body(std::true_type{});
+    else body(std::false_type{});
+  }
+  };
+  // sub-chunks gw, gw + gsz, ... of the stage; the remaining kNsc mod gsz
+  // sub-chunks rotate over the group's warps from stage to stage
+  const int nmain = (C::kNsc / gsz) * gsz;
+  for (int sc = gw; sc < nmain; sc += gsz) process(sc);
+  int who = rot;
+  for (int sc = nmain; sc < C::kNsc; ++sc) {
+    if (gw == who) process(sc);
+    who = (who + 1 == gsz) ? 0 : who + 1;
+  }
+  rot = who;
 }
 
 // MULTI (PageRank shards with a fused exchange, pcpm_shard_step_peers): the apply
@@ -176,129 +456,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   __syncthreads();
 
   if (warp == 0) {
-    // ================= producer (whole warp; lane 0 issues) =================
-    // The window of tile t is fixed by two decode anchors (chunk_base at the
-    // tile's ends).  Lanes load the anchors of 32 tiles at once, so the issue
-    // loop carries no dependent global load per tile.
-    const uint64_t pol = policy_evict_first();
-    int stage = 0;
-    uint32_t phase = 0;
-    auto claim = [&]() -> uint32_t {
-      uint32_t v = 0;
-      if (lane == 0) v = atomicAdd(&a.counters[0], 1u);
-      return __shfl_sync(0xffffffffu, v, 0);
-    };
-    auto push_meta = [&](const StageMeta& m) {      // a stage without data (empty item / stop)
-      if (lane == 0) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        meta[stage] = m;
-        mbar_arrive(&full[stage]);
-      }
-      __syncwarp();
-      if (++stage == S) { stage = 0; phase ^= 1; }
-    };
-    uint32_t it = claim();
-    GatherItem item{};
-    if (it < (uint32_t)a.n_items) item = a.items[it];
-    for (;;) {
-      if (it >= (uint32_t)a.n_items) {
-        StageMeta m{};
-        m.item = -1;
-        m.flags = kFlagStop;
-        push_meta(m);                              // one per consumer group
-        push_meta(m);
-        break;
-      }
-      // claim the next item now so its descriptor load overlaps this item's issue loop
-      const uint32_t it_next = claim();
-      GatherItem item_next{};
-      if (it_next < (uint32_t)a.n_items) item_next = a.items[it_next];
-      if (item.x0 == item.x1) {
-        StageMeta m{};
-        m.item = (int)it;
-        m.j = item.j;
-        m.flags = kFlagLast | kFlagEmpty;
-        push_meta(m);                              // both groups run the item's epilogue
-        push_meta(m);
-      } else {
-        const uint32_t t0 = item.x0 / C::kTile, t1 = (item.x1 - 1) / C::kTile;
-        for (uint32_t tb0 = t0; tb0 <= t1; tb0 += 32) {
-          const uint32_t tl = tb0 + lane;
-          uint32_t fa = 0, fb = 0;                 // #flags before the tile's first / after its last ID
-          if (tl <= t1) {
-            const uint32_t tb = tl * C::kTile;
-            fa = (tl == t0) ? item.fx0 : __ldg(a.chunk_base + tb / kChunkIds);
-            fb = (tl == t1) ? item.fx1 : __ldg(a.chunk_base + (tb + C::kTile) / kChunkIds);
-          }
-          const uint32_t nb = min(32u, t1 - tb0 + 1);
-          const uint32_t pf = (uint32_t)a.pf_tiles;
-          // L2 prefetch of the batch's first pf tiles (the ring then loads them from L2)
-          if (pf && lane < nb && lane < pf) {
-            const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
-            bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
-            if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
-          }
-          for (uint32_t k = 0; k < nb; ++k) {
-            const uint32_t flo = __shfl_sync(0xffffffffu, fa, k);
-            const uint32_t fhi = __shfl_sync(0xffffffffu, fb, k);
-            // keep the L2 prefetch pf tiles ahead of the ring (within the batch)
-            if (pf && lane == k + pf && lane < nb) {
-              const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
-              bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
-              if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
-            }
-            if constexpr (PR) {
-              // the apply's vertex arrays of partition j into L2 a few tiles before the epilogue
-              if (a.epi_pf && lane == 0 && tb0 + k == (t1 > t0 + (uint32_t)a.epi_pf ? t1 - (uint32_t)a.epi_pf : t0)) {
-                const int64_t v0 = (int64_t)item.j << a.b;
-                const uint32_t vb = (uint32_t)(min(int64_t(1) << a.b, a.n_dst - v0) * 4) & ~15u;
-                if (vb) {
-                  bulk_prefetch_l2(a.inv_deg + v0, vb);
-                  bulk_prefetch_l2(a.pr_old + v0, vb);
-                  if (SL) bulk_prefetch_l2(a.slotmap + v0 / 32, vb / 16);   // q/32 uint2 = q/4 bytes
-                }
-              }
-            }
-            if (lane == 0) {
-              const uint32_t t = tb0 + k;
-              const uint32_t tb = t * C::kTile;
-              const uint32_t wlo = flo > 0 ? flo - 1 : 0;   // the first ID may continue the previous run
-              const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
-              mbar_wait(&empty[stage], phase ^ 1);
-              StageMeta m{};
-              m.item = (int)it;
-              m.j = item.j;
-              m.lo = max(tb, item.x0);
-              m.hi = min(tb + C::kTile, item.x1);
-              m.tile_base = tb;
-              m.win_base = alo;
-              // the item's final stage of EACH group is flagged Last: tiles t1 and t1 - 1
-              m.flags = (t + 1 >= t1 + (t1 > t0 ? 0u : 1u)) ? kFlagLast : 0u;
-              meta[stage] = m;
-              uint8_t* sb = stage_base + stage * C::kStageBytes;
-              const uint32_t win_bytes = (ahi - alo) * 4;
-              mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
-              bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
-              bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
-              bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
-                       &full[stage], pol);
-              if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
-            }
-            __syncwarp();
-            if (++stage == S) { stage = 0; phase ^= 1; }
-          }
-        }
-        if (t1 == t0) {                             // single tile: the other group still needs its Last
-          StageMeta m{};
-          m.item = (int)it;
-          m.j = item.j;
-          m.flags = kFlagLast | kFlagEmpty;
-          push_meta(m);
-        }
-      }
-      it = it_next;
-      item = item_next;
-    }
+    gather_producer<C, IdT, W, PR, SL>(a, ids, stage_base, meta, full, empty, lane);
     return;
   }
 
@@ -337,125 +495,9 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;
     const uint32_t v0 = m.j << a.b;
-    if (!(m.flags & kFlagEmpty)) {
-      const uint8_t* sb = stage_base + stage * C::kStageBytes;
-      const IdT* ids_s = reinterpret_cast<const IdT*>(sb);
-      const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
-      const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
-      const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
-      auto process = [&](const int sc) {
-      const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
-      if (!PCPM_GATHER_NOOP && xs < m.hi && xs + C::kSub > m.lo) {
-        const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
-        auto body = [&](auto WHOLE) {
-          constexpr bool kWhole = decltype(WHOLE)::value;
-          // lane-strided decode: step c covers the 32 consecutive IDs c*32 .. c*32+31
-          // of the sub-chunk, so the window reads of a step hit ~32/r consecutive
-          // words (one or two smem wavefronts)
-          // IDs are read sign-extended: the run flag (MSB) becomes the sign, one
-          // compare per ID for the ballot
-          using SIdT = typename std::conditional<sizeof(IdT) == 2, int16_t, int32_t>::type;
-          const SIdT* sids = reinterpret_cast<const SIdT*>(ids_s);
-          uint32_t id[P];
-#pragma unroll
-          for (int c = 0; c < P; ++c) id[c] = (uint32_t)(int32_t)sids[sc * C::kSub + c * 32 + lane];
-          // Alg. 5 update_ptr = #flags in ids[0..x] - 1 (R5), from the sub-chunk's
-          // anchor plus a warp prefix count of the MSB flags, step by step
-          uint32_t run = cb_s[(sc * C::kSub) / kChunkIds] - 1u - m.win_base;
-          float val[P];
-          bool ok[P];
-#pragma unroll
-          for (int c = 0; c < P; ++c) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, (int32_t)id[c] < 0);
-            const uint32_t ptr = run + __popc(bal & lemask);
-            run += __popc(bal);
-            const uint32_t x = xs + c * 32 + lane;
-            ok[c] = kWhole || (x >= m.lo && x < m.hi);
-            val[c] = ok[c] ? win_s[ptr] : 0.0f;
-          }
-          if constexpr (PR) {
-            // PageRank: the apply stores SPR * 2^F (a power-of-two scaling, exact in fp32),
-            // so one conversion rounds each term to the 2^-F grid
-            uint32_t tlo[P], thi[P], old[P];
-#pragma unroll
-            for (int c = 0; c < P; ++c) {
-              // SPR is stored as SPR * 2^F; weighted PageRank (R24) applies w(u,v) here
-              const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
-              const unsigned long long T = __float2ull_rn(tv);
-              tlo[c] = (uint32_t)T;
-              thi[c] = (uint32_t)(T >> 32);
-            }
-#pragma unroll
-            for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
-            // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
-            // ok = false have lo = hi = 0 (val = 0) and never carry
-            uint32_t any = 0;
-#pragma unroll
-            for (int c = 0; c < P; ++c) any |= thi[c] | (tlo[c] > ~old[c] ? 1u : 0u);
-            if (any) {                                   // rare: carry into the global high word
-#pragma unroll
-              for (int c = 0; c < P; ++c) {
-                const uint32_t hinc = thi[c] + (tlo[c] > ~old[c] ? 1u : 0u);
-                if (hinc) {
-                  const uint32_t li = id[c] & qmask;
-                  atomicAdd(&a.hi[v0 + li], hinc);
-                  atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
-                }
-              }
-            }
-          } else {
-            // SpMV: signed 64-bit fixed point in "balanced" form: the smem low
-            // word is read as a signed int32, so a running sum that hovers
-            // around zero never wraps; only signed overflow of the low word
-            // (|partial| >= 2^31 units) carries +-1 into the global high word.
-            // w*x is rounded once to fp32 (<= 2^-24 |w x|, R22); F keeps
-            // |w x| 2^F <= 2^30, so each term T is an int32 and the high part of the
-            // balanced form is zero: only the low word's signed overflow carries.
-            uint32_t tlo[P], old[P];
-            int32_t thi[P];
-#pragma unroll
-            for (int c = 0; c < P; ++c) {
-              const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
-              tlo[c] = (uint32_t)__float2int_rn(tv * sp_scale_f);
-              thi[c] = 0;
-            }
-#pragma unroll
-            for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
-            uint32_t any = 0;
-            int32_t hinc[P];
-#pragma unroll
-            for (int c = 0; c < P; ++c) {
-              const uint32_t nw = old[c] + tlo[c];
-              const bool ovf = (int32_t)((old[c] ^ nw) & (tlo[c] ^ nw)) < 0;
-              hinc[c] = ok[c] ? thi[c] + (ovf ? ((int32_t)old[c] < 0 ? -1 : 1) : 0) : 0;
-              any |= (uint32_t)hinc[c];
-            }
-            if (any) {
-#pragma unroll
-              for (int c = 0; c < P; ++c)
-                if (hinc[c]) {
-                  const uint32_t li = id[c] & qmask;
-                  atomicAdd(&a.hi[v0 + li], (uint32_t)hinc[c]);
-                  atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
-                }
-            }
-          }
-        };
-        if (whole) body(std::true_type{});
-        else body(std::false_type{});
-      }
-      };
-      // sub-chunks gw, gw + gsz, ... of the stage; the remaining kNsc mod gsz
-      // sub-chunks rotate over the group's warps from stage to stage
-      const int nmain = (C::kNsc / gsz) * gsz;
-      for (int sc = gw; sc < nmain; sc += gsz) process(sc);
-      int who = rot;
-      for (int sc = nmain; sc < C::kNsc; ++sc) {
-        if (gw == who) process(sc);
-        who = (who + 1 == gsz) ? 0 : who + 1;
-      }
-      rot = who;
-    }
+    if (!(m.flags & kFlagEmpty))
+      decode_stage<C, IdT, W, PR>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
+                                  lemask, lane, sp_scale_f, v0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     stage += 2;
@@ -516,7 +558,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
         }
         return tot;
       };
-      double dang = 0.0, res = 0.0;
+      unsigned long long dang = 0, res = 0;   // 2^-62 fixed point (red_fx)
       if (PCPM_GATHER_NO_EPI) run_apply = false;
       if constexpr (SL) {
         // accumulator slots: vertex v reads slot16[v] (bins are never split with slots);
@@ -553,8 +595,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
             a.pr_new[v] = (float)prn;
             const float idg = __ldg(a.inv_deg + v);
             a.spr_new[v] = (float)prn * idg * fscale;
-            if (idg == 0.0f) dang += prn;
-            res += fabs(prn - (double)a.pr_old[v]);
+            if (idg == 0.0f) dang += red_fx(prn);
+            res += red_fx(fabs(prn - (double)a.pr_old[v]));
           } else {
             a.y[v] = (float)((double)(long long)tot * sp_inv);
           }
@@ -574,8 +616,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
               const double prn = base_pr + a.d * ((double)(long long)slot_total(sl[c]) * inv_scale);
               pn[c] = (float)prn;
               sp[c] = pn[c] * idv[c] * fscale;
-              dang += idv[c] != 0.0f ? 0.0 : prn;
-              res += fabs(prn - (double)pov[c]);
+              dang += idv[c] != 0.0f ? 0ull : red_fx(prn);
+              res += red_fx(fabs(prn - (double)pov[c]));
             }
             *reinterpret_cast<float4*>(a.pr_new + v) = make_float4(pn[0], pn[1], pn[2], pn[3]);
             *reinterpret_cast<float4*>(a.spr_new + v) = make_float4(sp[0], sp[1], sp[2], sp[3]);
@@ -612,8 +654,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
                 const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
                 pn[c] = (float)prn;
                 sp[c] = pn[c] * idv[c] * fscale;        // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
-                dang += idv[c] != 0.0f ? 0.0 : prn;
-                res += fabs(prn - (double)pov[c]);
+                dang += idv[c] != 0.0f ? 0ull : red_fx(prn);
+                res += red_fx(fabs(prn - (double)pov[c]));
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
               sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
@@ -630,8 +672,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
               a.spr_new[v] = (float)prn * idg * fscale;
               if constexpr (MULTI)
                 for (int r = 0; r < a.n_peer; ++r) a.spr_peer[r][v] = (float)prn * idg * fscale;
-              if (idg == 0.0f) dang += prn;
-              res += fabs(prn - (double)a.pr_old[v]);
+              if (idg == 0.0f) dang += red_fx(prn);
+              res += red_fx(fabs(prn - (double)a.pr_old[v]));
             }
           }
         } else {
@@ -641,28 +683,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       }
       if (!SL)
         for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
-      if constexpr (PR) {
-        for (int o = 16; o; o >>= 1) {
-          dang += __shfl_xor_sync(0xffffffffu, dang, o);
-          res += __shfl_xor_sync(0xffffffffu, res, o);
-        }
-        if (lane == 0) {
-          red_s[cw] = dang;
-          red_s[C::kWarps + cw] = res;
-        }
-      }
+      if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane);
       named_bar_sync(1, kCons);
-      if constexpr (PR) {
-        if (ctid == 0) {
-          double sd = 0.0, sr = 0.0;
-          for (int k = 0; k < C::kWarps; ++k) {
-            sd += red_s[k];
-            sr += red_s[C::kWarps + k];
-          }
-          a.item_red[2 * m.item] = sd;       // zero for non-last slices
-          a.item_red[2 * m.item + 1] = sr;
-        }
-      }
       for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
       named_bar_sync(1, kCons);
       if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[3] += t - tc; tc = t; }
@@ -684,28 +706,405 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   named_bar_sync(1, kCons);
   if (*flag_s) {
     __threadfence();
-    if constexpr (PR) {
-      if (cw == 0 && !a.has_split) {            // with split bins k_apply_split reduces
-        // fixed order: lane-strided partial sums, then a fixed shuffle tree
-        double sd = 0.0, sr = 0.0;
-        for (int i = lane; i < a.n_items; i += 32) {
-          sd += __ldcg(&a.item_red[2 * i]);
-          sr += __ldcg(&a.item_red[2 * i + 1]);
-        }
-        for (int o = 16; o; o >>= 1) {
-          sd += __shfl_xor_sync(0xffffffffu, sd, o);
-          sr += __shfl_xor_sync(0xffffffffu, sr, o);
-        }
-        if (lane == 0) {
-          *a.dang_out = sd;    // D_{t+1}
-          *a.res_out = sr;     // residual of iteration t
-        }
-      }
-    }
+    if constexpr (PR)
+      if (ctid == 0 && !a.has_split) red_finish(a);   // with split bins k_apply_split finishes
     if (ctid == 0) {
       a.counters[0] = 0u;
       a.counters[1] = 0u;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_gather2 (default, option "gather_variant" = 2): the same decode, with the apply
+// of Eq. 1 taken off the decoders' critical path.  Warp roles (1024 threads):
+//   warp 0          producer (as in k_gather)
+//   warps 1 .. 27   decoders, two groups on alternate stages (14 + 13 warps)
+//   warps 28 .. 31  apply warps, one per TMEM lane quadrant (warp % 4)
+// When an item's decode ends, the decoders move its 128 KB accumulator from shared
+// memory into one of two tensor-memory buffers (256 columns each: local vertex
+// i = 128 c + l lives in lane l, column c), zero the shared copy and start the next
+// item at once; the apply warps run the apply (or, for a slice of a split bin, the
+// flush to its slot buffer) from TMEM while the next item is decoded.  Handoff
+// protocol: tfull[b] (decoders -> apply, 1 arrival) / tempty[b] (apply -> decoders,
+// 1 arrival) mbarriers per buffer, with tcgen05 fences around the thread syncs.
+// timing-only experiment builds: FORCE_INLINE = the decoders apply every item themselves
+// (apply warps idle); NOAPPLY = the apply warps skip the work (results are wrong)
+#ifndef PCPM_GATHER2_FORCE_INLINE
+#define PCPM_GATHER2_FORCE_INLINE 0
+#endif
+#ifndef PCPM_GATHER2_NOAPPLY
+#define PCPM_GATHER2_NOAPPLY 0
+#endif
+#ifndef PCPM_GATHER2_APPLY
+#define PCPM_GATHER2_APPLY 4                     // apply warps (4 or 8: one or two per TMEM lane quadrant)
+#endif
+template <typename IdT, bool W>
+struct Cfg2 : Cfg<IdT, W> {
+  static constexpr int kApply = PCPM_GATHER2_APPLY;
+  static constexpr int kDec = 31 - kApply;
+  static constexpr int kFirstApply = 1 + kDec;
+  static constexpr int kThreads = 32 * (1 + kDec + kApply);
+  static constexpr int kGroupA = (kDec + 1) / 2;
+  static constexpr int kGroupB = kDec - kGroupA;
+  static constexpr int kBufCols = 256;           // TMEM columns per accumulator buffer (q <= 2^15)
+  static constexpr int kBmWords = 32;            // carry bitmap words (1 bit per 32 vertices, q <= 2^15)
+  static_assert(kThreads == 1024 && kFirstApply % 4 == 0 && kApply % 4 == 0,
+                "apply warps cover the four lane quadrants in order");
+};
+
+struct HandoffRec {        // one TMEM buffer's item (written by decoder 0, read by the apply warps)
+  int item;
+  uint32_t j, nsl, slot, stop, pad[3];
+  uint32_t bm[32];         // carry bitmap of the item's accumulator
+};
+
+template <typename IdT, bool W, bool PR>
+int smem_bytes2(int b) {
+  using C = Cfg2<IdT, W>;
+  const int64_t q = int64_t(1) << b;
+  const int64_t head = ((q + 31) / 32) * 32 * 4 + C::kBmWords * 4;
+  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 4 * 8 +
+               2 * sizeof(HandoffRec) + 32);
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// The apply of one item's accumulator straight from shared memory by nthr threads
+// (thread t of them): Eq. 1 for a whole bin, or the flush of a split bin's slice to
+// its slot buffer; resets the accumulator and carry words it reads.
+template <bool PR, bool MULTI>
+__device__ __forceinline__ void apply_from_smem(const GatherArgs& a, uint32_t* acc, const uint32_t* bitmap,
+                                                uint32_t v0, uint32_t cnt, int64_t q, uint32_t nsl, uint32_t slot,
+                                                int t, int nthr, double base_pr, double inv_scale, float fscale,
+                                                double sp_inv, unsigned long long& dang, unsigned long long& res) {
+  if (nsl > 1) {
+    uint32_t* sbuf = a.slot_buf + (size_t)slot * (size_t)q;
+    for (int64_t i = t; i < q; i += nthr) {
+      __stcg(sbuf + i, acc[i]);
+      acc[i] = 0u;
+    }
+    return;
+  }
+  for (uint32_t i = t; i < cnt; i += nthr) {
+    const uint32_t v = v0 + i;
+    uint64_t tot = PR ? (uint64_t)acc[i] : (uint64_t)(long long)(int32_t)acc[i];
+    acc[i] = 0u;
+    if ((bitmap[i >> 10] >> ((i >> 5) & 31)) & 1u) {
+      tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+      a.hi[v] = 0u;
+    }
+    if constexpr (PR) {
+      const float idg = __ldg(a.inv_deg + v);
+      const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
+      const float pn = (float)prn;
+      const float sp = pn * idg * fscale;
+      a.pr_new[v] = pn;
+      a.spr_new[v] = sp;
+      if constexpr (MULTI)
+        for (int rr = 0; rr < a.n_peer; ++rr) a.spr_peer[rr][v] = sp;
+      if (idg == 0.0f) dang += red_fx(prn);
+      res += red_fx(fabs(prn - (double)__ldg(a.pr_old + v)));
+    } else {
+      a.y[v] = (float)((double)(long long)tot * sp_inv);
+    }
+  }
+  for (int64_t i = (int64_t)cnt + t; i < q; i += nthr) acc[i] = 0u;   // tail of a short last partition
+}
+
+template <typename IdT, bool W, bool PR, bool MULTI = false>
+__global__ void __launch_bounds__(1024, 1) k_gather2(const GatherArgs a) {
+  using C = Cfg2<IdT, W>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t q = int64_t(1) << a.b;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // q words (128 B rounded)
+  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;                           // 1 bit per 32 vertices
+  uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + C::kBmWords);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  HandoffRec* hrec = reinterpret_cast<HandoffRec*>(tempty + 2);
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(hrec + 2);
+  uint32_t* flag_s = tmem_base_s + 1;
+  uint32_t* inline_s = tmem_base_s + 2;
+  const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bm_words = (int)((q + 1023) / 1024);
+  const uint32_t ncol8 = (uint32_t)((q + 1023) / 1024);                   // 8-column groups per buffer
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&tfull[t], 1);
+      mbar_init(&tempty[t], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == C::kFirstApply) tmem_alloc(tmem_base_s, 2 * C::kBufCols);     // all 512 columns
+  for (int i = threadIdx.x; i < C::kBmWords; i += blockDim.x) bitmap[i] = 0u;
+  for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc[i] = 0u;
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = *tmem_base_s;
+
+  if (warp == 0) {
+    gather_producer<C, IdT, W, PR, false>(a, ids, stage_base, meta, full, empty, lane);
+    return;
+  }
+  const int qd = warp & 3;                          // TMEM lane quadrant this warp may access
+  constexpr int kWork = 32 * (C::kDec + C::kApply); // threads of bar 3 (decoders + apply warps)
+  const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F (PageRank)
+  const double inv_scale = 1.0 / (double)fscale;
+  double base_pr = 0.0, sp_inv = 1.0;
+  float sp_scale_f = 1.0f;
+  if constexpr (PR) {
+    base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+  } else {
+    const int F = spmv_fbits(*a.xmax, a.wexp);
+    sp_scale_f = ldexpf(1.0f, F);
+    sp_inv = ldexp(1.0, -F);
+  }
+  unsigned long long pt[4] = {0, 0, 0, 0};
+  long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
+  auto prof = [&](int k) {
+    if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[k] += t - tc; tc = t; }
+  };
+
+  if (warp < C::kFirstApply) {
+    // ================= decoders =================
+    const int cw = warp - 1;
+    const int grp = cw < C::kGroupA ? 0 : 1;
+    const int gw = grp ? cw - C::kGroupA : cw;
+    const int gsz = grp ? C::kGroupB : C::kGroupA;
+    constexpr int kDecT = 32 * C::kDec;
+    // decoders of quadrant qd: warps qd0, qd0 + 4, ... <= kDec (qd0 = qd, or 4 for qd = 0)
+    const int qd0 = qd == 0 ? 4 : qd;
+    const int qrank = (warp - qd0) / 4, qcount = (C::kDec - qd0) / 4 + 1;
+    const uint32_t qmask = (uint32_t)(q - 1);
+    const uint32_t lemask = lanemask_le();
+    int stage = grp, rot = 0, tb = 0;
+    uint32_t phase = 0, tph = 0;
+    // item end: move the accumulator into TMEM buffer tb for the apply warps, or --
+    // when they are still busy with both buffers -- apply it here (decision taken by
+    // decoder 0 before the barrier that ends the item, so every decoder sees it)
+    auto item_end = [&](const StageMeta& m, bool stop) {
+      if (cw == 0 && lane == 0)
+        *inline_s = (!stop && (PCPM_GATHER2_FORCE_INLINE || !mbar_test(&tempty[tb], tph ^ 1))) ? 1u : 0u;
+      named_bar_sync(1, kDecT);                      // all atomics of the item are done
+      prof(1);
+      if (*inline_s) {
+        const uint32_t v0 = m.j << a.b;
+        const uint32_t cnt = (uint32_t)min(q, a.n_dst - (int64_t)v0);
+        unsigned long long dg = 0, rs = 0;
+        apply_from_smem<PR, MULTI>(a, acc, bitmap, v0, cnt, q, a.bin_nslices[m.j], a.items[m.item].pad[0],
+                                   threadIdx.x - 32, kDecT, base_pr, inv_scale, fscale, sp_inv, dg, rs);
+        if constexpr (PR) warp_red_add(a.red_fx, dg, rs, lane);
+        named_bar_sync(1, kDecT);                    // accumulator read and zeroed
+        for (int i = threadIdx.x - 32; i < C::kBmWords; i += kDecT) bitmap[i] = 0u;
+        named_bar_sync(1, kDecT);
+        prof(3);
+        return;
+      }
+      mbar_wait(&tempty[tb], tph ^ 1);               // the apply warps released buffer tb
+      tmem_fence_after();
+      prof(2);
+      if (!stop) {
+        const uint32_t tb_addr = tbase + (uint32_t)(tb * C::kBufCols) + ((uint32_t)(32 * qd) << 16);
+        for (uint32_t cc = (uint32_t)qrank; cc < ncol8; cc += (uint32_t)qcount) {
+          uint32_t r[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t i = (cc * 8 + k) * 128 + 32 * qd + lane;
+            r[k] = i < (uint32_t)q ? acc[i] : 0u;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t i = (cc * 8 + k) * 128 + 32 * qd + lane;
+            if (i < (uint32_t)q) acc[i] = 0u;
+          }
+          tmem_st8(tb_addr + cc * 8, r);
+        }
+        tmem_wait_st();
+      }
+      if (cw == 0) {
+        HandoffRec& H = hrec[tb];
+        if (lane == 0) {
+          H.stop = stop ? 1u : 0u;
+          H.item = m.item;
+          H.j = m.j;
+          if (!stop) {
+            H.nsl = a.bin_nslices[m.j];
+            H.slot = a.items[m.item].pad[0];
+          }
+        }
+        for (int i = lane; i < C::kBmWords; i += 32) {
+          H.bm[i] = i < bm_words ? bitmap[i] : 0u;
+          bitmap[i] = 0u;
+        }
+      }
+      tmem_fence_before();
+      named_bar_sync(1, kDecT);                      // every decoder copied + zeroed its share
+      if (cw == 0 && lane == 0) mbar_arrive(&tfull[tb]);
+      tb ^= 1;
+      if (tb == 0) tph ^= 1;
+      prof(3);
+    };
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      prof(0);
+      const StageMeta m = meta[stage];
+      if (m.flags & kFlagStop) break;
+      const uint32_t v0 = m.j << a.b;
+      if (!(m.flags & kFlagEmpty))
+        decode_stage<C, IdT, W, PR>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
+                                    lemask, lane, sp_scale_f, v0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      stage += 2;
+      if (stage >= S) { stage -= S; phase ^= 1; }
+      prof(1);
+      if (m.flags & kFlagLast) item_end(m, false);
+    }
+    StageMeta ms{};
+    item_end(ms, true);                              // tell the apply warps to stop
+    if (PCPM_GATHER_PROFILE && lane == 0) {
+      for (int k = 0; k < 4; ++k) atomicAdd(&g_gather_prof[k], pt[k]);
+      atomicAdd(&g_gather_prof[4], 1ull);
+    }
+  } else {
+    // ================= apply warps =================
+    const int aw_id = warp - C::kFirstApply;         // quadrant qd = aw_id % 4
+    const uint32_t aq = (uint32_t)(aw_id >> 2);      // which of the quadrant's apply warps
+    constexpr uint32_t kPerQ = C::kApply / 4;
+    unsigned long long dang = 0, res = 0;            // 2^-62 fixed point, this warp's share of the launch
+    int tb = 0;
+    uint32_t tph = 0;
+    for (;;) {
+      mbar_wait(&tfull[tb], tph);
+      tmem_fence_after();
+      prof(0);
+      const HandoffRec& H = hrec[tb];
+      if (H.stop) break;
+      const uint32_t v0 = H.j << a.b;
+      const uint32_t cnt = PCPM_GATHER2_NOAPPLY ? 0u : (uint32_t)min(q, a.n_dst - (int64_t)v0);
+      const uint32_t nsl = H.nsl;
+      const uint32_t tb_addr = tbase + (uint32_t)(tb * C::kBufCols) + ((uint32_t)(32 * qd) << 16);
+      uint32_t* sbuf = a.slot_buf + (size_t)H.slot * (size_t)q;
+      // per column k: vertices v0 + 128 c + 32 qd + lane -- 32 consecutive vertices per
+      // warp instruction (coalesced 128-byte loads and stores); the next chunk's
+      // vertex-array loads are issued before this chunk's arithmetic
+      float nidg[8], npo[8];
+      auto load_in = [&](uint32_t cc) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t i = (cc * 8 + k) * 128 + 32 * qd + lane;
+          nidg[k] = i < cnt ? __ldg(a.inv_deg + v0 + i) : 0.0f;
+          npo[k] = i < cnt ? __ldg(a.pr_old + v0 + i) : 0.0f;
+        }
+      };
+      if (PR && nsl <= 1) load_in(aq);
+#pragma unroll 1
+      for (uint32_t cc = aq; cc < ncol8; cc += kPerQ) {
+        if (cc * 1024 + 32 * qd >= cnt) break;      // columns beyond the partition (short last one)
+        uint32_t r[8];
+        tmem_ld8(tb_addr + cc * 8, r);
+        if (nsl > 1) {
+          // a slice of a split bin: its low words to the slot buffer (k_apply_split applies)
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t i = (cc * 8 + k) * 128 + 32 * qd + lane;
+            if (i < (uint32_t)q) __stcg(sbuf + i, r[k]);
+          }
+          continue;
+        }
+        float idg[8], po[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          idg[k] = nidg[k];
+          po[k] = npo[k];
+        }
+        if (PR && cc + kPerQ < ncol8) load_in(cc + kPerQ);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t c = cc * 8 + k;
+          const uint32_t i = c * 128 + 32 * qd + lane;
+          if (i >= cnt) continue;
+          const uint32_t v = v0 + i;
+          const uint32_t g = c * 4 + qd;            // carry-bitmap group (32 vertices) of i
+          uint64_t tot = PR ? (uint64_t)r[k] : (uint64_t)(long long)(int32_t)r[k];
+          if ((H.bm[g >> 5] >> (g & 31)) & 1u) {
+            tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+            a.hi[v] = 0u;
+          }
+          if constexpr (PR) {
+            const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
+            const float pn = (float)prn;
+            const float sp = pn * idg[k] * fscale;    // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
+            a.pr_new[v] = pn;
+            a.spr_new[v] = sp;
+            if constexpr (MULTI)
+              for (int rr = 0; rr < a.n_peer; ++rr) a.spr_peer[rr][v] = sp;
+            if (idg[k] == 0.0f) dang += red_fx(prn);
+            res += red_fx(fabs(prn - (double)po[k]));
+          } else {
+            a.y[v] = (float)((double)(long long)tot * sp_inv);
+          }
+        }
+      }
+      tmem_fence_before();
+      named_bar_sync(2, 32 * C::kApply);             // all apply warps are done with buffer tb
+      if (aw_id == 0 && lane == 0) mbar_arrive(&tempty[tb]);
+      tb ^= 1;
+      if (tb == 0) tph ^= 1;
+      prof(1);
+    }
+    if (PCPM_GATHER_PROFILE && lane == 0) {
+      atomicAdd(&g_gather_prof[5], pt[0]);
+      atomicAdd(&g_gather_prof[6], pt[1]);
+      atomicAdd(&g_gather_prof[7], 1ull);
+    }
+    if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane);
+  }
+
+  if constexpr (MULTI) __threadfence_system();     // peer stores performed before the kernel completes
+  // ---------------- last CTA: totals, counter reset ----------------
+  named_bar_sync(3, kWork);
+  const int wt = threadIdx.x - 32;
+  if (wt == 0) {
+    __threadfence();
+    const uint32_t done = atomicAdd(&a.counters[1], 1u);
+    *flag_s = (done == gridDim.x - 1) ? 1u : 0u;
+  }
+  named_bar_sync(3, kWork);
+  if (*flag_s && wt == 0) {
+    __threadfence();
+    if constexpr (PR)
+      if (!a.has_split) red_finish(a);
+    a.counters[0] = 0u;
+    a.counters[1] = 0u;
+  }
+  if (warp == C::kFirstApply) {
+    tmem_fence_after();
+    tmem_dealloc(tbase, 2 * C::kBufCols);
   }
 }
 
@@ -716,10 +1115,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
 constexpr int kSplitThreads = 256, kSplitChunk = 1024;
 
 template <bool PR>
-__global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs a, const uint32_t* split_bins,
-                                                              int n_split_blocks, double* split_red) {
-  __shared__ double red_s[2 * (kSplitThreads / 32)];
-  __shared__ uint32_t last_s;
+__global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs a, const uint32_t* split_bins) {
   const int64_t q = int64_t(1) << a.b;
   const int chunks = (int)((q + kSplitChunk - 1) / kSplitChunk);
   const uint32_t j = split_bins[blockIdx.x / chunks];
@@ -737,7 +1133,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
   } else {
     sp_inv = ldexp(1.0, -spmv_fbits(*a.xmax, a.wexp));
   }
-  double dang = 0.0, res = 0.0;
+  unsigned long long dang = 0, res = 0;   // 2^-62 fixed point (red_fx)
   const int64_t c1 = min(cnt, c0 + kSplitChunk);
   bool vec = PR && (c1 & 3) == 0 && (q & 3) == 0 && aligned16(a.hi + v0) && aligned16(a.pr_new + v0) && aligned16(a.spr_new + v0) &&
              aligned16(a.inv_deg + v0) && aligned16(a.pr_old + v0) && aligned16(sb);
@@ -770,8 +1166,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
         const double prn = base_pr + a.d * ((double)(long long)tv[c] * inv_scale);
         pn[c] = (float)prn;
         sp[c] = pn[c] * idv[c] * fscale;
-        if (idv[c] == 0.0f) dang += prn;
-        res += fabs(prn - (double)pov[c]);
+        if (idv[c] == 0.0f) dang += red_fx(prn);
+        res += red_fx(fabs(prn - (double)pov[c]));
       }
       *reinterpret_cast<float4*>(a.pr_new + v) = make_float4(pn[0], pn[1], pn[2], pn[3]);
       *reinterpret_cast<float4*>(a.spr_new + v) = make_float4(sp[0], sp[1], sp[2], sp[3]);
@@ -793,53 +1189,20 @@ __global__ void __launch_bounds__(kSplitThreads) k_apply_split(const GatherArgs 
       const float idg = __ldg(a.inv_deg + v);
       a.spr_new[v] = (float)prn * idg * fscale;
       for (int r = 0; r < a.n_peer; ++r) a.spr_peer[r][v] = (float)prn * idg * fscale;   // fused exchange
-      if (idg == 0.0f) dang += prn;
-      res += fabs(prn - (double)a.pr_old[v]);
+      if (idg == 0.0f) dang += red_fx(prn);
+      res += red_fx(fabs(prn - (double)a.pr_old[v]));
     } else {
       a.y[v] = (float)((double)(long long)tot * sp_inv);
     }
   }
   if constexpr (PR) {
-    for (int o = 16; o; o >>= 1) {
-      dang += __shfl_xor_sync(0xffffffffu, dang, o);
-      res += __shfl_xor_sync(0xffffffffu, res, o);
-    }
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) {
-      red_s[w] = dang;
-      red_s[kSplitThreads / 32 + w] = res;
-    }
+    warp_red_add(a.red_fx, dang, res, threadIdx.x & 31);
     __syncthreads();
     if (threadIdx.x == 0) {
-      double sd = 0.0, sr = 0.0;
-      for (int k = 0; k < kSplitThreads / 32; ++k) {
-        sd += red_s[k];
-        sr += red_s[kSplitThreads / 32 + k];
-      }
-      split_red[2 * blockIdx.x] = sd;
-      split_red[2 * blockIdx.x + 1] = sr;
       __threadfence();
-      last_s = atomicAdd(&a.counters[6], 1u) == gridDim.x - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (last_s && w == 0) {
-      __threadfence();
-      double sd = 0.0, sr = 0.0;             // fixed order: gather items, then split blocks
-      for (int i = lane; i < a.n_items; i += 32) {
-        sd += __ldcg(&a.item_red[2 * i]);
-        sr += __ldcg(&a.item_red[2 * i + 1]);
-      }
-      for (int i = lane; i < n_split_blocks; i += 32) {
-        sd += __ldcg(&split_red[2 * i]);
-        sr += __ldcg(&split_red[2 * i + 1]);
-      }
-      for (int o = 16; o; o >>= 1) {
-        sd += __shfl_xor_sync(0xffffffffu, sd, o);
-        sr += __shfl_xor_sync(0xffffffffu, sr, o);
-      }
-      if (lane == 0) {
-        *a.dang_out = sd;
-        *a.res_out = sr;
+      if (atomicAdd(&a.counters[6], 1u) == gridDim.x - 1) {   // last block: all partials are in
+        __threadfence();
+        red_finish(a);
         a.counters[6] = 0u;
       }
     }
@@ -866,6 +1229,20 @@ GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false, 
                     : (pagerank ? k_gather<uint32_t, false, true> : k_gather<uint32_t, false, false>);
   return weighted ? (pagerank ? k_gather<uint16_t, true, true> : k_gather<uint16_t, true, false>)
                   : (pagerank ? k_gather<uint16_t, false, true> : k_gather<uint16_t, false, false>);
+}
+
+GatherFn gather2_fn(bool wide, bool weighted, bool pagerank, bool multi) {
+  if (multi) return wide ? k_gather2<uint32_t, false, true, true> : k_gather2<uint16_t, false, true, true>;
+  if (wide)
+    return weighted ? (pagerank ? k_gather2<uint32_t, true, true> : k_gather2<uint32_t, true, false>)
+                    : (pagerank ? k_gather2<uint32_t, false, true> : k_gather2<uint32_t, false, false>);
+  return weighted ? (pagerank ? k_gather2<uint16_t, true, true> : k_gather2<uint16_t, true, false>)
+                  : (pagerank ? k_gather2<uint16_t, false, true> : k_gather2<uint16_t, false, false>);
+}
+
+int gather2_smem_bytes(int b, bool wide, bool weighted) {
+  if (wide) return weighted ? smem_bytes2<uint32_t, true, true>(b) : smem_bytes2<uint32_t, false, true>(b);
+  return weighted ? smem_bytes2<uint16_t, true, true>(b) : smem_bytes2<uint16_t, false, true>(b);
 }
 
 }  // namespace
@@ -902,6 +1279,17 @@ int prepare_gather(pcpm_handle* h) {
   for (int p = 0; p < 2; ++p)
     PCPM_CK(cudaFuncSetAttribute(gather_fn(false, false, p, false, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  maxsm));
+  for (int wd = 0; wd < 2; ++wd)
+    for (int w = 0; w < 2; ++w) {
+      if (gather2_smem_bytes(h->b, wd, w) > maxsm) {
+        set_error(PCPM_ECUDA, "gather (v2) shared-memory plan exceeds the device limit for this partition size");
+        return PCPM_ECUDA;
+      }
+      for (int p = 0; p < 2; ++p)
+        PCPM_CK(cudaFuncSetAttribute(gather2_fn(wd, w, p, false), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    }
+  for (int wd = 0; wd < 2; ++wd)
+    PCPM_CK(cudaFuncSetAttribute(gather2_fn(wd, false, true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   return PCPM_OK;
 }
 
@@ -935,9 +1323,9 @@ int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaS
   const int chunks = (int)((h->q + kSplitChunk - 1) / kSplitChunk);
   const int blocks = h->n_split_bins * chunks;
   if (pagerank)
-    k_apply_split<true><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins, blocks, h->split_red);
+    k_apply_split<true><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins);
   else
-    k_apply_split<false><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins, blocks, h->split_red);
+    k_apply_split<false><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins);
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
   return PCPM_OK;
@@ -945,6 +1333,14 @@ int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaS
 
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi) {
   const bool slots = a.slot16 != nullptr && !weighted && !multi;
+  if (!slots && h->opt_gather_variant == 2) {
+    const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
+    gather2_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted)<<<grid, 1024,
+                                                                           gather2_smem_bytes(a.b, h->wide, weighted), s>>>(a);
+    PCPM_CK(cudaGetLastError());
+    h->launches += 1;
+    return launch_apply_split(h, a, pagerank, s);
+  }
   const int smem = slots ? smem_bytes_for<uint16_t, false, true>(a.b, a.acc_words) : gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
   gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted, slots)<<<grid, gather_threads(h->wide, weighted),

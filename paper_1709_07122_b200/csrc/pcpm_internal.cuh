@@ -123,16 +123,16 @@ struct pcpm_handle {
   uint32_t* bin_arrive = nullptr;   // [k_dst] slice arrival counters (kept zero)
   uint32_t* split_bins = nullptr;   // [n_split_bins] bins cut into slices (applied by k_apply_split)
   int n_split_bins = 0;
-  double* split_red = nullptr;      // [2 * blocks of k_apply_split] dangling / residual partials
   uint32_t* hi = nullptr;           // [n_dst] fixed-point carry words (kept zero)
   uint32_t* counters = nullptr;     // [4] work counter, done counter (kept zero)
-  double* item_red = nullptr;       // [2*n_gitems] per-item (dangling, residual) partials
+  unsigned long long* red_fx = nullptr;  // [2] fixed-point dangling mass / residual accumulators (kept zero)
   double* red = nullptr;            // [2*(red_cap)] D_t, res_t
   int red_cap = 0;
   int last_iters = 0;
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
+  int opt_gather_variant = 1;       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
   int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
   int opt_epi_pf = 4;               // gather: L2 prefetch of the apply's vertex arrays, tiles before the item's end (0 = off)
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
@@ -231,6 +231,44 @@ __device__ __forceinline__ uint32_t lanemask_le() {
   return r;
 }
 
+// ---------------------------------------------------------------- tensor memory (tcgen05)
+// The gather parks a finished partition's accumulator in TMEM (256 KB per SM,
+// 128 lanes x 512 columns of 32 bits) so dedicated apply warps can run Eq. 1 on it
+// while the decoders accumulate the next partition in shared memory.  A TMEM
+// address is (lane << 16) | column; warp w may access lanes 32 (w % 4) .. + 31.
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {   // one whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {    // the allocating warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// 32 lanes x 8 consecutive columns: thread l writes / reads lane (taddr.lane + l), columns c .. c+7
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Fixed-point reductions of the apply (dangling mass, L1 residual): every term is
+// rounded once to 2^-62 and summed in u64 (exact, order-free), so the result does
+// not depend on which warp or kernel variant applied which vertex.  Terms and sums
+// are <= 2 (PR' <= 1), i.e. < 2^63.
+constexpr double kRedScale = 4611686018427387904.0;     // 2^62
+__device__ __forceinline__ unsigned long long red_fx(double x) { return __double2ull_rn(x * kRedScale); }
+
 // ---------------------------------------------------------------- launchers
 struct GatherArgs {
   const void* ids;         // uint16_t* (compact) or uint32_t* (wide)
@@ -249,7 +287,7 @@ struct GatherArgs {
   int has_split;           // split bins exist: k_apply_split applies them and writes the reductions
   uint32_t* bin_arrive;    // [k_dst] slices arrived per split bin (reset by the last)
   uint32_t* hi;
-  double* item_red;        // [2*n_items]
+  unsigned long long* red_fx;   // [2] dangling mass / residual of this launch, 2^-62 fixed point (kept zero)
   int b;
   int64_t n_dst;
   int fbits;

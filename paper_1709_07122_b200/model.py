@@ -1,9 +1,12 @@
 """The paper's analytical traffic models (§4), for reporting.
 
-These are closed-form byte counts, not part of the hot path.  bench.py prints
-them next to the measured bytes (BASELINE.json north_star: "Bytes actually
+These are closed-form byte / access counts, not part of the hot path.  bench.py
+prints them next to the measured bytes (BASELINE.json north_star: "Bytes actually
 moved per iteration are reported next to the paper's communication model, for
-both the compressed and the uncompressed bin layout").
+both the compressed and the uncompressed bin layout"): Eq. 5 for the PCPM
+layouts, Eq. 4 for BVGAS, Eq. 3 for the pull kernel with c_mr measured from its
+L2 misses, and the §4.1 random-access counts.  Pinned to the paper's own numbers
+(kron: Eq. 5 ~ 8.7 GB, §4.1's 66.9 M / 0.26 M) in tests/test_model.py.
 """
 from __future__ import annotations
 
@@ -43,18 +46,3 @@ def random_accesses(engine: str, m: float = 0, k: float = 0, c_mr: float = 1, l:
     if engine == "pcpm":
         return k * k
     raise ValueError(engine)
-
-
-def pcpm_iteration_bytes(n: int, m: int, e_prime: int, k_src: int, k_dst: int,
-                         weighted: bool = False) -> int:
-    """Algorithmic bytes of one PCPM iteration as this build streams it.
-
-    ids 4m (+ weights 4m), PNG sources 4E' read, updates 4E' written + 4E' read,
-    the source vector 4n read, the new vector 4n written, offsets 4 k_src k_dst.
-    This is Eq. 5 with d_i = d_v = 4 (the k^2 d_i term counts one offsets
-    matrix).  Compressed-layout form; the uncompressed form has E' = m.
-    """
-    b = 4 * m + 12 * e_prime + 8 * n + 4 * k_src * k_dst
-    if weighted:
-        b += 4 * m
-    return b

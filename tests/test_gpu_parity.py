@@ -401,15 +401,19 @@ CHUNK_CASES = [
 
 
 @pytest.mark.parametrize("name,mk,b,host,flags", CHUNK_CASES, ids=[c[0] for c in CHUNK_CASES])
-@pytest.mark.parametrize("chunk_edges", ["1", "777", "legacy"])
-def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, chunk_edges):
-    """The chunked build (chunks of whole source partitions, copied in and sorted
-    one by one) gives the oracle's layout for any chunk size, host or device
-    inputs, weights, wide IDs and uncompressed bins; so does the legacy path."""
-    if chunk_edges == "legacy":
+@pytest.mark.parametrize("mode", ["count", "count_seg1", "count_seg200", "sort_1", "sort_777", "legacy"])
+def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, mode):
+    """Every construction gives the oracle's layout, for host or device inputs, weights,
+    wide IDs and uncompressed bins: the counting build (default; segments of one
+    32-row batch with PCPM_BUILD_SEG_EDGES=1, ~200 edges, or the default plan), the
+    chunked sort for any chunk size (PCPM_BUILD=sort), and the legacy path."""
+    if mode == "legacy":
         monkeypatch.setenv("PCPM_BUILD_LEGACY", "1")
-    else:
-        monkeypatch.setenv("PCPM_BUILD_CHUNK_EDGES", chunk_edges)
+    elif mode.startswith("sort_"):
+        monkeypatch.setenv("PCPM_BUILD", "sort")
+        monkeypatch.setenv("PCPM_BUILD_CHUNK_EDGES", mode[5:])
+    elif mode.startswith("count_seg"):
+        monkeypatch.setenv("PCPM_BUILD_SEG_EDGES", mode[9:])
     g = mk()
     h = build(pcpm, g, b, device=not host, flags=flags)
     try:

@@ -30,6 +30,12 @@ pcpm.pcpm_pagerank(h, 0.85, cfg["iters"], out)
 torch.cuda.synchronize()
 c = pcpm.pcpm_get_debug_counters(reset=True)
 tot = float(sum(c[:4]))
-names = ["wait for stage", "decode", "epilogue barrier", "epilogue"]
-print(key, "warps", int(c[4]), " ".join(f"{n}={c[i] / tot:.3f}" for i, n in enumerate(names)))
+v2 = c[7] > 0                      # k_gather2: decoders [0..3], apply warps [5], [6], counts [4], [7]
+names = (["wait for stage", "decode", "wait for a TMEM buffer", "handoff / in-line apply"] if v2 else
+         ["wait for stage", "decode", "epilogue barrier", "epilogue"])
+print(key, "decoder warps", int(c[4]), " ".join(f"{n}={c[i] / tot:.3f}" for i, n in enumerate(names)))
+if v2:
+    ta = float(c[5] + c[6])
+    print(key, "apply warps", int(c[7]), f"idle={c[5] / ta:.3f} busy={c[6] / ta:.3f}",
+          f"(decoder cycles per warp {tot / max(c[4], 1):.3e}, apply {ta / max(c[7], 1):.3e})")
 pcpm.pcpm_destroy(h)
