@@ -23,7 +23,7 @@
  *  - Limits: n_src, n_dst < 2^31 (the MSB of a 4-byte ID is the run flag,
  *    P:172-173); nnz < 2^32 (u32 bin positions); partition_bits in [1, 15]
  *    (one destination partition's accumulator, 2^b x 4 B, lives in one CTA's
- *    shared memory); k_src * k_dst <= 2^26 (the O(k^2) offset matrices of
+ *    shared memory); k_src * k_dst <= 2^28 (the O(k^2) offset matrices of
  *    P:148 / P:246).
  */
 #ifndef PCPM_H
@@ -37,7 +37,7 @@ extern "C" {
 
 #define PCPM_OK 0
 #define PCPM_EINVAL -1   /* NULL pointer, partition_bits out of range, d not in (0,1), iters < 0 ... */
-#define PCPM_ETOOBIG -2  /* n >= 2^31, nnz >= 2^32, k_src*k_dst > 2^26 */
+#define PCPM_ETOOBIG -2  /* n >= 2^31, nnz >= 2^32, k_src*k_dst > 2^28 */
 #define PCPM_EBADCSR -3  /* row_ptr not monotone / row_ptr[0] != 0 / row_ptr[n] != nnz, col >= n_dst,
                             or a row whose columns are not strictly increasing (R6) */
 #define PCPM_ENOMEM -4   /* device allocation failed */
@@ -211,6 +211,28 @@ int pcpm_ipc_open(const void* handle, void** dev_ptr_out);
 int pcpm_ipc_close(void* dev_ptr);
 
 void pcpm_destroy(pcpm_handle* h);
+
+/* ---- Job runtime: whole PageRank jobs from HOST memory, pipelined (csrc/jobs.cu).
+ * A job is: H2D copy of a square CSR -> pcpm_build_ex(csr, partition_bits, flags) ->
+ * pcpm_pagerank(d, iters) -> n floats of PR_iters written to `out` (host or device).
+ * One worker thread runs the jobs in submission order on the runtime's compute stream;
+ * job k+1's CSR is uploaded on a copy stream while job k builds and iterates, and job
+ * k's result is copied out on a third stream, so consecutive jobs overlap their PCIe
+ * transfers with GPU work (one layout resident at a time).  Host arrays should be pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to run asynchronously; they are
+ * borrowed until pcpm_job_wait returns for the job.  With values and PCPM_KEEP_VALUES
+ * the job runs weighted PageRank (R24).
+ * pcpm_runtime_create: NULL on error.  pcpm_job_submit: returns at once (0 or
+ * PCPM_EINVAL / PCPM_ECUDA), *job_id identifies the job.  pcpm_job_wait: blocks until
+ * the job's result is in `out`; returns the job's status (build / iteration errors
+ * included) and forgets the id.  pcpm_runtime_destroy: finishes the queued jobs and
+ * releases the runtime (jobs not waited for are discarded). */
+typedef struct pcpm_runtime pcpm_runtime;
+pcpm_runtime* pcpm_runtime_create(void);
+int pcpm_job_submit(pcpm_runtime* rt, const pcpm_csr* csr, int partition_bits, unsigned flags, double d, int iters,
+                    float* out, int64_t* job_id);
+int pcpm_job_wait(pcpm_runtime* rt, int64_t job_id);
+void pcpm_runtime_destroy(pcpm_runtime* rt);
 
 /* Support: stream, errors, introspection. */
 /* Memory: handles take their device memory from the current device's stream-ordered

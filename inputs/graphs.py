@@ -216,6 +216,14 @@ CONFIGS = {
                   probs=(0.57, 0.19, 0.19), permute=True, bfs=True, bits=15, iters=20, op="pagerank"),
     "c5": dict(name="c5_spmv_rmat25", kind="rmat", scale=25, edge_factor=16, seed=5,
                probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=50, op="spmv"),
+    # SURVEY §8(f)#4 benchmark lines (not BASELINE configs): weighted PageRank (P:287-288,
+    # reading R24) on C4's graph with weights |U[-1,1)| keyed by the raw edge (R18), and a
+    # non-square SpMV: C5's matrix restricted to its first half of the columns
+    # (y = M^T x with M 2^25 x 2^24, "rows and columns partitioned separately")
+    "c4w": dict(name="c4w_rmat26_weighted", kind="rmat", scale=26, edge_factor=16, seed=4,
+                probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=20, op="pagerank", weights="abs"),
+    "c5ns": dict(name="c5ns_spmv_rmat25_2to1", kind="rmat", scale=25, edge_factor=16, seed=5,
+                 probs=(0.57, 0.19, 0.19), permute=True, bits=15, iters=50, op="spmv", cols_div=2),
 }
 
 
@@ -252,6 +260,20 @@ def make_graph(kind: str, seed: int, *, scale: int = 0, edge_factor: int = 16, n
     del ukeys
     meta = dict(m_raw=m_raw_, kind=kind, seed=seed, permute=permute, transpose=transpose)
     return GraphCSR(name or f"{kind}", nn, nn, row_ptr, col, vals, meta)
+
+
+def column_prefix(g: GraphCSR, n_cols: int) -> GraphCSR:
+    """The sub-matrix of g's columns [0, n_cols) (a non-square CSR, rows kept)."""
+    keep = g.col < n_cols if g.backend == "np" else g.col.view(-1) < n_cols
+    if g.backend == "np":
+        cm = np.concatenate([np.zeros(1, np.int64), np.cumsum(keep, dtype=np.int64)])
+    else:
+        import torch
+        cm = torch.cat([torch.zeros(1, dtype=torch.int64, device=g.col.device),
+                        torch.cumsum(keep.to(torch.int64), 0)])
+    rp = cm[g.row_ptr]
+    vals = None if g.values is None else g.values[keep]
+    return GraphCSR(g.name, g.n_src, n_cols, rp, g.col[keep], vals, dict(g.meta))
 
 
 def make_x(n: int, seed: int, backend: str = "np", device=None):
@@ -319,8 +341,13 @@ def make_config(key: str, backend: str = "np", device=None) -> GraphCSR:
     cfg = CONFIGS[key]
     if cfg["kind"] == "rmat":
         g = make_graph("rmat", cfg["seed"], scale=cfg["scale"], edge_factor=cfg["edge_factor"],
-                       probs=cfg["probs"], permute=cfg["permute"], values=cfg["op"] == "spmv",
+                       probs=cfg["probs"], permute=cfg["permute"],
+                       values=cfg["op"] == "spmv" or "weights" in cfg,
                        transpose=cfg["op"] == "spmv", backend=backend, device=device, name=cfg["name"])
+        if cfg.get("weights") == "abs":              # non-negative edge weights (R24)
+            g.values = abs(g.values)
+        if cfg.get("cols_div"):
+            g = column_prefix(g, g.n_dst // cfg["cols_div"])
     else:
         g = make_graph("er", cfg["seed"], n=cfg["n"], m_raw=cfg["m_raw"], permute=cfg["permute"],
                        backend=backend, device=device, name=cfg["name"])

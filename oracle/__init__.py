@@ -43,6 +43,7 @@ def _load():
         lib.oracle_num_threads.restype = ctypes.c_int
         lib.oracle_transpose.argtypes = [I64, P, P, P, P]
         lib.oracle_pagerank_pull.argtypes = [I64, P, P, P, ctypes.c_double, ctypes.c_int, P]
+        lib.oracle_pagerank_pull_step.argtypes = [I64, P, P, P, ctypes.c_double, P, P]
         lib.oracle_pagerank.argtypes = [I64, P, P, ctypes.c_double, ctypes.c_int, P]
         lib.oracle_pagerank_weighted.argtypes = [I64, P, P, P, ctypes.c_double, ctypes.c_int, P]
         lib.oracle_spmv_t.argtypes = [I64, I64, P, P, P, P, P]
@@ -50,7 +51,7 @@ def _load():
         lib.oracle_layout.argtypes = [I64, I64, P, P, P, ctypes.c_int, P, P, P, P, P, P, P]
         lib.oracle_scatter.argtypes = [I64, I64, P, P, P, P, P]
         lib.oracle_gather.argtypes = [I64, I64, P, P, P, P, P, P]
-        for f in ("oracle_transpose", "oracle_pagerank_pull", "oracle_pagerank", "oracle_pagerank_weighted",
+        for f in ("oracle_transpose", "oracle_pagerank_pull", "oracle_pagerank_pull_step", "oracle_pagerank", "oracle_pagerank_weighted",
                   "oracle_spmv_t",
                   "oracle_layout_sizes", "oracle_layout", "oracle_scatter", "oracle_gather"):
             getattr(lib, f).restype = ctypes.c_int
@@ -98,6 +99,28 @@ def pagerank_pull(n, row_ptr, in_ptr, in_src, d=0.85, iters=20):
     if rc:
         raise ValueError(f"oracle_pagerank_pull failed ({rc})")
     return pr
+
+
+class PullState:
+    """Caller-owned state for stepping the pull oracle one Eq. 1 update at a time
+    (oracle_pagerank_pull_step): PR_t and 3n doubles of scratch, allocated once."""
+
+    def __init__(self, n, row_ptr, in_ptr, in_src):
+        self.n = n
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self.in_ptr = np.ascontiguousarray(in_ptr, dtype=np.int64)
+        self.in_src = np.ascontiguousarray(in_src, dtype=np.uint32)
+        if self.in_src.size == 0:
+            self.in_src = np.zeros(1, dtype=np.uint32)
+        self.pr = np.full(n, 1.0 / n, dtype=np.float64)             # PR_0 (R2)
+        self.work = np.zeros(3 * n, dtype=np.float64)
+
+    def step(self, d=0.85):
+        rc = _load().oracle_pagerank_pull_step(self.n, _p(self.row_ptr), _p(self.in_ptr), _p(self.in_src), float(d),
+                                                _p(self.pr), _p(self.work))
+        if rc:
+            raise ValueError(f"oracle_pagerank_pull_step failed ({rc})")
+        return self.pr
 
 
 def pagerank(n, row_ptr, col, d=0.85, iters=20):

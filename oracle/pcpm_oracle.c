@@ -106,33 +106,44 @@ int oracle_transpose(int64_t n, const int64_t* row_ptr, const uint32_t* col,
  * Arguments: in-adjacency from oracle_transpose, out-degree from the CSR.
  * Output pr int64[n] doubles.  Returns 0, or <0 on bad input.
  * ------------------------------------------------------------------------- */
+/* One Eq. 1 update in pull form, PR_t -> PR_{t+1} in place (pr), with caller-owned
+ * scratch work[3n] (no allocation: the bench's reference arm times exactly one
+ * iteration per step with the buffers allocated outside the timed region). */
+int oracle_pagerank_pull_step(int64_t n, const int64_t* row_ptr, const int64_t* in_ptr,
+                              const uint32_t* in_src, double d, double* pr, double* work) {
+  if (n <= 0 || !(d > 0.0 && d < 1.0) || !work) return -1;
+  double* spr = work;
+  double* dang = work + n;
+  double* next = work + 2 * n;
+  /* SPR(u) = PR(u)/|N_o(u)| (Table 1); dangling mass D_t (R1). */
+  for (int64_t u = 0; u < n; ++u) {
+    int64_t deg = row_ptr[u + 1] - row_ptr[u];
+    spr[u] = deg > 0 ? pr[u] / (double)deg : 0.0;
+    dang[u] = deg > 0 ? 0.0 : pr[u];
+  }
+  double D = oracle_sum(dang, n);
+  /* Eq. 1: new value = (1-d)/|V| + d * sum over in-neighbours (+ R1 term). */
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < n; ++v) {
+    double temp = 0.0;
+    for (int64_t e = in_ptr[v]; e < in_ptr[v + 1]; ++e) temp += spr[in_src[e]];
+    next[v] = (1.0 - d) / (double)n + d * (temp + D / (double)n);
+  }
+  memcpy(pr, next, sizeof(double) * (size_t)n);
+  return 0;
+}
+
 int oracle_pagerank_pull(int64_t n, const int64_t* row_ptr, const int64_t* in_ptr,
                          const uint32_t* in_src, double d, int iters, double* pr) {
   if (n <= 0 || iters < 0 || !(d > 0.0 && d < 1.0)) return -1;
-  double* spr = (double*)malloc(sizeof(double) * (size_t)n);
-  double* dang = (double*)malloc(sizeof(double) * (size_t)n);
-  double* next = (double*)malloc(sizeof(double) * (size_t)n);
-  if (!spr || !dang || !next) { free(spr); free(dang); free(next); return -2; }
+  double* work = (double*)malloc(sizeof(double) * 3 * (size_t)n);
+  if (!work) return -2;
   for (int64_t v = 0; v < n; ++v) pr[v] = 1.0 / (double)n;           /* R2 */
-  for (int it = 0; it < iters; ++it) {
-    /* SPR(u) = PR(u)/|N_o(u)| (Table 1); dangling mass D_t (R1). */
-    for (int64_t u = 0; u < n; ++u) {
-      int64_t deg = row_ptr[u + 1] - row_ptr[u];
-      spr[u] = deg > 0 ? pr[u] / (double)deg : 0.0;
-      dang[u] = deg > 0 ? 0.0 : pr[u];
-    }
-    double D = oracle_sum(dang, n);
-    /* Eq. 1: new value = (1-d)/|V| + d * sum over in-neighbours (+ R1 term). */
-#pragma omp parallel for schedule(dynamic, 4096)
-    for (int64_t v = 0; v < n; ++v) {
-      double temp = 0.0;
-      for (int64_t e = in_ptr[v]; e < in_ptr[v + 1]; ++e) temp += spr[in_src[e]];
-      next[v] = (1.0 - d) / (double)n + d * (temp + D / (double)n);
-    }
-    memcpy(pr, next, sizeof(double) * (size_t)n);
-  }
-  free(spr); free(dang); free(next);
-  return 0;
+  int rc = 0;
+  for (int it = 0; it < iters && rc == 0; ++it)
+    rc = oracle_pagerank_pull_step(n, row_ptr, in_ptr, in_src, d, pr, work);
+  free(work);
+  return rc;
 }
 
 /* ---------------------------------------------------------------------------

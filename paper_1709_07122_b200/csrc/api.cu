@@ -347,8 +347,8 @@ static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsign
   }
   const int64_t q = int64_t(1) << partition_bits;
   const int64_t ks = (csr->n_src + q - 1) / q, kd = (csr->n_dst + q - 1) / q;
-  if (ks * kd > (int64_t(1) << 26)) {
-    set_error(PCPM_ETOOBIG, "k_src * k_dst > 2^26: the O(k^2) offset matrices (P:148) are too large");
+  if (ks * kd > (int64_t(1) << 28)) {
+    set_error(PCPM_ETOOBIG, "k_src * k_dst > 2^28: the O(k^2) offset matrices (P:148) are too large");
     return nullptr;
   }
   int ndev = 0;
@@ -835,6 +835,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
       return PCPM_EINVAL;
     }
     h->opt_gather_variant = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "cluster_gather")) {
+    h->opt_cluster_gather = value ? 1 : 0;
     free_graph(h);
     return PCPM_OK;
   }

@@ -768,6 +768,31 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   }
   std::stable_sort(gi.begin(), gi.end(),
                    [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
+  // cluster gather for few partitions: cs CTAs per bin (one tile-aligned slice each), cs = 2..8
+  h->cl_cs = 0;
+  if (k_dst >= 1 && 2 * k_dst <= h->num_sms && !getenv("PCPM_NO_CLUSTER_GATHER")) {
+    int cs = 1;
+    while (cs * 2 <= 8 && (int64_t)cs * 2 * k_dst <= h->num_sms) cs *= 2;
+    std::vector<GatherItem> gc;
+    for (int64_t j = 0; j < k_dst; ++j) {
+      const int64_t s0 = hbin[j], s1 = hbin[j + 1], per = ((s1 - s0 + cs - 1) / cs + kTileAlign - 1) / kTileAlign * kTileAlign;
+      for (int r = 0; r < cs; ++r) {
+        GatherItem it{};
+        it.j = (uint32_t)j;
+        int64_t a0 = r == 0 ? s0 : std::min(s1, ((s0 + r * per) / kTileAlign) * kTileAlign);
+        int64_t a1 = r == cs - 1 ? s1 : std::min(s1, ((s0 + (r + 1) * per) / kTileAlign) * kTileAlign);
+        a0 = std::max(a0, s0);
+        a1 = std::max(a1, a0);
+        it.x0 = (uint32_t)a0;
+        it.x1 = (uint32_t)a1;
+        it.pad[0] = 0xFFFFFFFFu;
+        gc.push_back(it);
+      }
+    }
+    if ((rc = dev_alloc_t(h, &h->gitems_cl, gc.size()))) return rc;
+    TK(cudaMemcpyAsync(h->gitems_cl, gc.data(), sizeof(GatherItem) * gc.size(), cudaMemcpyHostToDevice, s));
+    h->cl_cs = cs;
+  }
   h->n_gitems = (int)gi.size();
   if ((rc = dev_alloc_t(h, &h->gitems, gi.size()))) return rc;
   if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
@@ -788,6 +813,11 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
   TK(cudaGetLastError());
+  if (h->cl_cs) {
+    const int nc = (int)(k_dst * h->cl_cs);
+    k_item_f<<<grid_for(nc), kT, 0, s>>>(nc, h->gitems_cl, h->chunk_base, h->bin_upd_start);
+    TK(cudaGetLastError());
+  }
 
   // ---- iteration scratch (kept zero between uses by the kernels)
   const int64_t nv = std::max(n_src, n_dst);
@@ -1409,7 +1439,7 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 //     each bin lists its IDs in (u, v) order and each PNG group its sources in u
 //     order -- exactly the oracle's layout, deterministic, no atomics on the output.
 // The running bases live in shared memory, one k_dst-entry array pair per warp.
-constexpr int kCntWarps = 8;              // warps (segments in flight) per CTA
+constexpr int kCntWarps = 12;             // warps (segments in flight) per CTA
 constexpr int64_t kCountMaxK = 2048;      // counters: 2 x k_dst u32 per warp (16 KB at k = 2048)
 
 struct BSeg {
@@ -1431,9 +1461,12 @@ __global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* ci = csm + (size_t)warp * 2 * k_dst;    // IDs (count) / running ID slot (place) per bin j
   uint32_t* cr = ci + k_dst;                         // runs (count) / running PNG slot (place) per bin j
+  uint8_t* rowlist = reinterpret_cast<uint8_t*>(csm + (size_t)kCntWarps * 2 * k_dst) + warp * 32;
   const uint32_t qmask = (1u << b) - 1u;
-  uint32_t lt;
+  uint32_t lt, le;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(le));
+  constexpr int D = 4;                               // 32-edge steps whose column loads are in flight
   uint32_t errs = 0;
   for (;;) {
     uint32_t sidx = 0;
@@ -1452,11 +1485,21 @@ __global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
     }
     __syncwarp();
     uint32_t dang = 0;
+    // row bounds of the first 32-row batch; each batch prefetches the next one's
+    auto load_rows = [&](uint32_t ub, int64_t& rs, int64_t& re) {
+      const uint32_t u = ub + lane;
+      const bool ur = u < sg.u1;
+      rs = ub < sg.u1 ? row_ptr[ur ? u : sg.u1] : 0;
+      re = ub < sg.u1 ? (ur ? row_ptr[u + 1] : rs) : 0;
+    };
+    int64_t nrs, nre;
+    load_rows(sg.u0, nrs, nre);
     for (uint32_t ub = sg.u0; ub < sg.u1; ub += 32) {
       const uint32_t u = ub + lane;
       const bool ur = u < sg.u1;
-      const int64_t rs64 = row_ptr[ur ? u : sg.u1];
-      const int64_t re64 = ur ? row_ptr[u + 1] : rs64;
+      const int64_t rs64 = nrs, re64 = nre;
+      load_rows(ub + 32, nrs, nre);
+      const bool nonempty = ur && re64 > rs64;
       if (!PLACE) {
         if (ur) {
           const int64_t dg = re64 - rs64;
@@ -1466,67 +1509,83 @@ __global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
         }
         dang += __popc(__ballot_sync(0xffffffffu, ur && re64 == rs64));
       }
+      // the batch's non-empty rows in order: the k-th row start of the batch is row rowlist[k]
+      const uint32_t N = __ballot_sync(0xffffffffu, nonempty);
+      if (nonempty) rowlist[__popc(N & lt)] = (uint8_t)lane;
+      __syncwarp();
       const int64_t bs = __shfl_sync(0xffffffffu, rs64, 0);
       const int64_t be = __shfl_sync(0xffffffffu, re64, 31);
       const uint32_t rs = (uint32_t)(rs64 - bs);         // row starts relative to the batch (m < 2^32)
       uint32_t pv = 0, pj = 0;                           // edge before the step (lane 31 of the previous one)
-      for (int64_t x0 = bs; x0 < be; x0 += 32) {
-        const int64_t x = x0 + lane;
-        const bool valid = x < be;
-        const uint32_t v = valid ? col[x] : 0u;
-        const uint32_t xr = (uint32_t)(x - bs);
-        int r = 0;                                        // row of x: the last lane r with rs_r <= x
+      uint32_t starts = 0;                               // row starts before the step
+      for (int64_t x0 = bs; x0 < be; x0 += 32 * D) {
+        uint32_t vv[D];
 #pragma unroll
-        for (int st = 16; st; st >>= 1) {
-          const uint32_t t = __shfl_sync(0xffffffffu, rs, r + st);
-          if (t <= xr) r += st;
+        for (int d = 0; d < D; ++d) {
+          const int64_t x = x0 + 32 * d + lane;
+          vv[d] = x < be ? __ldcs(col + x) : 0u;
         }
-        const bool first = __shfl_sync(0xffffffffu, rs, r) == xr;
-        uint32_t j = v >> b;
-        const uint32_t upv = __shfl_up_sync(0xffffffffu, v, 1), upj = __shfl_up_sync(0xffffffffu, j, 1);
-        const uint32_t prv = lane ? upv : pv, prj = lane ? upj : pj;
-        if (!PLACE && valid) {
-          if (v >= (uint32_t)n_dst) errs |= 2u;
-          if (!first && prv >= v) errs |= 4u;
-        }
-        if (j >= (uint32_t)k_dst) j = (uint32_t)k_dst - 1;   // invalid input: keep indices in range
-        const bool flag = !COMPRESS || first || prj != j;   // Alg. 2 prev_bin / MSB demarcation
-        const uint32_t F = __ballot_sync(0xffffffffu, valid && flag);
-        const uint32_t me = __match_any_sync(0xffffffffu, valid ? j : 0xFFFFFFFFu);
-        const bool lead = lane == 31 - __clz(me);         // highest lane of the same-j group
-        if (!PLACE) {
-          if (valid && lead) {
-            ci[j] += __popc(me);
-            cr[j] += __popc(me & F);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int64_t xc = x0 + 32 * d;
+          if (xc >= be) break;
+          const int64_t x = xc + lane;
+          const bool valid = x < be;
+          const uint32_t v = vv[d];
+          const uint32_t xr = (uint32_t)(xc - bs);
+          // row starts inside this step (bit l: a non-empty row starts at edge xc + l)
+          const uint32_t Bm = __reduce_or_sync(0xffffffffu, (nonempty && rs - xr < 32u) ? 1u << (rs - xr) : 0u);
+          const bool first = (Bm >> lane) & 1u;
+          const uint32_t k = starts + __popc(Bm & le);      // row starts at or before x
+          starts += __popc(Bm);
+          const uint32_t r = k ? rowlist[k - 1] : 0u;
+          uint32_t j = v >> b;
+          const uint32_t upv = __shfl_up_sync(0xffffffffu, v, 1), upj = __shfl_up_sync(0xffffffffu, j, 1);
+          const uint32_t prv = lane ? upv : pv, prj = lane ? upj : pj;
+          if (!PLACE && valid) {
+            if (v >= (uint32_t)n_dst) errs |= 2u;
+            if (!first && prv >= v) errs |= 4u;
           }
-        } else {
-          uint32_t bi = 0, br = 0;
-          if (valid) {
-            bi = ci[j];
-            br = cr[j];
-          }
-          __syncwarp();
-          if (valid) {
-            const uint32_t pos = bi + __popc(me & lt);
-            ids16[pos] = (uint16_t)((v & qmask) | (flag ? 0x8000u : 0u));
-            if (WIDE) ids32[pos] = v | (flag ? 0x80000000u : 0u);
-            if (WEIGHTED) w[pos] = val[x];
-            if (flag) {
-              const uint32_t pp = br + __popc(me & F & lt);
-              const uint32_t uu = ub + (uint32_t)r;
-              png16[pp] = (uint16_t)(uu & qmask);
-              if (WIDE) png32[pp] = uu;
+          if (j >= (uint32_t)k_dst) j = (uint32_t)k_dst - 1;   // invalid input: keep indices in range
+          const bool flag = !COMPRESS || first || prj != j;   // Alg. 2 prev_bin / MSB demarcation
+          const uint32_t F = __ballot_sync(0xffffffffu, valid && flag);
+          const uint32_t me = __match_any_sync(0xffffffffu, valid ? j : 0xFFFFFFFFu);
+          const bool lead = lane == 31 - __clz(me);         // highest lane of the same-j group
+          if (!PLACE) {
+            if (valid && lead) {
+              ci[j] += __popc(me);
+              cr[j] += __popc(me & F);
             }
-            if (lead) {
-              ci[j] = bi + __popc(me);
-              cr[j] = br + __popc(me & F);
+          } else {
+            uint32_t bi = 0, br = 0;
+            if (valid) {
+              bi = ci[j];
+              br = cr[j];
             }
+            __syncwarp();
+            if (valid) {
+              const uint32_t pos = bi + __popc(me & lt);
+              ids16[pos] = (uint16_t)((v & qmask) | (flag ? 0x8000u : 0u));
+              if (WIDE) ids32[pos] = v | (flag ? 0x80000000u : 0u);
+              if (WEIGHTED) w[pos] = val[x];
+              if (flag) {
+                const uint32_t pp = br + __popc(me & F & lt);
+                const uint32_t uu = ub + r;
+                png16[pp] = (uint16_t)(uu & qmask);
+                if (WIDE) png32[pp] = uu;
+              }
+              if (lead) {
+                ci[j] = bi + __popc(me);
+                cr[j] = br + __popc(me & F);
+              }
+            }
+            __syncwarp();
           }
-          __syncwarp();
+          pv = __shfl_sync(0xffffffffu, v, 31);
+          pj = __shfl_sync(0xffffffffu, j, 31);
         }
-        pv = __shfl_sync(0xffffffffu, v, 31);
-        pj = __shfl_sync(0xffffffffu, j, 31);
       }
+      __syncwarp();
     }
     __syncwarp();
     if (!PLACE) {
@@ -1542,6 +1601,420 @@ __global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
     for (int o = 16; o; o >>= 1) errs |= __shfl_xor_sync(0xffffffffu, errs, o);
     if (lane == 0 && errs) atomicOr(err, errs);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-tile form of the two passes (the default; DESIGN.md §5 "build").  One CTA owns a
+// segment and walks it in tiles of kTileE consecutive CSR edges:
+//   prep   : column loads (coalesced, a whole tile in flight), the row of every edge
+//            (row starts marked, then a block max-scan), the run flags of Alg. 2;
+//   count  : per-bin ID and run counts with shared-memory atomics;
+//   place  : a stable block radix sort of the tile by bin j (LSD, 4-bit digits,
+//            warp-striped ranking with ballots), then each bin's run of the tile goes
+//            to its running slot -- consecutive positions, so the CTA's writes fill
+//            whole sectors while they are still in L2 (148 CTAs x k_dst open sectors,
+//            ~10 MB, instead of one open sector per (warp, bin)).
+constexpr int kTileThreads = 512, kTileWarps = kTileThreads / 32;
+constexpr int kTileE = 8192;                        // edges per tile
+constexpr int kTileItems = kTileE / kTileThreads;   // 16 per thread, warp-striped: element w*512 + l + 32 k
+constexpr int kRadixBits = 4, kRadixB = 1 << kRadixBits;
+
+struct TileSmem {           // carved from dynamic shared memory (k_dst-sized arrays first)
+  uint32_t* ci;             // [k_dst] counts (count) / running ID slot (place)
+  uint32_t* cr;             // [k_dst] run counts / running PNG slot
+  uint16_t* bstart;         // [k_dst] first sorted index of bin j in the tile
+  uint16_t* bfstart;        // [k_dst] flags before that index
+  uint16_t* key[2];         // [kTileE] bin j
+  uint32_t* pay[2];         // [kTileE] (v & (q-1)) | flag << 15 | (u & (q-1)) << 16; pay[1] doubles as the row marks
+  uint16_t* idx[2];         // [kTileE] tile position (weights)
+  uint32_t* sbits;          // [kTileE / 32] row-start bits
+  uint32_t* wsum;           // [kTileWarps * kRadixB + 64] scan scratch
+  uint32_t* colb[2];        // [kTileE + 8] the tile's columns (bulk-copied one tile ahead)
+};
+
+size_t tile_smem_bytes(int64_t k_dst) {
+  const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
+  return kd * 4 * 2 + kd * 2 * 2 + (size_t)kTileE * (2 + 4 + 2) * 2 + kTileE / 32 * 4 +
+         (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileE + 8) * 4 + 64;
+}
+
+__device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst) {
+  const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
+  TileSmem t;
+  t.ci = reinterpret_cast<uint32_t*>(base);
+  t.cr = t.ci + kd;
+  t.pay[0] = t.cr + kd;
+  t.pay[1] = t.pay[0] + kTileE;
+  t.sbits = t.pay[1] + kTileE;
+  t.wsum = t.sbits + kTileE / 32;
+  t.colb[0] = t.wsum + kTileWarps * kRadixB + 64;
+  t.colb[1] = t.colb[0] + kTileE + 8;
+  t.key[0] = reinterpret_cast<uint16_t*>(t.colb[1] + kTileE + 8);
+  t.key[1] = t.key[0] + kTileE;
+  t.idx[0] = t.key[1] + kTileE;
+  t.idx[1] = t.idx[0] + kTileE;
+  t.bstart = t.idx[1] + kTileE;
+  t.bfstart = t.bstart + kd;
+  return t;
+}
+
+template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED>
+__global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
+    const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
+    const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst, int kbits,
+    uint32_t* CI, uint32_t* CR, const uint32_t* __restrict__ G, uint32_t* outdeg, float* inv_deg,
+    unsigned long long* n_dang, uint32_t* err, uint16_t* ids16, uint32_t* ids32, float* w, uint16_t* png16,
+    uint32_t* png32) {
+  extern __shared__ __align__(16) uint8_t tsm[];
+  const TileSmem T = tile_carve(tsm, k_dst);
+  const int tid = threadIdx.x;
+  __shared__ uint32_t seg_s;
+  __shared__ __align__(8) uint64_t cbar[2];
+  // the tile's 16 B-aligned middle [a, c) of col comes in by one bulk copy (TMA engine), issued
+  // one tile ahead; its ragged ends are loaded by threads.  Element x of a tile starting at x0
+  // lives at colb[x - (x0 & ~3)].
+  const bool bulk_ok = (reinterpret_cast<uintptr_t>(col) & 15) == 0;
+  auto issue_cols = [&](int bsel, int64_t x0, int64_t x1) {       // thread 0
+    const int64_t a = (x0 + 3) & ~int64_t(3), c = x1 & ~int64_t(3);
+    if (bulk_ok && c > a) {
+      mbar_arrive_expect_tx(&cbar[bsel], (uint32_t)((c - a) * 4));
+      bulk_g2s(T.colb[bsel] + (a - (x0 & ~int64_t(3))), col + a, (uint32_t)((c - a) * 4), &cbar[bsel],
+               policy_evict_first());
+    } else {
+      mbar_arrive(&cbar[bsel]);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&cbar[0], 1);
+    mbar_init(&cbar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  uint32_t cphase[2] = {0u, 0u};
+  const int lane = tid & 31, warp = tid >> 5;
+  const uint32_t qmask = (1u << b) - 1u;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t errs = 0;
+  for (;;) {
+    if (tid == 0) seg_s = atomicAdd(seg_ctr, 1u);
+    __syncthreads();
+    const uint32_t sidx = seg_s;
+    if (sidx >= (uint32_t)n_seg) break;
+    const BSeg sg = segs[sidx];
+    for (int64_t j = tid; j < k_dst; j += kTileThreads) {
+      if (PLACE) {
+        T.ci[j] = CI[(int64_t)sidx * k_dst + j];
+        T.cr[j] = CR[(int64_t)sidx * k_dst + j] + G[(int64_t)sg.p * k_dst + j];
+      } else {
+        T.ci[j] = 0u;
+        T.cr[j] = 0u;
+      }
+    }
+    // out-degrees of the segment's rows (count pass)
+    if (!PLACE) {
+      uint32_t dang = 0;
+      for (uint32_t u = sg.u0 + tid; u < sg.u1; u += kTileThreads) {
+        const int64_t dg = row_ptr[u + 1] - row_ptr[u];
+        if (dg < 0) errs |= 1u;
+        outdeg[u] = (uint32_t)(dg > 0 ? dg : 0);
+        inv_deg[u] = dg > 0 ? 1.0f / (float)dg : 0.0f;
+        dang += dg == 0;
+      }
+      for (int o = 16; o; o >>= 1) dang += __shfl_xor_sync(0xffffffffu, dang, o);
+      if (lane == 0 && dang) atomicAdd(n_dang, (unsigned long long)dang);
+    }
+    const int64_t e0 = row_ptr[sg.u0], e1 = row_ptr[sg.u1];
+    uint32_t rnext = sg.u0;               // first row whose start is >= the tile's first edge
+    uint32_t rcur = sg.u0;                // row of the edge before the tile
+    uint32_t pj = 0xFFFFFFFFu, pv = 0;    // bin / column of the edge before the tile
+    int cb = 0;                           // column buffer of the current tile
+    if (tid == 0 && e0 < e1) issue_cols(0, e0, min(e1, e0 + kTileE));
+    __syncthreads();
+    for (int64_t x0 = e0; x0 < e1; x0 += kTileE, cb ^= 1) {
+      const int n = (int)min((int64_t)kTileE, e1 - x0);
+      const int64_t x1 = x0 + n;
+      // next tile's columns in flight under this tile's work (its buffer was last read by
+      // the previous tile, which every thread has finished)
+      if (tid == 0 && x1 < e1) issue_cols(cb ^ 1, x1, min(e1, x1 + kTileE));
+      // ---- prep: columns, row marks
+      uint32_t* mark = T.pay[1];
+      for (int i = tid; i < kTileE; i += kTileThreads) mark[i] = 0u;
+      for (int i = tid; i < kTileE / 32; i += kTileThreads) T.sbits[i] = 0u;
+      uint32_t* vfull = T.colb[cb] + (x0 & 3);   // vfull[i] = col[x0 + i]
+      {
+        const int64_t a = (x0 + 3) & ~int64_t(3), c = x1 & ~int64_t(3);
+        if (!bulk_ok || c <= a) {
+          for (int i = tid; i < n; i += kTileThreads) vfull[i] = __ldcs(col + x0 + i);
+        } else {
+          if (tid < a - x0) vfull[tid] = __ldcs(col + x0 + tid);                 // head (< 4)
+          if (tid >= 4 && tid - 4 < x1 - c) vfull[c - x0 + tid - 4] = __ldcs(col + c + tid - 4);   // tail (< 4)
+        }
+      }
+      mbar_wait(&cbar[cb], cphase[cb]);
+      cphase[cb] ^= 1u;
+      __syncthreads();
+      if (tid == 0) mark[0] = rcur + 1;   // edges before the first row start belong to rcur
+      for (uint32_t rb = rnext;; rb += kTileThreads) {
+        const uint32_t r = rb + tid;
+        int64_t rs = x1, re = x1;
+        if (r < sg.u1) {
+          rs = row_ptr[r];
+          re = row_ptr[r + 1];
+        }
+        const bool in = r < sg.u1 && rs < x1;
+        if (in && re > rs) {              // a non-empty row starting inside the tile
+          atomicMax(&mark[rs - x0], r + 1);
+          atomicOr(&T.sbits[(rs - x0) >> 5], 1u << ((rs - x0) & 31));
+        }
+        const int cnt = __syncthreads_count(in);
+        if (cnt < kTileThreads) {
+          rnext = rb + cnt;
+          break;
+        }
+      }
+      __syncthreads();
+      // block max-scan of the marks: element i's row (+1); warp-striped, 16 per thread; the 16
+      // rounds are scanned independently, then chained by their maxima (ILP instead of a chain)
+      {
+        const int base = warp * (kTileE / kTileWarps);
+        uint32_t loc[kTileItems];
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) loc[k] = mark[base + 32 * k + lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int k = 0; k < kTileItems; ++k) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, loc[k], o);
+            if (lane >= o) loc[k] = max(loc[k], y);
+          }
+        uint32_t mx = 0;
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const uint32_t top = __shfl_sync(0xffffffffu, loc[k], 31);
+          loc[k] = max(loc[k], mx);
+          mx = max(mx, top);
+        }
+        if (lane == 0) T.wsum[warp] = mx;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int ww = 0; ww < warp; ++ww) before = max(before, T.wsum[ww]);
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) mark[base + 32 * k + lane] = max(loc[k], before);
+      }
+      __syncthreads();
+      // carries for the next tile (the marks are overwritten by the payloads below)
+      if (tid == 0) T.wsum[kTileWarps * kRadixB + 2] = mark[n - 1] - 1u;
+      // ---- per edge: bin, run flag, payload
+      for (int i = tid; i < kTileE; i += kTileThreads) {
+        if (i < n) {
+          const uint32_t v = vfull[i];
+          const uint32_t u = mark[i] - 1u;
+          const bool first = (T.sbits[i >> 5] >> (i & 31)) & 1u;
+          const uint32_t prv = i ? vfull[i - 1] : pv;
+          uint32_t j = v >> b;
+          if (!PLACE) {
+            if (v >= (uint32_t)n_dst) errs |= 2u;
+            if (!first && prv >= v) errs |= 4u;
+          }
+          if (j >= (uint32_t)k_dst) j = (uint32_t)k_dst - 1;
+          uint32_t prj = i ? (prv >> b) : pj;
+          if (i && prj >= (uint32_t)k_dst) prj = (uint32_t)k_dst - 1;
+          const bool flag = !COMPRESS || first || prj != j;
+          T.key[0][i] = (uint16_t)j;
+          T.idx[0][i] = (uint16_t)i;
+          T.pay[0][i] = (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
+          if (!PLACE) {
+            atomicAdd(&T.ci[j], 1u);
+            if (flag) atomicAdd(&T.cr[j], 1u);
+          }
+        } else {
+          T.key[0][i] = 0xFFFFu;          // padding sorts last
+          T.idx[0][i] = 0;
+          T.pay[0][i] = 0u;
+        }
+      }
+      __syncthreads();
+      // carry (every thread needs pj/pv/rcur for the next tile): broadcast through smem
+      if (tid == 0) {
+        const uint32_t lv = vfull[n - 1];
+        uint32_t lj = lv >> b;
+        if (lj >= (uint32_t)k_dst) lj = (uint32_t)k_dst - 1;
+        T.wsum[kTileWarps * kRadixB] = lv;
+        T.wsum[kTileWarps * kRadixB + 1] = lj;
+      }
+      __syncthreads();
+      pv = T.wsum[kTileWarps * kRadixB];
+      pj = T.wsum[kTileWarps * kRadixB + 1];
+      rcur = T.wsum[kTileWarps * kRadixB + 2];
+      if (!PLACE) {
+        __syncthreads();
+        continue;
+      }
+
+      // ---- stable LSD radix sort of the tile by bin (kbits bits, 4 per pass)
+      int cur = 0;
+      for (int sh = 0; sh < kbits; sh += kRadixBits) {
+        const uint16_t* kin = T.key[cur];
+        const uint32_t* pin = T.pay[cur];
+        const uint16_t* iin = T.idx[cur];
+        const int base = warp * (kTileE / kTileWarps);
+        uint32_t rnk[kTileItems];
+        uint32_t dig[kTileItems];
+        uint32_t cnt = 0;                         // lane d < 16: this warp's count of digit d
+        const uint32_t dd = lane & (kRadixB - 1);
+        // rounds are independent: ballots per round, then lane dd's running count of digit dd
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const uint32_t d = (kin[base + 32 * k + lane] >> sh) & (kRadixB - 1);
+          uint32_t peers = 0xffffffffu, mdd = 0xffffffffu;   // lanes with my digit / with digit dd
+#pragma unroll
+          for (int bt = 0; bt < kRadixBits; ++bt) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bt) & 1u);
+            peers &= ((d >> bt) & 1u) ? bal : ~bal;
+            mdd &= ((dd >> bt) & 1u) ? bal : ~bal;
+          }
+          dig[k] = d;
+          rnk[k] = cnt | (__popc(peers & lt) << 16);        // (count before the round, rank in the round)
+          cnt += __popc(mdd);
+        }
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k)
+          rnk[k] = __shfl_sync(0xffffffffu, rnk[k] & 0xFFFFu, dig[k]) + (rnk[k] >> 16);
+        if (lane >= kRadixB) cnt = 0;
+        // warp totals per digit -> block bases: base(w, d) = sum_{d' < d} total(d') + sum_{w' < w} cnt(w', d)
+        if (lane < kRadixB) T.wsum[lane * kTileWarps + warp] = cnt;     // digit-major
+        __syncthreads();
+        if (warp == 0) {
+          // exclusive scan of the kRadixB * kTileWarps (= 256) counts, 8 per lane
+          uint32_t v8[8], s8 = 0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            v8[k] = T.wsum[lane * 8 + k];
+            s8 += v8[k];
+          }
+          uint32_t inc = s8;
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+          }
+          uint32_t run = inc - s8;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            T.wsum[lane * 8 + k] = run;
+            run += v8[k];
+          }
+        }
+        __syncthreads();
+        const int nxt = cur ^ 1;
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const int src = base + 32 * k + lane;
+          const uint32_t dst = T.wsum[dig[k] * kTileWarps + warp] + rnk[k];
+          T.key[nxt][dst] = kin[src];
+          T.pay[nxt][dst] = pin[src];
+          T.idx[nxt][dst] = iin[src];
+        }
+        __syncthreads();
+        cur = nxt;
+      }
+      // ---- positions: bin runs of the sorted tile, flag prefix
+      {
+        const uint16_t* ks = T.key[cur];
+        const uint32_t* ps = T.pay[cur];
+        const uint16_t* is = T.idx[cur];
+        const int base = warp * (kTileE / kTileWarps);
+        uint32_t fpre[kTileItems];
+        uint32_t fw = 0;
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const uint32_t f = (ps[base + 32 * k + lane] >> 15) & 1u;
+          const uint32_t bal = __ballot_sync(0xffffffffu, f);
+          fpre[k] = fw + __popc(bal & lt);
+          fw += __popc(bal);
+        }
+        if (lane == 0) T.wsum[warp] = fw;
+        __syncthreads();
+        uint32_t fbase = 0;
+        for (int ww = 0; ww < warp; ++ww) fbase += T.wsum[ww];
+        // run starts: bstart[j] = first sorted index of j, bfstart[j] = flags before it
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const int i = base + 32 * k + lane;
+          if (i < n) {
+            const uint32_t j = ks[i];
+            if (i == 0 || ks[i - 1] != j) {
+              T.bstart[j] = (uint16_t)i;
+              T.bfstart[j] = (uint16_t)(fbase + fpre[k]);
+            }
+          }
+        }
+        __syncthreads();
+        uint32_t nci[kTileItems], ncr[kTileItems];
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const int i = base + 32 * k + lane;
+          nci[k] = ncr[k] = 0xFFFFFFFFu;
+          if (i < n) {
+            const uint32_t j = ks[i];
+            const uint32_t pw = ps[i];
+            const bool f = (pw >> 15) & 1u;
+            const uint32_t pos = T.ci[j] + (uint32_t)(i - T.bstart[j]);
+            const uint32_t fx = fbase + fpre[k];                      // flags before i in the tile
+            const uint32_t pp = T.cr[j] + (fx - T.bfstart[j]);
+            ids16[pos] = (uint16_t)(pw & 0xFFFFu);
+            if (WIDE) ids32[pos] = ((j << b) | (pw & qmask)) | (f ? 0x80000000u : 0u);
+            if (WEIGHTED) w[pos] = val[x0 + is[i]];
+            if (f) {
+              png16[pp] = (uint16_t)(pw >> 16);
+              if (WIDE) png32[pp] = (sg.p << b) | (pw >> 16);
+            }
+            if (i == n - 1 || ks[i + 1] != j) {   // the bin's last element in the tile
+              nci[k] = pos + 1;
+              ncr[k] = pp + (f ? 1u : 0u);
+            }
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k)
+          if (nci[k] != 0xFFFFFFFFu) {
+            const uint32_t j = ks[base + 32 * k + lane];
+            T.ci[j] = nci[k];
+            T.cr[j] = ncr[k];
+          }
+        __syncthreads();
+      }
+    }
+    if (!PLACE) {
+      __syncthreads();
+      for (int64_t j = tid; j < k_dst; j += kTileThreads) {
+        CI[(int64_t)sidx * k_dst + j] = T.ci[j];
+        CR[(int64_t)sidx * k_dst + j] = T.cr[j];
+      }
+    }
+    __syncthreads();
+  }
+  if (!PLACE) {
+    for (int o = 16; o; o >>= 1) errs |= __shfl_xor_sync(0xffffffffu, errs, o);
+    if (lane == 0 && errs) atomicOr(err, errs);
+  }
+}
+
+using TilePassFn = void (*)(const BSeg*, int, uint32_t*, const int64_t*, const uint32_t*, const float*, int, int64_t,
+                            int64_t, int, uint32_t*, uint32_t*, const uint32_t*, uint32_t*, float*,
+                            unsigned long long*, uint32_t*, uint16_t*, uint32_t*, float*, uint16_t*, uint32_t*);
+
+template <bool PLACE>
+TilePassFn tile_pass_fn(bool compress, bool wide, bool weighted) {
+#define PCPM_TILE_FN(C, WI, WE) \
+  if (compress == C && wide == WI && weighted == WE) return k_tile_pass<PLACE, C, WI, WE>;
+  PCPM_TILE_FN(true, false, false) PCPM_TILE_FN(true, false, true) PCPM_TILE_FN(true, true, false)
+  PCPM_TILE_FN(true, true, true) PCPM_TILE_FN(false, false, false) PCPM_TILE_FN(false, false, true)
+  PCPM_TILE_FN(false, true, false) PCPM_TILE_FN(false, true, true)
+#undef PCPM_TILE_FN
+  return nullptr;
 }
 
 // Column prefix of a [rows x cols] count matrix, in place: cnt[r][c] <- sum_{r' < r} cnt[r'][c];
@@ -1685,7 +2158,11 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     set_error(PCPM_EBADCSR, "row_ptr is not monotone, or row_ptr[0] != 0, or row_ptr[n_src] != nnz");
     return PCPM_EBADCSR;
   }
-  int64_t seg_target = std::max<int64_t>(int64_t(1) << 16, m / ((int64_t)h->num_sms * kCntWarps * 3) + 1);
+  // warp mode (PCPM_BUILD_COUNT_MODE=warp, A/B): one warp per segment; tile mode (default): one CTA
+  const char* cmode = getenv("PCPM_BUILD_COUNT_MODE");
+  const bool warp_mode = cmode && !strcmp(cmode, "warp");
+  int64_t seg_target = warp_mode ? std::max<int64_t>(int64_t(1) << 16, m / ((int64_t)h->num_sms * kCntWarps * 3) + 1)
+                                 : std::max<int64_t>(int64_t(1) << 16, m / ((int64_t)h->num_sms * 6) + 1);
   if (const char* e = getenv("PCPM_BUILD_SEG_EDGES")) seg_target = std::max<int64_t>(1, atoll(e));   // tests
   std::vector<BSeg> segs;
   std::vector<uint32_t> seg_first(k_src + 1);
@@ -1744,17 +2221,33 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   pt.mark("count build: plan + allocations");
 
   const bool weighted_ids = h->weighted && values != nullptr;
-  const size_t smem = (size_t)kCntWarps * 2 * k_dst * sizeof(uint32_t);
+  const size_t smem = warp_mode ? (size_t)kCntWarps * 2 * k_dst * sizeof(uint32_t) + kCntWarps * 32
+                                : tile_smem_bytes(k_dst);
+  const int kbits = std::max(1, bits_for((uint64_t)std::max<int64_t>(k_dst - 1, 0)));
   SegPassFn cnt_fn = seg_pass_fn<false>(h->compressed, h->wide, weighted_ids);
   SegPassFn place_fn = seg_pass_fn<true>(h->compressed, h->wide, weighted_ids);
-  TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n_seg + kCntWarps - 1) / kCntWarps, h->num_sms));
+  TilePassFn tcnt_fn = tile_pass_fn<false>(h->compressed, h->wide, weighted_ids);
+  TilePassFn tplace_fn = tile_pass_fn<true>(h->compressed, h->wide, weighted_ids);
+  if (warp_mode) {
+    TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  } else {
+    TK(cudaFuncSetAttribute(tcnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TK(cudaFuncSetAttribute(tplace_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  }
+  const int grid = warp_mode
+                       ? (int)std::max<int64_t>(1, std::min<int64_t>((n_seg + kCntWarps - 1) / kCntWarps, h->num_sms))
+                       : (int)std::max<int64_t>(1, std::min<int64_t>(n_seg, h->num_sms));
 
   // ---- pass 1: counts, out-degrees, validation
-  cnt_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI, CR,
-                                            nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr, nullptr,
-                                            nullptr, nullptr);
+  if (warp_mode)
+    cnt_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI, CR,
+                                              nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr, nullptr,
+                                              nullptr, nullptr);
+  else
+    tcnt_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+                                             CI, CR, nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr,
+                                             nullptr, nullptr, nullptr);
   TK(cudaGetLastError());
   uint32_t herr = 0;
   TK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
@@ -1797,9 +2290,14 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 
   // ---- pass 2: place IDs (+ weights) and PNG sources
   TK(cudaMemsetAsync(ctr, 0, 4, s));
-  place_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI, CR, G,
-                                              nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w, h->png16,
-                                              h->wide ? h->png_src : nullptr);
+  if (warp_mode)
+    place_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI,
+                                                CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
+                                                h->png16, h->wide ? h->png_src : nullptr);
+  else
+    tplace_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+                                               CI, CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
+                                               h->png16, h->wide ? h->png_src : nullptr);
   TK(cudaGetLastError());
   if (h->weighted && !values) {
     // PCPM_KEEP_VALUES without values: every weight is 1

@@ -177,7 +177,13 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
   const uint64_t pol = policy_evict_first();
   int stage = 0;
   uint32_t phase = 0;
+  bool claimed = false;
   auto claim = [&]() -> uint32_t {
+    if (a.static_items) {                         // cluster gather: CTA b owns item b only
+      const uint32_t v = claimed ? (uint32_t)a.n_items : blockIdx.x;
+      claimed = true;
+      return v;
+    }
     uint32_t v = 0;
     if (lane == 0) v = atomicAdd(&a.counters[0], 1u);
     return __shfl_sync(0xffffffffu, v, 0);
@@ -1108,6 +1114,182 @@ __global__ void __launch_bounds__(1024, 1) k_gather2(const GatherArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// k_gather_cl: the gather for graphs with few destination partitions (k_dst <
+// SMs / 2, e.g. C2: k = 32 on 148 SMs).  Each bin is cut into cs tile-aligned slices
+// processed by the cs CTAs of one thread-block cluster (cs = 2..8), each into its own
+// shared-memory accumulator; after a cluster barrier every CTA applies 1/cs of the
+// bin's vertices, summing the cs partial low words straight out of its peers' shared
+// memory (distributed shared memory, ld.shared::cluster) -- no slot buffers in global
+// memory and no separate apply launch (the single-CTA path's k_apply_split).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_size() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+  return ra;
+}
+__device__ __forceinline__ uint4 dsmem_ld4(uint32_t ra) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(ra) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t dsmem_ld(uint32_t ra) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+  return v;
+}
+
+template <typename IdT, bool W, bool PR>
+__global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather_cl(const GatherArgs a) {
+  using C = Cfg<IdT, W>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t q = int64_t(1) << a.b;
+  uint32_t* acc = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* bitmap = acc + ((q + 31) / 32) * 32;
+  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
+  uint8_t* stage_base = reinterpret_cast<uint8_t*>(bitmap + ((bm_words + 31) / 32) * 32);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
+  uint64_t* empty = full + S;
+  uint32_t* orbm = reinterpret_cast<uint32_t*>(empty + S);               // [bm_words] OR of the cluster's bitmaps
+  uint32_t* flag_s = orbm + ((bm_words + 3) & ~3);
+  const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);
+    }
+    fence_mbar_init();
+  }
+  for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc[i] = 0u;
+  for (int i = threadIdx.x; i < bm_words; i += blockDim.x) bitmap[i] = 0u;
+  __syncthreads();
+  if (warp == 0) {
+    gather_producer<C, IdT, W, PR, false>(a, ids, stage_base, meta, full, empty, lane);
+  } else {
+    const int cw = warp - 1;
+    const int grp = cw < C::kGroupA ? 0 : 1;
+    const int gw = grp ? cw - C::kGroupA : cw;
+    const int gsz = grp ? C::kGroupB : C::kGroupA;
+    const uint32_t qmask = (uint32_t)(q - 1);
+    float sp_scale_f = 1.0f;
+    if constexpr (!PR) sp_scale_f = ldexpf(1.0f, spmv_fbits(*a.xmax, a.wexp));
+    const uint32_t lemask = lanemask_le();
+    int stage = grp, rot = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      const StageMeta m = meta[stage];
+      if (m.flags & kFlagStop) break;
+      if (!(m.flags & kFlagEmpty))
+        decode_stage<C, IdT, W, PR>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
+                                    lemask, lane, sp_scale_f, m.j << a.b);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      stage += 2;
+      if (stage >= S) { stage -= S; phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();                              // every slice of the bin is accumulated
+  const uint32_t rank = cluster_rank(), cs = cluster_size();
+  const uint32_t j = a.items[blockIdx.x].j;
+  const uint32_t v0 = j << a.b;
+  const uint32_t cnt = (uint32_t)min(q, a.n_dst - (int64_t)v0);
+  for (int i = threadIdx.x; i < bm_words; i += blockDim.x) {
+    uint32_t o = 0;
+    for (uint32_t r = 0; r < cs; ++r) o |= dsmem_ld(dsmem_addr(bitmap + i, r));
+    orbm[i] = o;
+  }
+  __syncthreads();
+  const uint32_t per = ((cnt + cs - 1) / cs + 3) & ~3u;     // this CTA's vertices [i0, i1)
+  const uint32_t i0 = min(cnt, rank * per), i1 = min(cnt, i0 + per);
+  const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);
+  const double inv_scale = 1.0 / (double)fscale;
+  double base_pr = 0.0, sp_inv = 1.0;
+  if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+  else sp_inv = ldexp(1.0, -spmv_fbits(*a.xmax, a.wexp));
+  unsigned long long dang = 0, res = 0;
+  auto carry_of = [&](uint32_t i) -> uint64_t {    // the global high word of local vertex i (reset)
+    if (!((orbm[i >> 10] >> ((i >> 5) & 31)) & 1u)) return 0;
+    const uint64_t hv = (uint64_t)ldcg_u32(&a.hi[v0 + i]) << 32;
+    a.hi[v0 + i] = 0u;
+    return hv;
+  };
+  // 4 consecutive vertices per thread (i0 and per are multiples of 4)
+  for (uint32_t i = i0 + 4 * threadIdx.x; i < i1; i += 4 * blockDim.x) {
+    uint64_t su[4] = {0, 0, 0, 0};
+    long long ss[4] = {0, 0, 0, 0};
+    for (uint32_t r = 0; r < cs; ++r) {
+      const uint4 w4 = dsmem_ld4(dsmem_addr(acc + i, r));
+      const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        su[c] += wv[c];
+        ss[c] += (int32_t)wv[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t ii = i + c;
+      if (ii >= i1) break;
+      const uint32_t v = v0 + ii;
+      const uint64_t tot = carry_of(ii) + (PR ? su[c] : (uint64_t)ss[c]);
+      if constexpr (PR) {
+        const double prn = base_pr + a.d * ((double)(long long)tot * inv_scale);
+        const float idg = __ldg(a.inv_deg + v);
+        a.pr_new[v] = (float)prn;
+        a.spr_new[v] = (float)prn * idg * fscale;
+        if (idg == 0.0f) dang += red_fx(prn);
+        res += red_fx(fabs(prn - (double)__ldg(a.pr_old + v)));
+      } else {
+        a.y[v] = (float)((double)(long long)tot * sp_inv);
+      }
+    }
+  }
+  if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane);
+  __syncthreads();
+  cluster_sync_all();                              // the peers are done reading this CTA's accumulator
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t done = atomicAdd(&a.counters[1], 1u);
+    *flag_s = (done == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (*flag_s && threadIdx.x == 0) {
+    __threadfence();
+    if constexpr (PR) red_finish(a);
+    a.counters[0] = 0u;
+    a.counters[1] = 0u;
+  }
+}
+
+template <typename IdT, bool W>
+int smem_bytes_cl(int b) {
+  using C = Cfg<IdT, W>;
+  const int64_t q = int64_t(1) << b;
+  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
+  const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
+  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
+               ((bm_words + 3) & ~3) * 4 + 16);
+}
+
 // Apply of the split bins (items whose bin was cut into slices): one block per
 // (split bin, 1024-vertex chunk); total = sum of the slices' low words + the carry
 // word.  The last block reduces the per-item (gather) and per-block (here)
@@ -1262,6 +1444,8 @@ bool gather_slots_fit(int b, int acc_words) {
   return smem_bytes_for<uint16_t, false, true>(b, acc_words) <= maxsm;
 }
 
+GatherFn gather_cl_fn(bool wide, bool weighted, bool pagerank);
+
 int prepare_gather(pcpm_handle* h) {
   int maxsm = 0;
   PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
@@ -1290,6 +1474,10 @@ int prepare_gather(pcpm_handle* h) {
     }
   for (int wd = 0; wd < 2; ++wd)
     PCPM_CK(cudaFuncSetAttribute(gather2_fn(wd, false, true, true), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  for (int wd = 0; wd < 2; ++wd)
+    for (int w = 0; w < 2; ++w)
+      for (int p = 0; p < 2; ++p)
+        PCPM_CK(cudaFuncSetAttribute(gather_cl_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   return PCPM_OK;
 }
 
@@ -1331,8 +1519,45 @@ int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaS
   return PCPM_OK;
 }
 
+GatherFn gather_cl_fn(bool wide, bool weighted, bool pagerank) {
+  if (wide)
+    return weighted ? (pagerank ? k_gather_cl<uint32_t, true, true> : k_gather_cl<uint32_t, true, false>)
+                    : (pagerank ? k_gather_cl<uint32_t, false, true> : k_gather_cl<uint32_t, false, false>);
+  return weighted ? (pagerank ? k_gather_cl<uint16_t, true, true> : k_gather_cl<uint16_t, true, false>)
+                  : (pagerank ? k_gather_cl<uint16_t, false, true> : k_gather_cl<uint16_t, false, false>);
+}
+
+int gather_cl_smem_bytes(int b, bool wide, bool weighted) {
+  if (wide) return weighted ? smem_bytes_cl<uint32_t, true>(b) : smem_bytes_cl<uint32_t, false>(b);
+  return weighted ? smem_bytes_cl<uint16_t, true>(b) : smem_bytes_cl<uint16_t, false>(b);
+}
+
+int launch_gather_cl(pcpm_handle* h, const GatherArgs& a0, bool weighted, bool pagerank, cudaStream_t s) {
+  GatherArgs a = a0;
+  a.items = h->gitems_cl;
+  a.n_items = (int)(h->k_dst * h->cl_cs);
+  a.static_items = 1;
+  a.has_split = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)a.n_items);
+  cfg.blockDim = dim3(gather_threads(h->wide, weighted));
+  cfg.dynamicSmemBytes = gather_cl_smem_bytes(a.b, h->wide, weighted);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)h->cl_cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PCPM_CK(cudaLaunchKernelEx(&cfg, gather_cl_fn(h->wide, weighted, pagerank), a));
+  h->launches += 1;
+  return PCPM_OK;
+}
+
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi) {
   const bool slots = a.slot16 != nullptr && !weighted && !multi;
+  if (h->cl_cs >= 2 && h->opt_cluster_gather && !slots && !multi) return launch_gather_cl(h, a, weighted, pagerank, s);
   if (!slots && h->opt_gather_variant == 2) {
     const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
     gather2_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted)<<<grid, 1024,

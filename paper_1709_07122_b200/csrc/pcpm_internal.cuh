@@ -111,6 +111,9 @@ struct pcpm_handle {
   uint32_t* bin_nslices = nullptr;  // [k_dst]
   pcpm::ScatterItem* sitems = nullptr;
   int n_sitems = 0;
+  // cluster gather (k_dst < SMs / 2): bin j's cl_cs slices are items [j * cl_cs, (j + 1) * cl_cs)
+  pcpm::GatherItem* gitems_cl = nullptr;
+  int cl_cs = 0;
 
   // iteration state
   float* pr[2] = {nullptr, nullptr};// [n]
@@ -132,7 +135,8 @@ struct pcpm_handle {
 
   // options (pcpm_set_option)
   int opt_use_graph = 1;
-  int opt_gather_variant = 1;       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
+  int opt_gather_variant = 1;
+  int opt_cluster_gather = 1;       // 1: k_gather_cl for graphs with few partitions (when built), 0: off       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
   int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
   int opt_epi_pf = 4;               // gather: L2 prefetch of the apply's vertex arrays, tiles before the item's end (0 = off)
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
@@ -305,6 +309,7 @@ struct GatherArgs {
   const float* xmax;       // device max|x| of this call (fixed-point scale)
   int wexp;                // max|w| <= 2^wexp
   int pf_tiles;            // L2 prefetch distance of the gather producer, in tiles
+  int static_items;        // 1: CTA b processes items[b] only (the cluster gather), 0: claim from counters[0]
   int epi_pf;              // prefetch inv_deg / pr_old of the item's partition this many tiles before its end
   // fused exchange (pcpm_shard_step_peers): SPR_{t+1} of the slice is also stored to
   // these (peer) buffers, indexed like spr_new

@@ -33,7 +33,8 @@ EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_p
             "pcpm_get_residuals", "pcpm_scatter", "pcpm_set_option", "pcpm_last_launch_count",
             "pcpm_get_phase_times", "pcpm_build_shard", "pcpm_shard_init", "pcpm_shard_step", "pcpm_get_debug_counters",
             "pcpm_shard_step_peers", "pcpm_pagerank_tol", "pcpm_shard_init_peers", "pcpm_ipc_handle_bytes", "pcpm_ipc_alloc", "pcpm_ipc_free", "pcpm_ipc_get_handle",
-            "pcpm_ipc_open", "pcpm_ipc_close", "pcpm_pool_reserve"]
+            "pcpm_ipc_open", "pcpm_ipc_close", "pcpm_pool_reserve", "pcpm_runtime_create", "pcpm_job_submit",
+            "pcpm_job_wait", "pcpm_runtime_destroy"]
 
 
 class PcpmError(RuntimeError):
@@ -105,6 +106,11 @@ def _load():
         "pcpm_ipc_open": (I, [P, ctypes.POINTER(P)]),
         "pcpm_ipc_close": (I, [P]),
         "pcpm_pool_reserve": (I, [I64]),
+        "pcpm_runtime_create": (P, []),
+        "pcpm_job_submit": (I, [P, ctypes.POINTER(pcpm_csr), I, ctypes.c_uint, ctypes.c_double, I, P,
+                                ctypes.POINTER(I64)]),
+        "pcpm_job_wait": (I, [P, I64]),
+        "pcpm_runtime_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -319,3 +325,27 @@ def pcpm_get_debug_counters(reset: bool = True) -> np.ndarray:
     if n < 0:
         _check(n)
     return buf[:n]
+
+
+def pcpm_runtime_create():
+    rt = _lib.pcpm_runtime_create()
+    if not rt:
+        raise PcpmError(pcpm_last_status(), pcpm_last_error())
+    return rt
+
+
+def pcpm_job_submit(rt, csr: pcpm_csr, partition_bits: int, flags: int, d: float, iters: int, out) -> int:
+    """Queue one PageRank job (host or device CSR -> PR in out); returns its id at once."""
+    jid = ctypes.c_int64()
+    _check(_lib.pcpm_job_submit(rt, ctypes.byref(csr), int(partition_bits), int(flags), float(d), int(iters),
+                                _ptr(out), ctypes.byref(jid)))
+    return jid.value
+
+
+def pcpm_job_wait(rt, job_id: int):
+    return _check(_lib.pcpm_job_wait(rt, int(job_id)))
+
+
+def pcpm_runtime_destroy(rt):
+    if rt:
+        _lib.pcpm_runtime_destroy(rt)

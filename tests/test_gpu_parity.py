@@ -363,6 +363,7 @@ def test_spmv_non_square(pcpm):
 
 
 @pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
+                                  {"cluster_gather": 0}, {"gather_variant": 2},
                                   {"epilogue_prefetch": 0}, {"gather_prefetch": 8, "epilogue_prefetch": 16},
                                   {"use_graph": 0}],
                          ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
@@ -401,7 +402,8 @@ CHUNK_CASES = [
 
 
 @pytest.mark.parametrize("name,mk,b,host,flags", CHUNK_CASES, ids=[c[0] for c in CHUNK_CASES])
-@pytest.mark.parametrize("mode", ["count", "count_seg1", "count_seg200", "sort_1", "sort_777", "legacy"])
+@pytest.mark.parametrize("mode", ["count", "count_seg1", "count_seg200", "warp", "warp_seg200", "sort_1", "sort_777",
+                                  "legacy"])
 def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, mode):
     """Every construction gives the oracle's layout, for host or device inputs, weights,
     wide IDs and uncompressed bins: the counting build (default; segments of one
@@ -414,6 +416,10 @@ def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, mode)
         monkeypatch.setenv("PCPM_BUILD_CHUNK_EDGES", mode[5:])
     elif mode.startswith("count_seg"):
         monkeypatch.setenv("PCPM_BUILD_SEG_EDGES", mode[9:])
+    elif mode.startswith("warp"):                    # the warp-per-segment form of the counting build
+        monkeypatch.setenv("PCPM_BUILD_COUNT_MODE", "warp")
+        if mode == "warp_seg200":
+            monkeypatch.setenv("PCPM_BUILD_SEG_EDGES", "200")
     g = mk()
     h = build(pcpm, g, b, device=not host, flags=flags)
     try:
@@ -620,3 +626,50 @@ def test_compact_slots_ragged_partition(pcpm):
     finally:
         pcpm.pcpm_destroy(h0)
         pcpm.pcpm_destroy(h1)
+
+
+def test_job_runtime_matches_oracle_and_single_calls(pcpm):
+    """pcpm_runtime / pcpm_job_*: jobs from host memory (H2D, build, iterations, D2H), run
+    back to back by the native worker with uploads overlapping compute, give the same PR
+    as one pcpm_build + pcpm_pagerank per graph (bit for bit) and match the oracle."""
+    ga = graphs.make_graph("rmat", 12, scale=13, permute=True)
+    gb = graphs.make_graph("er", 9, n=30001, m_raw=300000)
+    jobs = [(ga, 9, 10), (gb, 11, 7), (ga, 9, 10), (gb, 6, 3)]
+    rt = pcpm.pcpm_runtime_create()
+    try:
+        keep, ids, outs = [], [], []
+        for g, b, it in jobs:
+            rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
+            col = np.ascontiguousarray(g.col, dtype=np.uint32)
+            out = np.zeros(g.n_src, dtype=np.float32)
+            keep.append((rp, col))
+            outs.append(out)
+            ids.append(pcpm.pcpm_job_submit(rt, pcpm.make_csr(g.n_src, g.n_dst, rp, col), b, 0, 0.85, it, out))
+        for i in reversed(ids):                  # any wait order
+            pcpm.pcpm_job_wait(rt, i)
+        with pytest.raises(pcpm.PcpmError):
+            pcpm.pcpm_job_wait(rt, ids[0])       # already waited for
+        for (g, b, it), out in zip(jobs, outs):
+            h = build(pcpm, g, b)
+            try:
+                single = np.zeros(g.n_src, dtype=np.float32)
+                pcpm.pcpm_pagerank(h, 0.85, it, single)
+            finally:
+                pcpm.pcpm_destroy(h)
+            np.testing.assert_array_equal(out.view(np.uint32), single.view(np.uint32))
+            pr_check(out, oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, it), "job")
+        # a failing job reports its error and the runtime keeps working
+        bad_rp = np.array([0, 2, 3], dtype=np.int64)
+        bad_col = np.array([1, 0, 0], dtype=np.uint32)        # unsorted row: PCPM_EBADCSR
+        out = np.zeros(2, dtype=np.float32)
+        j = pcpm.pcpm_job_submit(rt, pcpm.make_csr(2, 2, bad_rp, bad_col), 1, 0, 0.85, 2, out)
+        with pytest.raises(pcpm.PcpmError) as e:
+            pcpm.pcpm_job_wait(rt, j)
+        assert e.value.code == pcpm.PCPM_EBADCSR
+        g, b, it = jobs[1]
+        out = np.zeros(g.n_src, dtype=np.float32)
+        j = pcpm.pcpm_job_submit(rt, pcpm.make_csr(g.n_src, g.n_dst, keep[1][0], keep[1][1]), b, 0, 0.85, it, out)
+        pcpm.pcpm_job_wait(rt, j)
+        np.testing.assert_array_equal(out, outs[1])
+    finally:
+        pcpm.pcpm_runtime_destroy(rt)

@@ -101,3 +101,19 @@ def test_relabel_torch_equals_numpy():
     b = graphs.relabel(gt, torch.from_numpy(nid)).to_numpy()
     np.testing.assert_array_equal(a.row_ptr, b.row_ptr)
     np.testing.assert_array_equal(a.col, b.col)
+
+
+def test_column_prefix_keeps_each_rows_leading_columns():
+    g = graphs.make_graph("rmat", 5, scale=10, permute=True, values=True, transpose=True)
+    h = graphs.column_prefix(g, 300)
+    assert (h.n_src, h.n_dst) == (g.n_src, 300) and h.m == int((g.col < 300).sum())
+    for u in range(0, g.n_src, 7):
+        a = g.col[g.row_ptr[u]:g.row_ptr[u + 1]]
+        va = g.values[g.row_ptr[u]:g.row_ptr[u + 1]]
+        np.testing.assert_array_equal(h.col[h.row_ptr[u]:h.row_ptr[u + 1]], a[a < 300])
+        np.testing.assert_array_equal(h.values[h.row_ptr[u]:h.row_ptr[u + 1]], va[a < 300])
+    ht = graphs.column_prefix(graphs.make_graph("rmat", 5, scale=10, permute=True, values=True, transpose=True,
+                                                backend="torch"), 300).to_numpy()
+    np.testing.assert_array_equal(ht.row_ptr, h.row_ptr)
+    np.testing.assert_array_equal(ht.col, h.col)
+    np.testing.assert_array_equal(ht.values, h.values)
