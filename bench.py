@@ -259,7 +259,17 @@ def run_pcpm(args, world, rank, local):
     peak = float(pk.get("hbm_gbs", 6650.0))
     sb, gb = layout_bytes(info, op, args.wide, weighted_pr)
     kernels = {}
-    if op == "pagerank":
+    fused = op == "pagerank" and bool(getattr(pcpm.pcpm_get_info(h), "fused_iterations", 0))
+    if op == "pagerank" and fused:
+        # fused iteration: one kernel per iteration gathers, applies and scatters the
+        # next iteration's updates; its bytes = gather + scatter - 8n (SPR neither written nor re-read)
+        ph = pcpm.pcpm_get_phase_times(h)
+        it_ms = [float(ph[2 + t]) for t in range(iters - 1)]
+        kernels["scatter"] = {"ms": float(ph[1]), "bytes": sb, "note": "the first iteration's scatter only"}
+        kernels["gather_apply_scatter"] = {"ms": statistics.mean(it_ms), "bytes": gb + sb - 8 * n}
+        kernels["gather_apply"] = {"ms": float(ph[1 + iters]), "bytes": gb, "note": "last iteration (no scatter)"}
+        step_kernel_ms = float(np.sum(ph))
+    elif op == "pagerank":
         ph = pcpm.pcpm_get_phase_times(h)
         sc = [float(ph[1 + 2 * t]) for t in range(iters)]
         ga = [float(ph[2 + 2 * t]) for t in range(iters)]
@@ -275,16 +285,17 @@ def run_pcpm(args, world, rank, local):
     for k, v in kernels.items():
         v["gbs"] = v["bytes"] / (v["ms"] * 1e-3) / 1e9
         v["frac"] = v["gbs"] / peak
-    dom = "gather_apply" if op == "pagerank" else "gather"
-    iter_bytes = sb + gb
+    dom = ("gather_apply_scatter" if fused else "gather_apply") if op == "pagerank" else "gather"
+    iter_bytes = sb + gb - (8 * n if fused else 0)
     ms_iter = ms_per_step / iters
     hbm_gbs = iter_bytes / (ms_iter * 1e-3) / 1e9
     # the committed ncu capture is of the default build (compact, compressed, the
     # config's partition bits, default options); other variants report null
     default_variant = not (args.no_compress or args.wide or args.bits or args.opt)
-    traffic = ncu_traffic(key, dom) if default_variant else None
+    traffic = ncu_traffic(key, dom, strict=dom == "gather_apply_scatter") if default_variant else None
     sm_clk = float(peaks().get("sm_max_mhz", 1965.0))
-    smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk) if default_variant else None
+    smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk, strict=dom == "gather_apply_scatter") \
+        if default_variant else None
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GTEPS" if op == "pagerank" else "G-nnz/s",
@@ -618,14 +629,14 @@ def ncu_traffic(key, kernel, strict=False):
         return None
 
 
-def smem_roofline(key, kernel, ms, clk_mhz):
+def smem_roofline(key, kernel, ms, clk_mhz, strict=False):
     """Secondary ceiling of the gather: the shared-memory data pipe (one 128-byte
     wavefront per SM-cycle).  Wavefronts per launch come from the committed ncu capture,
     the time from this run's CUDA events; null when no capture exists for the config."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         dk = json.load(open(p))[key]
-        d = dk.get(kernel) or dk["gather_apply"]
+        d = dk[kernel] if strict else (dk.get(kernel) or dk["gather_apply"])
         wf = float(d["smem_wavefronts_per_launch"])
     except Exception:
         return None

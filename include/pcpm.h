@@ -93,6 +93,9 @@ typedef struct {
   int64_t gather_items, scatter_items;  /* work-list sizes of the two kernels */
   int32_t fixed_point_bits;   /* F of the last pcpm_pagerank / pcpm_spmv call */
   int32_t compact_slots;      /* 1: built with accumulator slots (PCPM_COMPACT_SLOTS applied) */
+  int32_t fused_iterations;   /* 1: the last pcpm_pagerank ran the fused iteration (each gather kernel also
+                                 scatters the next iteration's updates; phase times then read: init, the
+                                 first scatter, one entry per iteration) */
 } pcpm_info;
 
 /* Device pointers to the built layout, for bit-exact tests (read-only).

@@ -160,6 +160,11 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.inv_deg = h->inv_deg + h->shard_lo;  // apply: 1 / global out-degree of destination v (shards: lo + v)
   a.epi_pf = h->opt_epi_pf;
   a.pf_tiles = h->opt_gather_pf;
+  a.png16 = h->png16;
+  a.png_off = h->png_off;
+  a.upd_off = h->upd_off;
+  a.grp_at = h->grp_at;
+  a.k_dst = h->k_dst;
   return a;
 }
 
@@ -199,6 +204,13 @@ int enqueue_iteration(pcpm_handle* h, double d, int t, float* pr_new, cudaStream
   return mark(h, s);
 }
 
+// The fused iteration (gather + apply + the next iteration's scatter in one kernel, DESIGN.md
+// §5) applies to square, compact, single-GPU handles on the persistent gather path.
+bool fused_ok(const pcpm_handle* h) {
+  return h->opt_fuse && !h->wide && !h->shard && h->n_src == h->n_dst && h->k_src == h->k_dst && !h->slot16 &&
+         !(h->cl_cs >= 2 && h->opt_cluster_gather) && h->opt_gather_variant == 1 && h->e_prime > 0;
+}
+
 int enqueue_pagerank(pcpm_handle* h, double d, int iters, float* dst, cudaStream_t s) {
   int rc;
   const int fbits = pr_fixed_bits(h->n_src);
@@ -217,8 +229,36 @@ int enqueue_pagerank(pcpm_handle* h, double d, int iters, float* dst, cudaStream
     PCPM_CK(cudaMemcpyAsync(dst, h->pr[0], sizeof(float) * h->n_src, cudaMemcpyDeviceToDevice, s));
     return PCPM_OK;
   }
-  for (int t = 0; t < iters; ++t)
-    if ((rc = enqueue_iteration(h, d, t, (t == iters - 1) ? dst : h->pr[(t + 1) & 1], s))) return rc;
+  h->last_fused = fused_ok(h) && h->upd2 != nullptr && iters > 1;
+  if (!h->last_fused) {
+    for (int t = 0; t < iters; ++t)
+      if ((rc = enqueue_iteration(h, d, t, (t == iters - 1) ? dst : h->pr[(t + 1) & 1], s))) return rc;
+    return PCPM_OK;
+  }
+  // fused: scatter of SPR_0 (Alg. 4), then per iteration one kernel that gathers the bins of
+  // iteration t (buffer t & 1), applies, and scatters SPR_{t+1} into buffer (t + 1) & 1
+  float* bins[2] = {h->upd, h->upd2};
+  if ((rc = launch_scatter(h, h->spr, s, bins[0]))) return rc;
+  if ((rc = mark(h, s))) return rc;
+  for (int t = 0; t < iters; ++t) {
+    const bool fuse = t < iters - 1;
+    GatherArgs a = base_args(h, h->fixed_bits);
+    a.d = d;
+    a.n = (double)h->n_src;
+    a.red_in = h->red + 2 * t;
+    a.res_out = h->red + 2 * t + 1;
+    a.dang_out = h->red + 2 * t + 2;
+    a.pr_old = h->pr[t & 1];
+    a.pr_new = (t == iters - 1) ? dst : h->pr[(t + 1) & 1];
+    a.spr_new = h->spr;
+    a.upd = bins[t & 1];
+    a.upd_next = bins[(t + 1) & 1];
+    if (wpr) a.inv_deg = h->inv_wdeg;
+    if ((rc = launch_gather(h, a, wpr, true, s, false, fuse))) return rc;
+    // split partitions: k_apply_split wrote their SPR to global memory; scatter them now
+    if (fuse && h->n_sitems_split && (rc = launch_scatter(h, h->spr, s, bins[(t + 1) & 1], true))) return rc;
+    if ((rc = mark(h, s))) return rc;
+  }
   return PCPM_OK;
 }
 
@@ -300,6 +340,10 @@ int pagerank_common(pcpm_handle* h, double d, int iters, float* out, int kind) {
   }
   int rc = ensure_red(h, iters);
   if (rc) return rc;
+  if (kind == 0 && fused_ok(h) && !h->upd2 && iters > 1) {   // second update-bin buffer of the fused path
+    if ((rc = dev_alloc_t(h, &h->upd2, h->e_prime + 8))) return rc;
+    PCPM_CK(cudaMemsetAsync(h->upd2, 0, sizeof(float) * (h->e_prime + 8), h->stream));
+  }
   // refreshed on every call: a cached graph skips enqueue_pagerank, which also sets them
   h->fixed_bits = kind == 0 ? pr_fixed_bits(h->n_src) : 0;
   h->last_was_spmv = false;
@@ -754,6 +798,7 @@ int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
   i.scatter_items = h->n_sitems;
   i.fixed_point_bits = h->fixed_bits;
   i.compact_slots = h->slot16 ? 1 : 0;
+  i.fused_iterations = h->last_fused ? 1 : 0;
   if (h->last_was_spmv && h->xmax) {   // same rule as spmv_fbits() in gather.cu
     float xm = 0.f;
     if (cudaMemcpy(&xm, h->xmax, 4, cudaMemcpyDeviceToHost) == cudaSuccess) {
@@ -821,8 +866,9 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     return PCPM_OK;
   }
   if (!strcmp(key, "scatter_variant")) {
-    if (value < 0 || value > 1) {
-      set_error(PCPM_EINVAL, "scatter_variant must be 0 (TMA stream) or 1 (warp per group)");
+    if (value < 0 || value > 2) {
+      set_error(PCPM_EINVAL, "scatter_variant must be 0 (TMA stream), 1 (warp per group) or 2 (TMA stream, "
+                             "source values read through L1/L2)");
       return PCPM_EINVAL;
     }
     h->opt_scatter_variant = (int)value;
@@ -835,6 +881,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
       return PCPM_EINVAL;
     }
     h->opt_gather_variant = (int)value;
+    free_graph(h);
+    return PCPM_OK;
+  }
+  if (!strcmp(key, "fuse_scatter")) {
+    h->opt_fuse = value ? 1 : 0;
     free_graph(h);
     return PCPM_OK;
   }

@@ -771,8 +771,9 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   // cluster gather for few partitions: cs CTAs per bin (one tile-aligned slice each), cs = 2..8
   h->cl_cs = 0;
   if (k_dst >= 1 && 2 * k_dst <= h->num_sms && !getenv("PCPM_NO_CLUSTER_GATHER")) {
-    int cs = 1;
-    while (cs * 2 <= 8 && (int64_t)cs * 2 * k_dst <= h->num_sms) cs *= 2;
+    int cs = 1, cs_max = 8;
+    if (const char* e = getenv("PCPM_CLUSTER_MAX")) cs_max = std::max(2, std::min(8, atoi(e)));   // A/B
+    while (cs * 2 <= cs_max && (int64_t)cs * 2 * k_dst <= h->num_sms) cs *= 2;
     std::vector<GatherItem> gc;
     for (int64_t j = 0; j < k_dst; ++j) {
       const int64_t s0 = hbin[j], s1 = hbin[j + 1], per = ((s1 - s0 + cs - 1) / cs + kTileAlign - 1) / kTileAlign * kTileAlign;
@@ -809,6 +810,20 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
     if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
     if (!sb.empty())
       TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
+    // the fused iteration scatters a split partition after k_apply_split: its scatter items
+    h->n_sitems_split = 0;
+    if (!sb.empty() && k_src == k_dst && h->n_sitems > 0) {
+      std::vector<ScatterItem> si(h->n_sitems), ss;
+      TK(cudaMemcpyAsync(si.data(), h->sitems, sizeof(ScatterItem) * si.size(), cudaMemcpyDeviceToHost, s));
+      TK(cudaStreamSynchronize(s));
+      for (const ScatterItem& it : si)
+        if (it.p < (uint32_t)k_dst && nsl[it.p] > 1) ss.push_back(it);
+      if (!ss.empty()) {
+        if ((rc = dev_alloc_t(h, &h->sitems_split, ss.size()))) return rc;
+        TK(cudaMemcpyAsync(h->sitems_split, ss.data(), sizeof(ScatterItem) * ss.size(), cudaMemcpyHostToDevice, s));
+        h->n_sitems_split = (int)ss.size();
+      }
+    }
   }
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
@@ -1625,12 +1640,14 @@ struct TileSmem {           // carved from dynamic shared memory (k_dst-sized ar
   uint32_t* cr;             // [k_dst] run counts / running PNG slot
   uint16_t* bstart;         // [k_dst] first sorted index of bin j in the tile
   uint16_t* bfstart;        // [k_dst] flags before that index
-  uint16_t* key[2];         // [kTileE] bin j
-  uint32_t* pay[2];         // [kTileE] (v & (q-1)) | flag << 15 | (u & (q-1)) << 16; pay[1] doubles as the row marks
-  uint16_t* idx[2];         // [kTileE] tile position (weights)
+  // double buffers as named fields (a runtime-indexed pointer array would live in local
+  // memory and lose the shared address space: generic LD/ST on every access, measured)
+  uint16_t *key0, *key1;    // [kTileE] bin j
+  uint32_t *pay0, *pay1;    // [kTileE] (v & (q-1)) | flag << 15 | (u & (q-1)) << 16; pay1 doubles as the row marks
+  uint16_t *idx0, *idx1;    // [kTileE] tile position (weights)
   uint32_t* sbits;          // [kTileE / 32] row-start bits
   uint32_t* wsum;           // [kTileWarps * kRadixB + 64] scan scratch
-  uint32_t* colb[2];        // [kTileE + 8] the tile's columns (bulk-copied one tile ahead)
+  uint32_t *colb0, *colb1;  // [kTileE + 8] the tile's columns (bulk-copied one tile ahead)
 };
 
 size_t tile_smem_bytes(int64_t k_dst) {
@@ -1644,17 +1661,17 @@ __device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst) {
   TileSmem t;
   t.ci = reinterpret_cast<uint32_t*>(base);
   t.cr = t.ci + kd;
-  t.pay[0] = t.cr + kd;
-  t.pay[1] = t.pay[0] + kTileE;
-  t.sbits = t.pay[1] + kTileE;
+  t.pay0 = t.cr + kd;
+  t.pay1 = t.pay0 + kTileE;
+  t.sbits = t.pay1 + kTileE;
   t.wsum = t.sbits + kTileE / 32;
-  t.colb[0] = t.wsum + kTileWarps * kRadixB + 64;
-  t.colb[1] = t.colb[0] + kTileE + 8;
-  t.key[0] = reinterpret_cast<uint16_t*>(t.colb[1] + kTileE + 8);
-  t.key[1] = t.key[0] + kTileE;
-  t.idx[0] = t.key[1] + kTileE;
-  t.idx[1] = t.idx[0] + kTileE;
-  t.bstart = t.idx[1] + kTileE;
+  t.colb0 = t.wsum + kTileWarps * kRadixB + 64;
+  t.colb1 = t.colb0 + kTileE + 8;
+  t.key0 = reinterpret_cast<uint16_t*>(t.colb1 + kTileE + 8);
+  t.key1 = t.key0 + kTileE;
+  t.idx0 = t.key1 + kTileE;
+  t.idx1 = t.idx0 + kTileE;
+  t.bstart = t.idx1 + kTileE;
   t.bfstart = t.bstart + kd;
   return t;
 }
@@ -1679,7 +1696,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     const int64_t a = (x0 + 3) & ~int64_t(3), c = x1 & ~int64_t(3);
     if (bulk_ok && c > a) {
       mbar_arrive_expect_tx(&cbar[bsel], (uint32_t)((c - a) * 4));
-      bulk_g2s(T.colb[bsel] + (a - (x0 & ~int64_t(3))), col + a, (uint32_t)((c - a) * 4), &cbar[bsel],
+      bulk_g2s((bsel ? T.colb1 : T.colb0) + (a - (x0 & ~int64_t(3))), col + a, (uint32_t)((c - a) * 4), &cbar[bsel],
                policy_evict_first());
     } else {
       mbar_arrive(&cbar[bsel]);
@@ -1691,7 +1708,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     fence_mbar_init();
   }
   __syncthreads();
-  uint32_t cphase[2] = {0u, 0u};
+  uint32_t cphase = 0u;                 // bit b: parity of column buffer b
   const int lane = tid & 31, warp = tid >> 5;
   const uint32_t qmask = (1u << b) - 1u;
   uint32_t lt;
@@ -1739,10 +1756,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       // the previous tile, which every thread has finished)
       if (tid == 0 && x1 < e1) issue_cols(cb ^ 1, x1, min(e1, x1 + kTileE));
       // ---- prep: columns, row marks
-      uint32_t* mark = T.pay[1];
+      uint32_t* mark = T.pay1;
       for (int i = tid; i < kTileE; i += kTileThreads) mark[i] = 0u;
       for (int i = tid; i < kTileE / 32; i += kTileThreads) T.sbits[i] = 0u;
-      uint32_t* vfull = T.colb[cb] + (x0 & 3);   // vfull[i] = col[x0 + i]
+      uint32_t* vfull = (cb ? T.colb1 : T.colb0) + (x0 & 3);   // vfull[i] = col[x0 + i]
       {
         const int64_t a = (x0 + 3) & ~int64_t(3), c = x1 & ~int64_t(3);
         if (!bulk_ok || c <= a) {
@@ -1752,8 +1769,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
           if (tid >= 4 && tid - 4 < x1 - c) vfull[c - x0 + tid - 4] = __ldcs(col + c + tid - 4);   // tail (< 4)
         }
       }
-      mbar_wait(&cbar[cb], cphase[cb]);
-      cphase[cb] ^= 1u;
+      mbar_wait(&cbar[cb], (cphase >> cb) & 1u);
+      cphase ^= 1u << cb;
       __syncthreads();
       if (tid == 0) mark[0] = rcur + 1;   // edges before the first row start belong to rcur
       for (uint32_t rb = rnext;; rb += kTileThreads) {
@@ -1822,17 +1839,17 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
           uint32_t prj = i ? (prv >> b) : pj;
           if (i && prj >= (uint32_t)k_dst) prj = (uint32_t)k_dst - 1;
           const bool flag = !COMPRESS || first || prj != j;
-          T.key[0][i] = (uint16_t)j;
-          T.idx[0][i] = (uint16_t)i;
-          T.pay[0][i] = (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
+          T.key0[i] = (uint16_t)j;
+          T.idx0[i] = (uint16_t)i;
+          T.pay0[i] = (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
           if (!PLACE) {
             atomicAdd(&T.ci[j], 1u);
             if (flag) atomicAdd(&T.cr[j], 1u);
           }
         } else {
-          T.key[0][i] = 0xFFFFu;          // padding sorts last
-          T.idx[0][i] = 0;
-          T.pay[0][i] = 0u;
+          T.key0[i] = 0xFFFFu;          // padding sorts last
+          T.idx0[i] = 0;
+          T.pay0[i] = 0u;
         }
       }
       __syncthreads();
@@ -1856,9 +1873,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       // ---- stable LSD radix sort of the tile by bin (kbits bits, 4 per pass)
       int cur = 0;
       for (int sh = 0; sh < kbits; sh += kRadixBits) {
-        const uint16_t* kin = T.key[cur];
-        const uint32_t* pin = T.pay[cur];
-        const uint16_t* iin = T.idx[cur];
+        const uint16_t* kin = cur ? T.key1 : T.key0;
+        const uint32_t* pin = cur ? T.pay1 : T.pay0;
+        const uint16_t* iin = cur ? T.idx1 : T.idx0;
+        uint16_t* kout = cur ? T.key0 : T.key1;
+        uint32_t* pout = cur ? T.pay0 : T.pay1;
+        uint16_t* iout = cur ? T.idx0 : T.idx1;
         const int base = warp * (kTileE / kTileWarps);
         uint32_t rnk[kTileItems];
         uint32_t dig[kTileItems];
@@ -1912,18 +1932,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
         for (int k = 0; k < kTileItems; ++k) {
           const int src = base + 32 * k + lane;
           const uint32_t dst = T.wsum[dig[k] * kTileWarps + warp] + rnk[k];
-          T.key[nxt][dst] = kin[src];
-          T.pay[nxt][dst] = pin[src];
-          T.idx[nxt][dst] = iin[src];
+          kout[dst] = kin[src];
+          pout[dst] = pin[src];
+          iout[dst] = iin[src];
         }
         __syncthreads();
         cur = nxt;
       }
       // ---- positions: bin runs of the sorted tile, flag prefix
       {
-        const uint16_t* ks = T.key[cur];
-        const uint32_t* ps = T.pay[cur];
-        const uint16_t* is = T.idx[cur];
+        const uint16_t* ks = cur ? T.key1 : T.key0;
+        const uint32_t* ps = cur ? T.pay1 : T.pay0;
+        const uint16_t* is = cur ? T.idx1 : T.idx0;
         const int base = warp * (kTileE / kTileWarps);
         uint32_t fpre[kTileItems];
         uint32_t fw = 0;

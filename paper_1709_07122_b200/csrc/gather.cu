@@ -38,6 +38,7 @@
 //    (staged with the IDs) before the fixed-point add.
 //  * The decode is bound by the shared-memory pipe (one random ATOMS per ID,
 //    ~4.4 wavefronts per warp instruction), see DESIGN.md §6.
+#include <cstdlib>
 #include <type_traits>
 
 #include "pcpm_internal.cuh"
@@ -45,7 +46,8 @@
 namespace pcpm {
 namespace {
 
-constexpr uint32_t kFlagLast = 1u, kFlagEmpty = 2u, kFlagStop = 4u;
+constexpr uint32_t kFlagLast = 1u, kFlagEmpty = 2u, kFlagStop = 4u, kFlagScatter = 8u;
+constexpr int kFusePng = 8192;                // PNG entries per scatter stage of the fused kernel (16 KB)
 
 struct StageMeta {
   int item;
@@ -166,10 +168,11 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
 
 // Warp 0 of a gather CTA: claims work items and streams their tiles (IDs, update
 // window, decode anchors, weights) into the ring of S stages with bulk async copies.
-template <typename C, typename IdT, bool W, bool PR, bool SL>
+template <typename C, typename IdT, bool W, bool PR, bool SL, bool FUSE = false>
 __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* ids, uint8_t* stage_base,
                                                 StageMeta* meta, uint64_t* full, uint64_t* empty, int lane) {
   constexpr int S = C::kStages;
+  static_assert(!FUSE || C::kStageBytes >= kFusePng * 2 + 256, "a scatter stage fits in a ring stage");
   // ================= producer (whole warp; lane 0 issues) =================
   // The window of tile t is fixed by two decode anchors (chunk_base at the
   // tile's ends).  Lanes load the anchors of 32 tiles at once, so the issue
@@ -296,9 +299,97 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
         push_meta(m);
       }
     }
+    if constexpr (FUSE) {
+      // the next iteration's scatter of source partition p = j (Alg. 4): its PNG entries
+      // [png_off[p][0], png_off[p][k]) in stages of kFusePng, each with the grp_at anchors
+      // of its 256-entry chunks; every group's last scatter stage is flagged Last.  Slices
+      // of split bins are scattered after k_apply_split instead (no stages here).
+      if (a.bin_nslices[item.j] == 1) {
+        const uint32_t p = item.j;
+        const uint32_t s0 = __ldg(a.png_off + (int64_t)p * (a.k_dst + 1));
+        const uint32_t s1 = __ldg(a.png_off + (int64_t)p * (a.k_dst + 1) + a.k_dst);
+        const uint32_t base0 = s0 & ~(uint32_t)(kPngChunk - 1);
+        const uint32_t nst = s1 > s0 ? (s1 - base0 + kFusePng - 1) / kFusePng : 0u;
+        for (uint32_t c = 0; c < nst; ++c) {
+          if (lane == 0) {
+            const uint32_t base = base0 + c * kFusePng;
+            mbar_wait(&empty[stage], phase ^ 1);
+            StageMeta m{};
+            m.item = (int)it;
+            m.j = p;
+            m.lo = max(base, s0);
+            m.hi = min(base + (uint32_t)kFusePng, s1);
+            m.tile_base = base;
+            const uint32_t c0 = base / kPngChunk, ca = c0 & ~3u;
+            const uint32_t nga = ((((m.hi - base) + kPngChunk - 1) / kPngChunk) + (c0 - ca) + 3) & ~3u;
+            m.win_base = c0 - ca;                  // grp_at of the stage's chunk 0 at word win_base
+            m.flags = kFlagScatter | ((c + 2 >= nst + (nst > 1 ? 0u : 1u)) ? kFlagLast : 0u);
+            meta[stage] = m;
+            uint8_t* sb = stage_base + stage * C::kStageBytes;
+            const uint32_t bytes = (((m.hi - base) * 2u) + 15u) & ~15u;    // png16 is padded
+            mbar_arrive_expect_tx(&full[stage], bytes + nga * 4);
+            bulk_g2s(sb, a.png16 + base, bytes, &full[stage], pol);
+            bulk_g2s(sb + 2 * kFusePng, a.grp_at + ca, nga * 4, &full[stage], pol);   // grp_at padded
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        for (uint32_t c = nst; c < 2; ++c) {      // empty PNG or a single stage: Last for the other group(s)
+          StageMeta m{};
+          m.item = (int)it;
+          m.j = p;
+          m.flags = kFlagScatter | kFlagLast | kFlagEmpty;
+          push_meta(m);
+        }
+      }
+    }
     it = it_next;
     item = item_next;
   }
+}
+
+// Fused scatter: one PNG stage of source partition p (Alg. 4) by one consumer warp of its
+// group: sub-ranges gw, gw + gsz, ... of 256 entries (plus its turn of the rotating
+// remainder); upd_next[upd_off[p][j] + t] = xs[u] with the partition's SPR values xs in
+// shared memory.  Offsets are read through L1 on group crossings.  Out of line so the
+// decode loop's register allocation is not disturbed.
+__device__ __noinline__ void fused_scatter_stage(const GatherArgs& a, const StageMeta& m, const uint8_t* sb,
+                                                 const float* xs, int gw, int gsz, int& rot, int lane) {
+  const uint16_t* ps = reinterpret_cast<const uint16_t*>(sb);
+  const uint32_t* gs = reinterpret_cast<const uint32_t*>(sb + 2 * kFusePng) + m.win_base;
+  const uint32_t p = m.j;
+  const uint32_t* offs = a.png_off + (int64_t)p * (a.k_dst + 1);
+  const uint32_t* uos = a.upd_off + (int64_t)p * a.k_dst;
+  const uint32_t gbase = p * (uint32_t)a.k_dst;
+  auto range = [&](const int sr) {
+    const uint32_t wb = m.tile_base + (uint32_t)(sr * kPngChunk);
+    const uint32_t wlo = max(wb, m.lo), whi = min(wb + (uint32_t)kPngChunk, m.hi);
+    if (wlo >= whi) return;
+    const int32_t ga = (int32_t)(gs[sr] - gbase);
+    uint32_t g = ga > 0 ? (uint32_t)ga : 0u;
+    uint32_t gend = __ldg(offs + g + 1);
+    uint32_t delta = __ldg(uos + g) - __ldg(offs + g);
+#pragma unroll 4
+    for (uint32_t e = wlo + lane; e < whi; e += 32) {
+      if (e >= gend) {
+        do {
+          ++g;
+          gend = __ldg(offs + g + 1);
+        } while (e >= gend);
+        delta = __ldg(uos + g) - __ldg(offs + g);
+      }
+      a.upd_next[e + delta] = xs[ps[e - m.tile_base]];
+    }
+  };
+  constexpr int kNsr = kFusePng / kPngChunk;
+  const int nmain = (kNsr / gsz) * gsz;
+  for (int sr = gw; sr < nmain; sr += gsz) range(sr);
+  int who = rot;
+  for (int sr = nmain; sr < kNsr; ++sr) {
+    if (gw == who) range(sr);
+    who = (who + 1 == gsz) ? 0 : who + 1;
+  }
+  rot = who;
 }
 
 // Decode of one full stage by one consumer warp (Alg. 5): the
@@ -431,7 +522,11 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
 // MULTI (PageRank shards with a fused exchange, pcpm_shard_step_peers): the apply
 // also stores each SPR group to a.spr_peer[0 .. n_peer) -- other ranks' buffers,
 // NVLink P2P -- and the kernel ends with a system-scope fence.
-template <typename IdT, bool W, bool PR, bool MULTI = false, bool SL = false>
+// FUSE (PageRank, DESIGN.md §5 "fused iteration"): after the apply of destination
+// partition j the SPR values stay in the accumulator's shared memory and the CTA scatters
+// source partition j of the next iteration from them (kFlagScatter stages); SPR is not
+// written to global memory.
+template <typename IdT, bool W, bool PR, bool MULTI = false, bool SL = false, bool FUSE = false>
 __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const GatherArgs a) {
   using C = Cfg<IdT, W, SL>;
   constexpr int S = C::kStages;
@@ -462,7 +557,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   __syncthreads();
 
   if (warp == 0) {
-    gather_producer<C, IdT, W, PR, SL>(a, ids, stage_base, meta, full, empty, lane);
+    gather_producer<C, IdT, W, PR, SL, FUSE>(a, ids, stage_base, meta, full, empty, lane);
     return;
   }
 
@@ -492,6 +587,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   const uint32_t lemask = lanemask_le();
 
   int stage = grp, rot = 0;
+  int srot = 0;                                     // FUSE: rotation of the scatter stages' remainder
   uint32_t phase = 0;
   unsigned long long pt[4] = {0, 0, 0, 0};
   long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
@@ -500,6 +596,22 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
     if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[0] += t - tc; tc = t; }
     const StageMeta m = meta[stage];
     if (m.flags & kFlagStop) break;
+    if (FUSE && (m.flags & kFlagScatter)) {
+      // next iteration's scatter of source partition m.j from the SPR values in acc
+      if (!(m.flags & kFlagEmpty))
+        fused_scatter_stage(a, m, stage_base + stage * C::kStageBytes, reinterpret_cast<const float*>(acc), gw, gsz,
+                            srot, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      stage += 2;
+      if (stage >= S) { stage -= S; phase ^= 1; }
+      if (m.flags & kFlagLast) {
+        named_bar_sync(1, kCons);                   // both groups are done reading the SPR values
+        for (int64_t i = ctid; i < q; i += kCons) acc[i] = 0u;
+        named_bar_sync(1, kCons);
+      }
+      continue;
+    }
     const uint32_t v0 = m.j << a.b;
     if (!(m.flags & kFlagEmpty))
       decode_stage<C, IdT, W, PR>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
@@ -664,7 +776,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
                 res += red_fx(fabs(prn - (double)pov[c]));
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
-              sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
+              if (FUSE && nsl == 1)                     // the next scatter's source values stay on chip
+                *reinterpret_cast<uint4*>(acc + 4 * i4) =
+                    make_uint4(__float_as_uint(sp[0]), __float_as_uint(sp[1]), __float_as_uint(sp[2]),
+                               __float_as_uint(sp[3]));
+              else
+                sp4[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
               if constexpr (MULTI)
                 for (int r = 0; r < a.n_peer; ++r)
                   reinterpret_cast<float4*>(a.spr_peer[r] + v0)[i4] = make_float4(sp[0], sp[1], sp[2], sp[3]);
@@ -675,7 +792,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
               const double prn = base_pr + a.d * ((double)(long long)total(i) * inv_scale);
               a.pr_new[v] = (float)prn;
               const float idg = __ldg(a.inv_deg + v);
-              a.spr_new[v] = (float)prn * idg * fscale;
+              if (FUSE && nsl == 1) acc[i] = __float_as_uint((float)prn * idg * fscale);
+              else a.spr_new[v] = (float)prn * idg * fscale;
               if constexpr (MULTI)
                 for (int r = 0; r < a.n_peer; ++r) a.spr_peer[r][v] = (float)prn * idg * fscale;
               if (idg == 0.0f) dang += red_fx(prn);
@@ -1413,6 +1531,10 @@ GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false, 
                   : (pagerank ? k_gather<uint16_t, false, true> : k_gather<uint16_t, false, false>);
 }
 
+GatherFn gather_fuse_fn(bool weighted) {       // compact PageRank with the next scatter fused in
+  return weighted ? k_gather<uint16_t, true, true, false, false, true> : k_gather<uint16_t, false, true, false, false, true>;
+}
+
 GatherFn gather2_fn(bool wide, bool weighted, bool pagerank, bool multi) {
   if (multi) return wide ? k_gather2<uint32_t, false, true, true> : k_gather2<uint16_t, false, true, true>;
   if (wide)
@@ -1478,6 +1600,8 @@ int prepare_gather(pcpm_handle* h) {
     for (int w = 0; w < 2; ++w)
       for (int p = 0; p < 2; ++p)
         PCPM_CK(cudaFuncSetAttribute(gather_cl_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  for (int w = 0; w < 2; ++w)
+    PCPM_CK(cudaFuncSetAttribute(gather_fuse_fn(w), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   return PCPM_OK;
 }
 
@@ -1550,13 +1674,28 @@ int launch_gather_cl(pcpm_handle* h, const GatherArgs& a0, bool weighted, bool p
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (getenv("PCPM_DEBUG_CLUSTER")) {          // how many clusters fit at once (A/B diagnostics)
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, (const void*)gather_cl_fn(h->wide, weighted, pagerank), &cfg);
+    cudaGetLastError();
+    fprintf(stderr, "[pcpm] cluster gather: %d clusters of %d CTAs, %d can be resident at once\n",
+            (int)h->k_dst, h->cl_cs, ncl);
+  }
   PCPM_CK(cudaLaunchKernelEx(&cfg, gather_cl_fn(h->wide, weighted, pagerank), a));
   h->launches += 1;
   return PCPM_OK;
 }
 
-int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi) {
+int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s, bool multi,
+                  bool fuse) {
   const bool slots = a.slot16 != nullptr && !weighted && !multi;
+  if (fuse) {                                      // PageRank iteration with the next scatter fused in
+    const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
+    gather_fuse_fn(weighted)<<<grid, gather_threads(false, weighted), gather_smem_bytes(a.b, false, weighted), s>>>(a);
+    PCPM_CK(cudaGetLastError());
+    h->launches += 1;
+    return launch_apply_split(h, a, pagerank, s);
+  }
   if (h->cl_cs >= 2 && h->opt_cluster_gather && !slots && !multi) return launch_gather_cl(h, a, weighted, pagerank, s);
   if (!slots && h->opt_gather_variant == 2) {
     const int grid = std::min(h->num_sms, std::max(a.n_items, 1));

@@ -97,6 +97,9 @@ struct pcpm_handle {
   int64_t n_wdangling = 0;          // #{u : W(u) = 0}
   int neg_weights = 0;              // some weight < 0 (SpMV only)
   float* upd = nullptr;             // [E' + 8]
+  float* upd2 = nullptr;            // [E' + 8] second update-bin buffer of the fused iteration (lazy)
+  pcpm::ScatterItem* sitems_split = nullptr;  // scatter items of the source partitions whose bin is split
+  int n_sitems_split = 0;
   int wexp = 0;                     // max|w| <= 2^wexp (SpMV fixed-point scale)
   float* xmax = nullptr;            // [1] device max|x| of the last pcpm_spmv
   bool last_was_spmv = false;
@@ -136,7 +139,9 @@ struct pcpm_handle {
   // options (pcpm_set_option)
   int opt_use_graph = 1;
   int opt_gather_variant = 1;
-  int opt_cluster_gather = 1;       // 1: k_gather_cl for graphs with few partitions (when built), 0: off       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
+  int opt_cluster_gather = 1;       // 1: k_gather_cl for graphs with few partitions (when built), 0: off
+  int opt_fuse = 0;                 // 1: gather + next scatter fused (PageRank, compact, square, not shard; measured slower), 0: off
+  bool last_fused = false;          // the last pcpm_pagerank ran the fused iteration       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
   int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
   int opt_epi_pf = 4;               // gather: L2 prefetch of the apply's vertex arrays, tiles before the item's end (0 = off)
   int opt_scatter_variant = 0;      // 0: TMA-staged PNG stream (k_scatter_tma), 1: warp per group
@@ -310,6 +315,15 @@ struct GatherArgs {
   int wexp;                // max|w| <= 2^wexp
   int pf_tiles;            // L2 prefetch distance of the gather producer, in tiles
   int static_items;        // 1: CTA b processes items[b] only (the cluster gather), 0: claim from counters[0]
+  // fused scatter (FUSE instantiations, DESIGN.md §5 "fused iteration"): after applying
+  // destination partition j, the CTA scatters source partition p = j of the NEXT iteration
+  // (Alg. 4) from the SPR values it just computed, into the other update-bin buffer
+  float* upd_next;
+  const uint16_t* png16;
+  const uint32_t* png_off;
+  const uint32_t* upd_off;
+  const uint32_t* grp_at;
+  int64_t k_dst;
   int epi_pf;              // prefetch inv_deg / pr_old of the item's partition this many tiles before its end
   // fused exchange (pcpm_shard_step_peers): SPR_{t+1} of the slice is also stored to
   // these (peer) buffers, indexed like spr_new
@@ -319,11 +333,13 @@ struct GatherArgs {
 __device__ int spmv_fbits(float xmax, int wexp);
 int launch_absmax(pcpm_handle* h, const float* x, int64_t n, float* out, cudaStream_t s);
 int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pagerank, cudaStream_t s,
-                  bool multi = false);
+                  bool multi = false, bool fuse = false);
 int gather_smem_bytes(int b, bool wide, bool weighted);
 bool gather_slots_fit(int b, int acc_words);   // the 6-stage slot kernel fits in shared memory
 
-int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s);
+// x: the source vector; out: the update bins to write (nullptr = h->upd); split_only: only
+// the items of source partitions whose destination bin is split (the fused iteration's rest)
+int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out = nullptr, bool split_only = false);
 int read_debug_counters(unsigned long long* out, int cap, bool reset);
 int prepare_gather(pcpm_handle* h);
 int prepare_scatter(pcpm_handle* h);

@@ -82,7 +82,11 @@ struct ScatterArgs {
   int pf_stages;         // L2 prefetch distance in stages
 };
 
-template <typename SrcT>
+// XG (scatter_variant 2, the "SPR through L1/L2" A/B of DESIGN.md §6): the source values
+// are read with ld.global.nc instead of a 128 KB shared-memory copy of the partition's
+// slice per item -- for graphs whose vector is L2-resident and whose items are many
+// per source partition (small k), the staging is mostly redundant traffic.
+template <typename SrcT, bool XG = false>
 __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const ScatterArgs a) {
   constexpr int kScW = ScCfg<SrcT>::kW;
   constexpr int kChunk = kScStageBytes / (int)sizeof(SrcT);   // PNG entries per stage
@@ -200,8 +204,8 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
         im.off_shift = (uint32_t)(orow - oal);
         im.uo_shift = (uint32_t)(urow - ual);
         *imeta = im;
-        mbar_arrive_expect_tx(ifull, xbytes + obytes + ubytes);
-        bulk_g2s(xs, a.x + xbase, xbytes, ifull, pol_keep);
+        mbar_arrive_expect_tx(ifull, (XG ? 0u : xbytes) + obytes + ubytes);
+        if (!XG) bulk_g2s(xs, a.x + xbase, xbytes, ifull, pol_keep);
         bulk_g2s(off_s, a.png_off + oal, obytes, ifull, pol_keep);
         bulk_g2s(uo_s, a.upd_off + ual, ubytes, ifull, pol_keep);
         for (; cb < s1; cb += kChunk) issue(cb);
@@ -222,6 +226,7 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
       const uint32_t* offs = off_s + im.off_shift;    // offs[g] = png_off[p][j0 + g], g in [0, ng]
       const uint32_t* uos = uo_s + im.uo_shift;       // uos[g] = upd_off[p][j0 + g]
       const uint32_t ubase = sizeof(SrcT) == 2 ? 0u : (im.p << a.b);   // wide sources are global IDs
+      const float* xg = a.x + ((int64_t)im.p << a.b);                   // XG: the slice in global memory
       for (;;) {
         mbar_wait(&full[stage], phase);
         const ScStageMeta sm = smeta[stage];
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
               delta = uos[g] - offs[g];
             }
             const uint32_t u = (uint32_t)ps[e - sm.base] - ubase;
-            a.upd[e + delta] = xs[u];
+            a.upd[e + delta] = XG ? __ldg(xg + u) : xs[u];
           }
         }
         };
@@ -358,6 +363,10 @@ int prepare_scatter(pcpm_handle* h) {
                                scatter_tma_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                scatter_warp_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -365,19 +374,22 @@ int prepare_scatter(pcpm_handle* h) {
   return PCPM_OK;
 }
 
-int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
-  if (h->n_sitems == 0) return PCPM_OK;
-  const int grid = std::min(h->n_sitems, h->num_sms);
+int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out, bool split_only) {
+  const ScatterItem* items = split_only ? h->sitems_split : h->sitems;
+  const int n_items = split_only ? h->n_sitems_split : h->n_sitems;
+  float* upd = out ? out : h->upd;
+  if (n_items == 0) return PCPM_OK;
+  const int grid = std::min(n_items, h->num_sms);
   if (h->opt_scatter_variant == 1 || h->b < 2) {   // the bulk-copy variant needs 16 B aligned slices
     const int smem = scatter_warp_smem_bytes(h->b);
     if (h->wide)
-      k_scatter_warp<uint32_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b,
+      k_scatter_warp<uint32_t><<<grid, kScatterThreads, smem, s>>>(items, n_items, x, h->n_src, h->b,
                                                                    h->k_dst, h->png_src, h->png_off, h->upd_off,
-                                                                   h->upd);
+                                                                   upd);
     else
-      k_scatter_warp<uint16_t><<<grid, kScatterThreads, smem, s>>>(h->sitems, h->n_sitems, x, h->n_src, h->b,
+      k_scatter_warp<uint16_t><<<grid, kScatterThreads, smem, s>>>(items, n_items, x, h->n_src, h->b,
                                                                    h->k_dst, h->png16, h->png_off, h->upd_off,
-                                                                   h->upd);
+                                                                   upd);
   } else {
     // the bulk copy of a source slice reads whole 16 B words: x must be 16 B aligned
     // and readable up to round16(n_src); internal vectors are padded, user vectors
@@ -388,8 +400,8 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
       x = h->xbuf;
     }
     ScatterArgs a{};
-    a.items = h->sitems;
-    a.n_items = h->n_sitems;
+    a.items = items;
+    a.n_items = n_items;
     a.x = x;
     a.n_src = h->n_src;
     a.b = h->b;
@@ -398,14 +410,15 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
     a.png_off = h->png_off;
     a.upd_off = h->upd_off;
     a.grp_at = h->grp_at;
-    a.upd = h->upd;
+    a.upd = upd;
     a.counters = h->counters;
     a.pf_stages = h->opt_scatter_pf;
     const int smem = scatter_tma_smem_bytes(h->b);
+    const bool xg = h->opt_scatter_variant == 2;
     if (h->wide)
-      k_scatter_tma<uint32_t><<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
+      (xg ? k_scatter_tma<uint32_t, true> : k_scatter_tma<uint32_t>)<<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
     else
-      k_scatter_tma<uint16_t><<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
+      (xg ? k_scatter_tma<uint16_t, true> : k_scatter_tma<uint16_t>)<<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
   }
   PCPM_CK(cudaGetLastError());
   h->launches += 1;

@@ -55,7 +55,8 @@ class pcpm_info(ctypes.Structure):
                 ("n_dangling", ctypes.c_int64), ("weighted", ctypes.c_int32), ("compressed", ctypes.c_int32),
                 ("device_bytes", ctypes.c_int64), ("build_ms", ctypes.c_double),
                 ("gather_items", ctypes.c_int64), ("scatter_items", ctypes.c_int64),
-                ("fixed_point_bits", ctypes.c_int32), ("compact_slots", ctypes.c_int32)]
+                ("fixed_point_bits", ctypes.c_int32), ("compact_slots", ctypes.c_int32),
+                ("fused_iterations", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -362,7 +362,7 @@ def test_spmv_non_square(pcpm):
         pcpm.pcpm_destroy(h)
 
 
-@pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
+@pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_variant": 2}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
                                   {"cluster_gather": 0}, {"gather_variant": 2},
                                   {"epilogue_prefetch": 0}, {"gather_prefetch": 8, "epilogue_prefetch": 16},
                                   {"use_graph": 0}],
@@ -673,3 +673,38 @@ def test_job_runtime_matches_oracle_and_single_calls(pcpm):
         np.testing.assert_array_equal(out, outs[1])
     finally:
         pcpm.pcpm_runtime_destroy(rt)
+
+
+FUSE_CASES = [
+    ("rmat14_b6", lambda: graphs.make_graph("rmat", 12, scale=14, permute=True), 6, False),
+    ("rmat15_unpermuted_b7", lambda: graphs.make_graph("rmat", 13, scale=15, permute=False), 7, False),  # hub bins: split
+    ("er_ragged_b9", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 9, False),
+    ("rmat14_weighted_b6", lambda: weighted(graphs.make_graph("rmat", 12, scale=14, permute=True), 4), 6, True),
+]
+
+
+@pytest.mark.parametrize("name,mk,b,wpr", FUSE_CASES, ids=[c[0] for c in FUSE_CASES])
+def test_fused_iteration_matches_unfused_and_oracle(pcpm, name, mk, b, wpr):
+    """The fused iteration (each gather kernel also scatters the next iteration's updates from the
+    SPR values it keeps on chip; split partitions scattered after k_apply_split) computes the
+    same PageRank, bit for bit, as separate scatter and gather kernels, and matches the oracle."""
+    g = mk()
+    h = build(pcpm, g, b)
+    try:
+        if wpr:
+            pcpm.pcpm_set_option(h, "weighted_pagerank", 1)
+        outs = {}
+        for fuse in (1, 0):                       # the fused iteration is opt-in (measured slower)
+            pcpm.pcpm_set_option(h, "fuse_scatter", fuse)
+            out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, 9, out)
+            torch.cuda.synchronize()
+            assert pcpm.pcpm_get_info(h).fused_iterations == fuse
+            outs[fuse] = (out.cpu().numpy(), pcpm.pcpm_get_residuals(h))
+        np.testing.assert_array_equal(outs[1][0].view(np.uint32), outs[0][0].view(np.uint32))
+        np.testing.assert_array_equal(outs[1][1], outs[0][1])
+        ref = (oracle.pagerank_weighted(g.n_src, g.row_ptr, g.col, g.values, 0.85, 9) if wpr
+               else oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 9))
+        pr_check(outs[1][0], ref, name)
+    finally:
+        pcpm.pcpm_destroy(h)
