@@ -292,7 +292,11 @@ def run_pcpm(args, world, rank, local):
     # the committed ncu capture is of the default build (compact, compressed, the
     # config's partition bits, default options); other variants report null
     default_variant = not (args.no_compress or args.wide or args.bits or args.opt)
-    traffic = ncu_traffic(key, dom, strict=dom == "gather_apply_scatter") if default_variant else None
+    # the uncompressed layout has its own committed capture (key "<cfg>_nocompress")
+    nocomp_only = args.no_compress and not (args.wide or args.bits or args.opt)
+    tkey = key + "_nocompress" if nocomp_only else key
+    traffic = ncu_traffic(tkey, dom, strict=dom == "gather_apply_scatter") if (default_variant or nocomp_only) \
+        else None
     sm_clk = float(peaks().get("sm_max_mhz", 1965.0))
     smem = smem_roofline(key, dom, kernels[dom]["ms"], sm_clk, strict=dom == "gather_apply_scatter") \
         if default_variant else None
@@ -335,6 +339,12 @@ def run_pcpm(args, world, rank, local):
             "paper_eq5_uncompressed_r1": round(model.pcpm_comm(n, m, info.k_dst, 1.0)),
             "paper_eq4_bvgas": round(model.bvgas_comm(n, m)),
         },
+        "measured_dram_bytes_per_iter": (lambda a, b_: None if a is None or b_ is None else {
+            "scatter": a, "gather": b_, "total": a + b_,
+            "vs_model": "paper_eq4_bvgas" if args.no_compress else "paper_eq5_pcpm_d_i_2",
+            "source": "committed ncu --set full capture (profiles/ncu_traffic.json)"})(
+                ncu_traffic(tkey, "scatter", strict=True) if (default_variant or nocomp_only) else None,
+                ncu_traffic(tkey, "gather_apply", strict=True) if (default_variant or nocomp_only) else None),
         "options": args.opt, "compact_slots": int(info.compact_slots) if hasattr(info, "compact_slots") else 0,
         "clocks": clk,
         "gpu_launches": int(launches),

@@ -261,7 +261,7 @@ int pcpm_get_residuals(pcpm_handle* h, double* host, int cap);
  * update bins (exported as pcpm_layout_view.upd); for bit-exact tests. */
 int pcpm_scatter(pcpm_handle* h, const float* x);
 /* Select a kernel variant for A/B experiments.
- * Keys: "phase_timing", "use_graph", "scatter_variant" (0|1), "gather_variant" (1: the
+ * Keys: "phase_timing", "use_graph", "scatter_variant" (0|1|2|3: 3 = 16-byte vector stores of update quads), "gather_variant" (1: the
  * gather applies each finished partition itself, the default; 2: k_gather2, which parks
  * the partition's accumulator in tensor memory and lets 4 dedicated warps apply it
  * while 27 warps decode the next one -- measured slower), "scatter_lpt",

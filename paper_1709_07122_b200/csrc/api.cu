@@ -866,9 +866,9 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     return PCPM_OK;
   }
   if (!strcmp(key, "scatter_variant")) {
-    if (value < 0 || value > 2) {
-      set_error(PCPM_EINVAL, "scatter_variant must be 0 (TMA stream), 1 (warp per group) or 2 (TMA stream, "
-                             "source values read through L1/L2)");
+    if (value < 0 || value > 3) {
+      set_error(PCPM_EINVAL, "scatter_variant must be 0 (TMA stream), 1 (warp per group), 2 (TMA stream, "
+                             "source values read through L1/L2) or 3 (TMA stream, 16-byte stores)");
       return PCPM_EINVAL;
     }
     h->opt_scatter_variant = (int)value;

@@ -1676,13 +1676,24 @@ __device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst) {
   return t;
 }
 
-template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED>
+// BUCKET (with PLACE; the two-level placement for k_dst > kBucketMinK): instead of the
+// tile sort by bin, each edge's record ((j & 31) << 32 | payload) goes to the scratch
+// sub-range of its segment and bucket h = j >> 5 (SB[s][h], stable: tiles in CSR order,
+// ranks by (warp, step, lane)); k_bucket_place then places each (segment, bucket).
+struct BucketArgs {
+  const uint32_t* SB;       // [n_seg][nbk + 1] scratch start of (s, h); [s][nbk] = the segment's end
+  int nbk;                  // buckets = ceil(k_dst / 32)
+  uint64_t* rec;            // [m] records
+  float* recw;              // [m] weights (WEIGHTED)
+};
+
+template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED, bool BUCKET = false>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
     const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst, int kbits,
     uint32_t* CI, uint32_t* CR, const uint32_t* __restrict__ G, uint32_t* outdeg, float* inv_deg,
     unsigned long long* n_dang, uint32_t* err, uint16_t* ids16, uint32_t* ids32, float* w, uint16_t* png16,
-    uint32_t* png32) {
+    uint32_t* png32, const BucketArgs ba) {
   extern __shared__ __align__(16) uint8_t tsm[];
   const TileSmem T = tile_carve(tsm, k_dst);
   const int tid = threadIdx.x;
@@ -1720,7 +1731,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     const uint32_t sidx = seg_s;
     if (sidx >= (uint32_t)n_seg) break;
     const BSeg sg = segs[sidx];
-    for (int64_t j = tid; j < k_dst; j += kTileThreads) {
+    if (BUCKET) {
+      for (int h = tid; h < ba.nbk; h += kTileThreads) T.ci[h] = ba.SB[(int64_t)sidx * (ba.nbk + 1) + h];
+    }
+    for (int64_t j = tid; !BUCKET && j < k_dst; j += kTileThreads) {
       if (PLACE) {
         T.ci[j] = CI[(int64_t)sidx * k_dst + j];
         T.cr[j] = CR[(int64_t)sidx * k_dst + j] + G[(int64_t)sg.p * k_dst + j];
@@ -1866,6 +1880,73 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       pj = T.wsum[kTileWarps * kRadixB + 1];
       rcur = T.wsum[kTileWarps * kRadixB + 2];
       if (!PLACE) {
+        __syncthreads();
+        continue;
+      }
+      if constexpr (BUCKET) {
+        // ---- stable counting placement of the tile's records by bucket h = j >> 5 (< 64):
+        // per warp (its 512 elements: steps k, lanes) ranks from 6 ballots of the bucket
+        // bits and per-warp counts in registers (lane l counts buckets l and l + 32); then
+        // per-bucket bases over the warps (earlier warps = earlier elements); records go to
+        // SB's running slot + base + rank.
+        constexpr int kWs = 65;                       // padded stride of the per-warp totals
+        uint32_t* wc = T.pay1;                        // [kTileWarps][kWs] (the row marks are consumed)
+        const int base = warp * (kTileE / kTileWarps);
+        uint32_t rk[kTileItems];
+        uint32_t c_lo = 0, c_hi = 0;
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const int i = base + 32 * k + lane;
+          const bool ok = i < n;
+          const uint32_t hb = ok ? (uint32_t)(T.key0[i] >> 5) : 0u;
+          const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+          uint32_t mb = vm;                           // lanes whose bucket is `lane` or `lane` + 32
+#pragma unroll
+          for (int t = 0; t < 5; ++t)
+            mb &= __ballot_sync(0xffffffffu, (hb >> t) & 1u) ^ (((lane >> t) & 1) ? 0u : 0xFFFFFFFFu);
+          const uint32_t b5 = __ballot_sync(0xffffffffu, (hb >> 5) & 1u);
+          const uint32_t pm = __shfl_sync(0xffffffffu, mb, hb & 31u) & ((hb & 32u) ? b5 : ~b5);
+          const uint32_t bl = __shfl_sync(0xffffffffu, c_lo, hb & 31u), bh = __shfl_sync(0xffffffffu, c_hi, hb & 31u);
+          rk[k] = ((hb & 32u) ? bh : bl) + __popc(pm & lt);
+          c_lo += __popc(mb & ~b5);
+          c_hi += __popc(mb & b5);
+        }
+        wc[warp * kWs + lane] = c_lo;
+        wc[warp * kWs + 32 + lane] = c_hi;
+        __syncthreads();
+        {
+          // bucket 4 w + 2 r + (lane >> 4), r = 0, 1: exclusive scan over the 16 warps (lane & 15)
+          static_assert(kTileWarps == 16, "two buckets per 32-lane scan");
+          const int l16 = lane & 15;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int hh = 4 * warp + 2 * r + (lane >> 4);
+            const uint32_t a = hh < ba.nbk ? wc[l16 * kWs + hh] : 0u;
+            uint32_t ia = a;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, ia, o, 16);
+              if (l16 >= o) ia += y;
+            }
+            const uint32_t bb = hh < ba.nbk ? T.ci[hh] : 0u;
+            __syncwarp();
+            if (hh < ba.nbk) {
+              wc[l16 * kWs + hh] = bb + ia - a;
+              if (l16 == 15) T.ci[hh] = bb + ia;
+            }
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kTileItems; ++k) {
+          const int i = base + 32 * k + lane;
+          if (i < n) {
+            const uint32_t j = T.key0[i];
+            const uint32_t pos = wc[warp * kWs + (j >> 5)] + rk[k];
+            ba.rec[pos] = ((uint64_t)(j & 31u) << 32) | T.pay0[i];
+            if (WEIGHTED) ba.recw[pos] = val[x0 + i];
+          }
+        }
         __syncthreads();
         continue;
       }
@@ -2024,17 +2105,288 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
 
 using TilePassFn = void (*)(const BSeg*, int, uint32_t*, const int64_t*, const uint32_t*, const float*, int, int64_t,
                             int64_t, int, uint32_t*, uint32_t*, const uint32_t*, uint32_t*, float*,
-                            unsigned long long*, uint32_t*, uint16_t*, uint32_t*, float*, uint16_t*, uint32_t*);
+                            unsigned long long*, uint32_t*, uint16_t*, uint32_t*, float*, uint16_t*, uint32_t*,
+                            const BucketArgs);
 
-template <bool PLACE>
+template <bool PLACE, bool BUCKET = false>
 TilePassFn tile_pass_fn(bool compress, bool wide, bool weighted) {
 #define PCPM_TILE_FN(C, WI, WE) \
-  if (compress == C && wide == WI && weighted == WE) return k_tile_pass<PLACE, C, WI, WE>;
+  if (compress == C && wide == WI && weighted == WE) return k_tile_pass<PLACE, C, WI, WE, BUCKET>;
   PCPM_TILE_FN(true, false, false) PCPM_TILE_FN(true, false, true) PCPM_TILE_FN(true, true, false)
   PCPM_TILE_FN(true, true, true) PCPM_TILE_FN(false, false, false) PCPM_TILE_FN(false, false, true)
   PCPM_TILE_FN(false, true, false) PCPM_TILE_FN(false, true, true)
 #undef PCPM_TILE_FN
   return nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// Two-level placement (k_dst > kBucketMinK; DESIGN.md §5 "build").  The one-level place
+// pass writes each tile's edges to k_dst bins in runs of ~m/(tiles k_dst) IDs (4 at c4):
+// partial sectors, written back to DRAM several times (measured: 11.6 GB written for 3.6 GB
+// of layout).  Here the tile pass first moves each edge's record into its segment's
+// bucket h = j >> 5 (runs of ~128 records), then k_bucket_place takes one (segment s,
+// bucket h) at a time -- its records in CSR order -- and places them into the 32 bins of h
+// (runs of ~256 IDs per tile).  Same stable order, so the same layout, bit for bit.
+constexpr int64_t kBucketMinK = 64;        // up to 64 bins the one-level pass already writes long runs
+constexpr uint32_t kHeavyUnit = 4 * kTileE;
+
+// SB[s][h] = first scratch slot of (segment s, bucket h): the segment's first edge + the
+// IDs of its earlier buckets; SB[s][nbk] = the segment's end.  CI holds the absolute ID
+// bases per (s, j) (after the column prefix), so the count of (s, j) is the next
+// segment's base minus this one (the last segment: the bin's end).  One block per segment.
+__global__ void __launch_bounds__(1024) k_seg_buckets(int64_t n_seg, int64_t k_dst, int nbk, const BSeg* segs,
+                                                      const int64_t* __restrict__ row_ptr,
+                                                      const uint32_t* __restrict__ CI,
+                                                      const uint32_t* __restrict__ bin_id_start, uint32_t* SB) {
+  __shared__ uint32_t hs[64];
+  const int64_t sg = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int h = warp; h < nbk; h += 32) {
+    const int64_t j = (int64_t)h * 32 + lane;
+    uint32_t c = 0;
+    if (j < k_dst) {
+      const uint32_t nxt = sg + 1 < n_seg ? CI[(sg + 1) * k_dst + j] : bin_id_start[j + 1];
+      c = nxt - CI[sg * k_dst + j];
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) hs[h] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = (uint32_t)row_ptr[segs[sg].u0];
+    for (int h = 0; h < nbk; ++h) {
+      SB[sg * (nbk + 1) + h] = run;
+      run += hs[h];
+    }
+    SB[sg * (nbk + 1) + nbk] = run;
+  }
+}
+
+// Work list of the (s, h) units with records: heavy ones (> kHeavyUnit) from the front,
+// the rest from the back (claim order only; the output does not depend on it).
+__global__ void k_bucket_units(int64_t n_units, int nbk, const uint32_t* __restrict__ SB, uint32_t* units,
+                               uint32_t* nheavy_nlight) {
+  GRID_STRIDE(u, n_units) {
+    const int64_t sg = u / nbk, h = u % nbk;
+    const uint32_t sz = SB[sg * (nbk + 1) + h + 1] - SB[sg * (nbk + 1) + h];
+    if (sz == 0) continue;
+    if (sz > kHeavyUnit) units[atomicAdd(&nheavy_nlight[0], 1u)] = (uint32_t)u;
+    else units[n_units - 1 - atomicAdd(&nheavy_nlight[1], 1u)] = (uint32_t)u;
+  }
+}
+
+// Place the records of unit (s, h) into bins j = 32 h + (0..31): destID slot = CI[s][j] +
+// rank among the unit's bin-j records, PNG slot = G[p][j] + CR[s][j] + rank among its
+// flagged ones (runs, Alg. 2).  Tiles of kTileE records, warp-striped like the tile pass.
+// 2 CTAs of 512 threads per SM, 4096-record tiles (8 per thread).  The CTA walks its units'
+// tiles as one stream: the records of the next tile (possibly of the next unit, claimed one
+// tile ahead by warp 0, which also loads that unit's bin bases) are bulk-copied (TMA) into
+// the other half of a double buffer while this tile is ranked and placed.
+#ifndef PCPM_BP_CTAS
+#define PCPM_BP_CTAS 2
+#endif
+constexpr int kBpThreads = 1024 / PCPM_BP_CTAS, kBpWarps = kBpThreads / 32, kBpItems = 8;
+constexpr int kBpTile = kBpThreads * kBpItems;
+struct BpUnit {
+  uint32_t r0, r1, p, h;     // records [r0, r1) of bucket h of a segment of partition p
+  uint32_t ci[32], cr[32];   // the 32 bins' first ID slot / first PNG slot for this segment
+  uint32_t valid, pad[3];
+};
+size_t bucket_place_smem(bool weighted) {
+  return 2 * ((size_t)kBpTile + 2) * 8 + (weighted ? 2 * ((size_t)kBpTile + 4) * 4 : 0) + 2 * sizeof(BpUnit) + 64;
+}
+
+template <bool WIDE, bool WEIGHTED>
+__global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
+    const uint32_t* __restrict__ units, const uint32_t* nheavy_nlight, int64_t n_units, uint32_t* ctr,
+    const BSeg* __restrict__ segs, int b, int64_t k_dst, const uint32_t* __restrict__ CI,
+    const uint32_t* __restrict__ CR, const uint32_t* __restrict__ G, const BucketArgs ba, uint16_t* ids16,
+    uint32_t* ids32, float* w, uint16_t* png16, uint32_t* png32) {
+  // Per warp and bin, counts are kept in registers (lane l counts bin l): a step's bins come
+  // from 5 ballots of the bin bits, so a step has no shared-memory round trip.
+  extern __shared__ __align__(16) uint8_t bsm[];
+  uint64_t* rbuf = reinterpret_cast<uint64_t*>(bsm);                          // [2][kBpTile + 2]
+  float* wbuf = reinterpret_cast<float*>(rbuf + 2 * (kBpTile + 2));           // [2][kBpTile + 4]
+  BpUnit* un = reinterpret_cast<BpUnit*>(reinterpret_cast<uint8_t*>(wbuf) + (WEIGHTED ? 2 * (kBpTile + 4) * 4 : 0));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(un + 2);                         // [2]
+  __shared__ uint32_t wI[kBpWarps][33], wF[kBpWarps][33];   // per-warp totals -> per-warp bases
+  __shared__ uint32_t ciS[32], crS[32];                      // running ID / PNG slot of bin 32 h + l
+  __shared__ uint32_t tile_s[4];                             // next tile: x0, unit slot, first-of-unit, valid
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  uint32_t sel[5];                                 // lane l's bin mask: AND_t (bal_t ^ sel_t)
+#pragma unroll
+  for (int t = 0; t < 5; ++t) sel[t] = ((lane >> t) & 1) ? 0u : 0xFFFFFFFFu;
+  const uint32_t nh = nheavy_nlight[0], nl = nheavy_nlight[1];
+  const uint32_t qmask = (1u << b) - 1u;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  // warp 0: claim the next non-empty unit into slot us, with its bin bases
+  auto claim = [&](int us) {
+    uint32_t u = 0xFFFFFFFFu;
+    if (lane == 0) {
+      const uint32_t t = atomicAdd(ctr, 1u);
+      u = t < nh ? units[t] : (t - nh < nl ? units[n_units - nl + (t - nh)] : 0xFFFFFFFFu);
+    }
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u == 0xFFFFFFFFu) {
+      if (lane == 0) un[us].valid = 0u;
+      return;
+    }
+    const int64_t sg = u / ba.nbk;
+    const int h = (int)(u % ba.nbk);
+    const uint32_t p = segs[sg].p;
+    const int64_t j = (int64_t)h * 32 + lane;
+    un[us].ci[lane] = j < k_dst ? CI[sg * k_dst + j] : 0u;
+    un[us].cr[lane] = j < k_dst ? CR[sg * k_dst + j] + G[(int64_t)p * k_dst + j] : 0u;
+    if (lane == 0) {
+      un[us].r0 = ba.SB[sg * (ba.nbk + 1) + h];
+      un[us].r1 = ba.SB[sg * (ba.nbk + 1) + h + 1];
+      un[us].p = p;
+      un[us].h = (uint32_t)h;
+      un[us].valid = 1u;
+    }
+  };
+  // thread 0: bulk copy of the tile [x0, min(x0 + kBpTile, r1)) of unit slot us into buffer bf
+  auto issue = [&](int bf, uint32_t x0, uint32_t r1) {
+    const uint32_t xe = min(x0 + (uint32_t)kBpTile, r1);
+    const uint32_t xa = x0 & ~1u, xb = (xe + 1) & ~1u;           // 16-byte aligned record range
+    const uint32_t wa = x0 & ~3u, wb = (xe + 3) & ~3u;
+    mbar_arrive_expect_tx(&bar[bf], (xb - xa) * 8 + (WEIGHTED ? (wb - wa) * 4 : 0));
+    bulk_g2s(rbuf + bf * (kBpTile + 2), ba.rec + xa, (xb - xa) * 8, &bar[bf], policy_evict_first());
+    if (WEIGHTED) bulk_g2s(wbuf + bf * (kBpTile + 4), ba.recw + wa, (wb - wa) * 4, &bar[bf], policy_evict_first());
+  };
+  // the first tile
+  if (warp == 0) {
+    claim(0);
+    __syncwarp();
+    if (lane == 0) {
+      tile_s[0] = un[0].r0;
+      tile_s[1] = 0;
+      tile_s[2] = 1;
+      tile_s[3] = un[0].valid;
+      if (un[0].valid) issue(0, un[0].r0, un[0].r1);
+    }
+  }
+  __syncthreads();
+  uint32_t phase[2] = {0u, 0u};
+  int bf = 0;
+  for (;;) {
+    const uint32_t x0 = tile_s[0], us = tile_s[1], first = tile_s[2];
+    if (!tile_s[3]) break;
+    const BpUnit& U = un[us];
+    const uint32_t r1 = U.r1;
+    if (first && tid < 32) {
+      ciS[tid] = U.ci[tid];
+      crS[tid] = U.cr[tid];
+    }
+    __syncthreads();                                 // everyone has read tile_s / the unit slot
+    // next tile (same unit, or the first tile of a newly claimed unit) into the other buffer
+    if (warp == 0) {
+      uint32_t nx0 = x0 + kBpTile, nus = us, nfirst = 0, nvalid = 1;
+      if (nx0 >= r1) {
+        nus = us ^ 1;
+        claim((int)nus);
+        __syncwarp();
+        nx0 = un[nus].r0;
+        nfirst = 1;
+        nvalid = un[nus].valid;
+      }
+      if (lane == 0) {
+        if (nvalid) issue(bf ^ 1, nx0, un[nus].r1);
+        tile_s[0] = nx0;
+        tile_s[1] = nus;
+        tile_s[2] = nfirst;
+        tile_s[3] = nvalid;
+      }
+    }
+    mbar_wait(&bar[bf], phase[bf]);
+    phase[bf] ^= 1u;
+    const uint64_t* rs = rbuf + bf * (kBpTile + 2) + (x0 & 1u);
+    const float* wsv = wbuf + bf * (kBpTile + 4) + (x0 & 3u);
+    const int base = warp * (kBpTile / kBpWarps);
+    const uint32_t h = U.h, p = U.p;
+    const uint32_t j0 = h * 32u;
+    uint64_t rc[kBpItems];
+    uint32_t rk[kBpItems];                          // rank among the warp's bin-j records | flagged rank << 16
+    uint32_t cI = 0, cF = 0;                        // this warp's counts of bin `lane` so far
+#pragma unroll
+    for (int k = 0; k < kBpItems; ++k) {
+      const int e = base + 32 * k + lane;
+      const bool ok = x0 + (uint32_t)e < r1;
+      rc[k] = ok ? rs[e] : ~0ull;
+      const uint32_t jl = ok ? (uint32_t)(rc[k] >> 32) & 31u : 0u;   // invalid lanes: out of vm
+      const uint32_t vm = __ballot_sync(0xffffffffu, ok);
+      const uint32_t fb = __ballot_sync(0xffffffffu, ok && ((uint32_t)rc[k] & 0x8000u));
+      uint32_t mb = vm;                             // lanes of bin `lane`
+#pragma unroll
+      for (int t = 0; t < 5; ++t) mb &= __ballot_sync(0xffffffffu, (jl >> t) & 1u) ^ sel[t];
+      const uint32_t pm = __shfl_sync(0xffffffffu, mb, jl);   // lanes of my bin (lane jl's mask)
+      const uint32_t bI = __shfl_sync(0xffffffffu, cI, jl), bF = __shfl_sync(0xffffffffu, cF, jl);
+      rk[k] = (bI + __popc(pm & lt)) | ((bF + __popc(pm & fb & lt)) << 16);
+      cI += __popc(mb);
+      cF += __popc(mb & fb);
+    }
+    wI[warp][lane] = cI;
+    wF[warp][lane] = cF;
+    __syncthreads();
+    {
+      // bins kBpB w .. kBpB w + kBpB - 1: exclusive scans of the kBpWarps warps' counts
+      // (segments of kBpWarps lanes), plus the bins' running slots
+      constexpr int kBpB = 32 / kBpWarps;            // bins per warp
+      const int ls = lane % kBpWarps;
+      const int bin = kBpB * warp + lane / kBpWarps;
+      const uint32_t a = wI[ls][bin], c = wF[ls][bin];
+      uint32_t ia = a, ic = c;
+#pragma unroll
+      for (int o = 1; o < kBpWarps; o <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ia, o, kBpWarps);
+        const uint32_t yc = __shfl_up_sync(0xffffffffu, ic, o, kBpWarps);
+        if (ls >= o) {
+          ia += ya;
+          ic += yc;
+        }
+      }
+      const uint32_t bI = ciS[bin], bF = crS[bin];
+      wI[ls][bin] = bI + ia - a;
+      wF[ls][bin] = bF + ic - c;
+      __syncwarp();
+      if (ls == kBpWarps - 1) {
+        ciS[bin] = bI + ia;
+        crS[bin] = bF + ic;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBpItems; ++k) {
+      if (rc[k] != ~0ull) {
+        const uint32_t jl = (uint32_t)(rc[k] >> 32), pw = (uint32_t)rc[k];
+        const uint32_t pos = wI[warp][jl] + (rk[k] & 0xFFFFu);
+        ids16[pos] = (uint16_t)(pw & 0xFFFFu);
+        if (WIDE) ids32[pos] = (((j0 + jl) << b) | (pw & qmask)) | ((pw & 0x8000u) ? 0x80000000u : 0u);
+        if (WEIGHTED) w[pos] = wsv[base + 32 * k + lane];
+        if (pw & 0x8000u) {
+          const uint32_t pp = wF[warp][jl] + (rk[k] >> 16);
+          png16[pp] = (uint16_t)(pw >> 16);
+          if (WIDE) png32[pp] = (p << b) | (pw >> 16);
+        }
+      }
+    }
+    __syncthreads();                                 // wI / wF / this buffer are reused
+    bf ^= 1;
+  }
+}
+
+using BucketPlaceFn = void (*)(const uint32_t*, const uint32_t*, int64_t, uint32_t*, const BSeg*, int, int64_t,
+                               const uint32_t*, const uint32_t*, const uint32_t*, const BucketArgs, uint16_t*,
+                               uint32_t*, float*, uint16_t*, uint32_t*);
+BucketPlaceFn bucket_place_fn(bool wide, bool weighted) {
+  if (wide) return weighted ? k_bucket_place<true, true> : k_bucket_place<true, false>;
+  return weighted ? k_bucket_place<false, true> : k_bucket_place<false, false>;
 }
 
 // Column prefix of a [rows x cols] count matrix, in place: cnt[r][c] <- sum_{r' < r} cnt[r'][c];
@@ -2247,7 +2599,10 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   SegPassFn cnt_fn = seg_pass_fn<false>(h->compressed, h->wide, weighted_ids);
   SegPassFn place_fn = seg_pass_fn<true>(h->compressed, h->wide, weighted_ids);
   TilePassFn tcnt_fn = tile_pass_fn<false>(h->compressed, h->wide, weighted_ids);
-  TilePassFn tplace_fn = tile_pass_fn<true>(h->compressed, h->wide, weighted_ids);
+  // two-level placement for many bins (PCPM_BUILD_ONE_LEVEL=1 keeps the one-level pass, A/B)
+  const bool two_level = !warp_mode && k_dst > kBucketMinK && !getenv("PCPM_BUILD_ONE_LEVEL");
+  TilePassFn tplace_fn = two_level ? tile_pass_fn<true, true>(h->compressed, h->wide, weighted_ids)
+                                   : tile_pass_fn<true>(h->compressed, h->wide, weighted_ids);
   if (warp_mode) {
     TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -2267,7 +2622,7 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   else
     tcnt_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
                                              CI, CR, nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr,
-                                             nullptr, nullptr, nullptr);
+                                             nullptr, nullptr, nullptr, BucketArgs{});
   TK(cudaGetLastError());
   uint32_t herr = 0;
   TK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s));
@@ -2310,14 +2665,42 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 
   // ---- pass 2: place IDs (+ weights) and PNG sources
   TK(cudaMemsetAsync(ctr, 0, 4, s));
-  if (warp_mode)
+  BucketArgs ba{};
+  if (two_level) {
+    // records into (segment, bucket) sub-ranges, then each sub-range into its 32 bins
+    const int nbk = (int)((k_dst + 31) / 32);
+    const int64_t n_units = n_seg * nbk;
+    uint32_t *SB, *units, *nhl;
+    TK(tmp.alloc(&SB, n_seg * (nbk + 1)));
+    TK(tmp.alloc(&units, n_units));
+    TK(tmp.alloc(&nhl, 4));
+    TK(tmp.alloc(&ba.rec, m + 2));                 // the bulk copies read whole 16-byte words
+    if (weighted_ids) TK(tmp.alloc(&ba.recw, m + 4));
+    ba.SB = SB;
+    ba.nbk = nbk;
+    TK(cudaMemsetAsync(nhl, 0, 16, s));
+    k_seg_buckets<<<(unsigned)n_seg, 1024, 0, s>>>(n_seg, k_dst, nbk, d_segs, row_ptr, CI, h->bin_id_start, SB);
+    tplace_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+                                               CI, CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
+                                               h->png16, h->wide ? h->png_src : nullptr, ba);
+    TK(cudaGetLastError());
+    pt.mark("count build: pass 2a (buckets)");
+    k_bucket_units<<<grid_for(n_units), kT, 0, s>>>(n_units, nbk, SB, units, nhl);
+    TK(cudaMemsetAsync(ctr, 0, 4, s));
+    const size_t bpsm = bucket_place_smem(weighted_ids);
+    TK(cudaFuncSetAttribute(bucket_place_fn(h->wide, weighted_ids), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)bpsm));
+    bucket_place_fn(h->wide, weighted_ids)<<<h->num_sms * PCPM_BP_CTAS, kBpThreads, bpsm, s>>>(
+        units, nhl, n_units, ctr, d_segs, b, k_dst, CI, CR, G, ba, h->ids16, ids32, h->w, h->png16,
+        h->wide ? h->png_src : nullptr);
+  } else if (warp_mode)
     place_fn<<<grid, 32 * kCntWarps, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, CI,
                                                 CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
                                                 h->png16, h->wide ? h->png_src : nullptr);
   else
     tplace_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
                                                CI, CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
-                                               h->png16, h->wide ? h->png_src : nullptr);
+                                               h->png16, h->wide ? h->png_src : nullptr, ba);
   TK(cudaGetLastError());
   if (h->weighted && !values) {
     // PCPM_KEEP_VALUES without values: every weight is 1
@@ -2360,7 +2743,12 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   // the counting construction (default) unless the pull CSC is wanted or the bins are too many
   const char* mode = getenv("PCPM_BUILD");                   // "sort": the chunked sort (A/B)
   const int64_t q = int64_t(1) << h->b, k_dst = (csr->n_dst + q - 1) / q;
-  if (!(mode && !strcmp(mode, "sort")) && !(flags & PCPM_BUILD_PULL) && k_dst <= kCountMaxK)
+  // host CSRs take the chunked sort, whose chunks sort while the next ones upload (the H2D
+  // hides the build); "count" forces the counting construction (A/B, tests)
+  const bool host_in = !is_device_ptr(csr->col_idx) || !is_device_ptr(csr->row_ptr);
+  const bool force_count = mode && !strcmp(mode, "count");
+  if (!(mode && !strcmp(mode, "sort")) && !(flags & PCPM_BUILD_PULL) && k_dst <= kCountMaxK &&
+      (!host_in || force_count))
     return build_layout_count(h, csr, flags);
   return csr->values ? build_layout_chunked<PayW>(h, csr, flags) : build_layout_chunked<uint32_t>(h, csr, flags);
 }

@@ -126,6 +126,9 @@ __device__ unsigned long long g_gather_prof[8];
 #ifndef PCPM_GATHER_NO_EPI
 #define PCPM_GATHER_NO_EPI 0
 #endif
+#ifndef PCPM_GATHER_ITEM_FENCE
+#define PCPM_GATHER_ITEM_FENCE 0     // 1: fence after every item's reduction atomics (round-1 form, A/B)
+#endif
 
 __device__ int spmv_fbits(float xmax, int wexp) {
   int ex = 0;
@@ -137,8 +140,10 @@ __device__ int spmv_fbits(float xmax, int wexp) {
 namespace {
 
 // fixed-point (dangling, residual) partials of one warp into the launch's totals (lane 0)
+// (fence = false: the caller fences once before its completion count instead of per item;
+// a per-item fence stalls each warp until its apply's stores are acknowledged)
 __device__ __forceinline__ void warp_red_add(unsigned long long* red, unsigned long long dang, unsigned long long res,
-                                             int lane) {
+                                             int lane, bool fence = true) {
   for (int o = 16; o; o >>= 1) {
     dang += __shfl_xor_sync(0xffffffffu, dang, o);
     res += __shfl_xor_sync(0xffffffffu, res, o);
@@ -146,7 +151,7 @@ __device__ __forceinline__ void warp_red_add(unsigned long long* red, unsigned l
   if (lane == 0) {
     if (dang) atomicAdd(red, dang);
     if (res) atomicAdd(red + 1, res);
-    __threadfence();
+    if (fence) __threadfence();
   }
 }
 // after every partial is in: D_{t+1} and the residual as doubles, totals reset to zero
@@ -807,7 +812,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       }
       if (!SL)
         for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
-      if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane);
+      if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane, PCPM_GATHER_ITEM_FENCE != 0);
       named_bar_sync(1, kCons);
       for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
       named_bar_sync(1, kCons);
@@ -820,6 +825,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   }
 
   if constexpr (MULTI) __threadfence_system();     // peer stores performed before the kernel completes
+  else __threadfence();                            // this warp's red_fx atomics before the completion count
   // ---------------- last CTA: fixed-order reduction, counter reset ----------------
   named_bar_sync(1, kCons);
   if (ctid == 0) {

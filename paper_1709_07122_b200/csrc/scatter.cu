@@ -86,7 +86,14 @@ struct ScatterArgs {
 // are read with ld.global.nc instead of a 128 KB shared-memory copy of the partition's
 // slice per item -- for graphs whose vector is L2-resident and whose items are many
 // per source partition (small k), the staging is mostly redundant traffic.
-template <typename SrcT, bool XG = false>
+// VEC (scatter_variant 3, north star (2)'s "vectorised 128-bit stores"): each lane writes
+// 4 consecutive update slots with one 16-byte store.  A group's slots are contiguous but
+// start at any word (upd_off is a running count), so the quads are aligned in
+// DESTINATION space per group: group g's segment of the sub-range covers the quads
+// floor4(lo + delta_g) .. of upd, its first and last quads partial (scalar stores).  The
+// quads of all groups in the sub-range are numbered consecutively and dealt to the lanes
+// 32 at a time; a lane finds its group by walking from the round's first group.
+template <typename SrcT, bool XG = false, bool VEC = false>
 __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const ScatterArgs a) {
   constexpr int kScW = ScCfg<SrcT>::kW;
   constexpr int kChunk = kScStageBytes / (int)sizeof(SrcT);   // PNG entries per stage
@@ -231,7 +238,63 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
         mbar_wait(&full[stage], phase);
         const ScStageMeta sm = smeta[stage];
         const SrcT* ps = reinterpret_cast<const SrcT*>(ring + stage * kScStageBytes);
+        // VEC: quads of destination slots, aligned per group (see the kernel's comment)
+        auto range_vec = [&](const int sr) {
+          const uint32_t wb = sm.base + (uint32_t)(sr * kSub);
+          const uint32_t wlo = max(wb, sm.lo), whi = min(wb + (uint32_t)kSub, sm.hi);
+          if (wlo >= whi) return;
+          const int32_t ga = (int32_t)(grp_s[stage * kScGrpCap + sm.gshift + (wb - sm.base) / kPngChunk] -
+                                       (im.p * (uint32_t)a.k_dst + im.j0));
+          uint32_t g = ga > 0 ? (uint32_t)ga : 0u;
+          while (offs[g + 1] <= wlo) ++g;                 // the group of wlo (the anchor is wb's)
+          // quads of group gg inside [wlo, whi): 0 if the segment is empty
+          auto nq = [&](uint32_t gg) -> uint32_t {
+            const uint32_t slo = max(offs[gg], wlo), shi = min(offs[gg + 1], whi);
+            if (slo >= shi) return 0u;
+            const uint32_t dl = uos[gg] - offs[gg];
+            return ((shi + dl + 3) >> 2) - ((slo + dl) >> 2);
+          };
+          uint32_t total = 0;
+          for (uint32_t gg = g; offs[gg] < whi; ++gg) total += nq(gg);
+          uint32_t gcur = g, qcur = 0;                    // the round's first quad: quad qcur of group gcur
+          for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+            uint32_t gg = gcur, rem = qcur + lane, n = nq(gg);
+            while (rem >= n && t0 + lane < total) {
+              rem -= n;
+              ++gg;
+              n = nq(gg);
+            }
+            if (t0 + lane < total) {
+              const uint32_t dl = uos[gg] - offs[gg];
+              const uint32_t slo = max(offs[gg], wlo), shi = min(offs[gg + 1], whi);
+              const uint32_t dq = (((slo + dl) >> 2) + rem) << 2;          // first slot of the quad
+              const int32_t lead = (int32_t)(dq - dl - slo);                // < 0: the quad starts before slo
+              const uint32_t elo = lead > 0 ? slo + (uint32_t)lead : slo, ehi = min(dq + 4 - dl, shi);
+              const SrcT* pe = ps + (elo - sm.base);
+              if (ehi - elo == 4) {
+                const uint32_t u0 = (uint32_t)pe[0] - ubase, u1 = (uint32_t)pe[1] - ubase;
+                const uint32_t u2 = (uint32_t)pe[2] - ubase, u3 = (uint32_t)pe[3] - ubase;
+                *reinterpret_cast<float4*>(a.upd + dq) =
+                    XG ? make_float4(__ldg(xg + u0), __ldg(xg + u1), __ldg(xg + u2), __ldg(xg + u3))
+                       : make_float4(xs[u0], xs[u1], xs[u2], xs[u3]);
+              } else {
+                for (uint32_t e = elo; e < ehi; ++e) {
+                  const uint32_t u = (uint32_t)ps[e - sm.base] - ubase;
+                  a.upd[e + dl] = XG ? __ldg(xg + u) : xs[u];
+                }
+              }
+            }
+            // next round starts after lane 31's quad
+            const uint32_t g31 = __shfl_sync(0xffffffffu, gg, 31), r31 = __shfl_sync(0xffffffffu, rem, 31);
+            gcur = g31;
+            qcur = r31 + 1;
+          }
+        };
         auto range = [&](const int sr) {
+          if constexpr (VEC) {
+            range_vec(sr);
+            return;
+          }
         const uint32_t wb = sm.base + (uint32_t)(sr * kSub);
         const uint32_t wlo = max(wb, sm.lo), whi = min(wb + (uint32_t)kSub, sm.hi);
         if (wlo < whi) {
@@ -367,6 +430,10 @@ int prepare_scatter(pcpm_handle* h) {
                                scatter_tma_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint16_t, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
+  PCPM_CK(cudaFuncSetAttribute(k_scatter_tma<uint32_t, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               scatter_tma_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                scatter_warp_smem_bytes(kMaxBits)));
   PCPM_CK(cudaFuncSetAttribute(k_scatter_warp<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -414,11 +481,13 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out, b
     a.counters = h->counters;
     a.pf_stages = h->opt_scatter_pf;
     const int smem = scatter_tma_smem_bytes(h->b);
-    const bool xg = h->opt_scatter_variant == 2;
+    const bool xg = h->opt_scatter_variant == 2, vec = h->opt_scatter_variant == 3;
     if (h->wide)
-      (xg ? k_scatter_tma<uint32_t, true> : k_scatter_tma<uint32_t>)<<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
+      (xg ? k_scatter_tma<uint32_t, true> : vec ? k_scatter_tma<uint32_t, false, true> : k_scatter_tma<uint32_t>)
+          <<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
     else
-      (xg ? k_scatter_tma<uint16_t, true> : k_scatter_tma<uint16_t>)<<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
+      (xg ? k_scatter_tma<uint16_t, true> : vec ? k_scatter_tma<uint16_t, false, true> : k_scatter_tma<uint16_t>)
+          <<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
   }
   PCPM_CK(cudaGetLastError());
   h->launches += 1;

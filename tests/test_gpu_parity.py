@@ -200,11 +200,13 @@ def test_bad_csr_rejected(pcpm):
     assert e.value.code == pcpm.PCPM_EBADCSR
 
 
+@pytest.mark.parametrize("variant", [0, 3], ids=["scatter_v0", "scatter_v3_vec4"])
 @pytest.mark.parametrize("name,mk,b", LAYOUT_CASES[:7], ids=[c[0] for c in LAYOUT_CASES[:7]])
-def test_scatter_bit_exact(pcpm, name, mk, b):
+def test_scatter_bit_exact(pcpm, name, mk, b, variant):
     g = mk()
     h = build(pcpm, g, b)
     try:
+        pcpm.pcpm_set_option(h, "scatter_variant", variant)
         x = np.random.default_rng(1).random(g.n_src).astype(np.float32)
         xd = torch.from_numpy(x).cuda()
         pcpm.pcpm_scatter(h, xd)
@@ -362,7 +364,7 @@ def test_spmv_non_square(pcpm):
         pcpm.pcpm_destroy(h)
 
 
-@pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_variant": 2}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
+@pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_variant": 2}, {"scatter_variant": 3}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
                                   {"cluster_gather": 0}, {"gather_variant": 2},
                                   {"epilogue_prefetch": 0}, {"gather_prefetch": 8, "epilogue_prefetch": 16},
                                   {"use_graph": 0}],
@@ -402,13 +404,20 @@ CHUNK_CASES = [
 
 
 @pytest.mark.parametrize("name,mk,b,host,flags", CHUNK_CASES, ids=[c[0] for c in CHUNK_CASES])
-@pytest.mark.parametrize("mode", ["count", "count_seg1", "count_seg200", "warp", "warp_seg200", "sort_1", "sort_777",
-                                  "legacy"])
+@pytest.mark.parametrize("mode", ["count", "count_seg1", "count_seg200", "count_onelevel", "warp", "warp_seg200",
+                                  "sort_1", "sort_777", "legacy", "default"])
 def test_layout_chunked_build(pcpm, monkeypatch, name, mk, b, host, flags, mode):
     """Every construction gives the oracle's layout, for host or device inputs, weights,
     wide IDs and uncompressed bins: the counting build (default; segments of one
     32-row batch with PCPM_BUILD_SEG_EDGES=1, ~200 edges, or the default plan), the
-    chunked sort for any chunk size (PCPM_BUILD=sort), and the legacy path."""
+    chunked sort for any chunk size (PCPM_BUILD=sort), and the legacy path.  The counting
+    build places in two levels (segment buckets, then bins) when k_dst > 64 and in one level
+    with PCPM_BUILD_ONE_LEVEL=1; "default" leaves the choice to pcpm_build (host inputs:
+    the chunked sort)."""
+    if mode.startswith("count") or mode.startswith("warp"):
+        monkeypatch.setenv("PCPM_BUILD", "count")    # also for host inputs
+    if mode == "count_onelevel":
+        monkeypatch.setenv("PCPM_BUILD_ONE_LEVEL", "1")
     if mode == "legacy":
         monkeypatch.setenv("PCPM_BUILD_LEGACY", "1")
     elif mode.startswith("sort_"):
