@@ -686,10 +686,27 @@ def cpu_baseline(g, key, op, iters, budget_s=20.0):
         for _ in range(k):
             st.step(0.85)
         t1 = (time.perf_counter() - t0) / k
-        return {"value": round(m / t1 / 1e9, 4), "unit": "GTEPS", "cores": cores, "kind": "oracle",
-                "sample": f"{k} of {iters} iterations of the fp64 pull oracle (one Eq. 1 update each, buffers "
-                          f"allocated beforehand) on the full {key} graph (its CSC transpose, {t_tr:.1f} s, "
-                          f"excluded); {t1 * 1e3:.1f} ms/iteration"}
+        out = {"value": round(m / t1 / 1e9, 4), "unit": "GTEPS", "cores": cores, "kind": "oracle",
+               "sample": f"{k} of {iters} iterations of the fp64 pull oracle (one Eq. 1 update each, buffers "
+                         f"allocated beforehand) on the full {key} graph (its CSC transpose, {t_tr:.1f} s, "
+                         f"excluded); {t1 * 1e3:.1f} ms/iteration"}
+        if key in ("c1", "c2"):
+            # BASELINE.md §2 / SURVEY §8(d): also one core for the small configs
+            oracle.set_threads(1)
+            try:
+                t0 = time.perf_counter()
+                st.step(0.85)
+                t_one = time.perf_counter() - t0
+                k1 = int(max(1, min(iters, (budget_s / 4) / max(t_one, 1e-6))))
+                t0 = time.perf_counter()
+                for _ in range(k1):
+                    st.step(0.85)
+                t_one = (time.perf_counter() - t0) / k1
+            finally:
+                oracle.set_threads(cores)
+            out["single_core"] = {"value": round(m / t_one / 1e9, 4), "cores": 1,
+                                  "ms_per_iter": round(t_one * 1e3, 3), "iterations_timed": k1}
+        return out
     x = None
     from inputs import graphs
     x = graphs.make_x(n, gn.meta["seed"])

@@ -75,6 +75,11 @@ def num_threads() -> int:
     return int(_load().oracle_num_threads())
 
 
+def set_threads(t: int) -> None:
+    """OpenMP threads of the oracle's parallel loops (timing only; results do not depend on it)."""
+    _load().oracle_set_threads(int(t))
+
+
 def transpose(n, row_ptr, col):
     """In-adjacency (CSC) of the CSR graph: (in_ptr int64[n+1], in_src uint32[m])."""
     row_ptr, col = _csr(row_ptr, col)

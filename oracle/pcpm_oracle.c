@@ -56,6 +56,15 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops (bench.py's single-core baseline). */
+void oracle_set_threads(int t) {
+#ifdef _OPENMP
+  omp_set_num_threads(t > 0 ? t : 1);
+#else
+  (void)t;
+#endif
+}
+
 /* Neumaier compensated sum of x[0..n) (D_t and checks use a
  * compensated fp64 sum so that sum(PR)=1 holds to ~1e-16 n). */
 static double oracle_sum(const double* x, int64_t n) {
