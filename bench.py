@@ -191,6 +191,8 @@ def run_pcpm(args, world, rank, local):
         flags |= pcpm.PCPM_NO_COMPRESS
     if args.slots:
         flags |= pcpm.PCPM_COMPACT_SLOTS
+    if args.engine == "bvgas":
+        flags |= pcpm.PCPM_BVGAS                  # the BVGAS comparison engine (Alg. 3)
     # the first build grows the stream-ordered memory pool; build_ms is the median of the next three
     h = pcpm.pcpm_build_ex(csr, b, flags, stream)
     build_ms_cold = pcpm.pcpm_get_info(h).build_ms
@@ -258,6 +260,11 @@ def run_pcpm(args, world, rank, local):
     pk = peaks()
     peak = float(pk.get("hbm_gbs", 6650.0))
     sb, gb = layout_bytes(info, op, args.wide, weighted_pr)
+    if args.engine == "bvgas":
+        # Alg. 3's scatter: the CSR (row_ptr 8(n+1) + col 4m), one source value per vertex (4n)
+        # and one update per edge written (4m) -- Eq. 4's scatter term with d_i = 4 and 8-byte
+        # offsets; the 8-byte records written and re-read between its two passes are extra
+        sb = 8 * (n + 1) + 4 * m + 4 * n + 4 * m
     kernels = {}
     fused = op == "pagerank" and bool(getattr(pcpm.pcpm_get_info(h), "fused_iterations", 0))
     if op == "pagerank" and fused:
@@ -291,9 +298,9 @@ def run_pcpm(args, world, rank, local):
     hbm_gbs = iter_bytes / (ms_iter * 1e-3) / 1e9
     # the committed ncu capture is of the default build (compact, compressed, the
     # config's partition bits, default options); other variants report null
-    default_variant = not (args.no_compress or args.wide or args.bits or args.opt)
+    default_variant = not (args.no_compress or args.wide or args.bits or args.opt or args.engine != "pcpm")
     # the uncompressed layout has its own committed capture (key "<cfg>_nocompress")
-    nocomp_only = args.no_compress and not (args.wide or args.bits or args.opt)
+    nocomp_only = args.no_compress and not (args.wide or args.bits or args.opt or args.engine != "pcpm")
     tkey = key + "_nocompress" if nocomp_only else key
     traffic = ncu_traffic(tkey, dom, strict=dom == "gather_apply_scatter") if (default_variant or nocomp_only) \
         else None
@@ -309,7 +316,9 @@ def run_pcpm(args, world, rank, local):
         "data": "synthetic (seeded RMAT/ER, inputs/)",
         "hbm_gbs": round(hbm_gbs, 1), "hbm_frac_of_measured": round(hbm_gbs / peak, 4),
         "hbm_frac_of_8tbs_spec": round(hbm_gbs / 8000.0, 4),
-        "config": {"workload": WORKLOADS[key], "n": n, "m": m, "k": info.k_dst, "q": info.q,
+        "config": {"workload": WORKLOADS[key] + (" -- BVGAS engine (Alg. 3, PCPM_BVGAS)" if args.engine == "bvgas"
+                                                 else ""),
+                   "n": n, "m": m, "k": info.k_dst, "q": info.q,
                    "e_prime": info.e_prime, "r": round(info.r, 4), "iters": iters, "partition_bits": b,
                    "n_dangling": info.n_dangling, "build_ms": round(build_ms, 2),
                    "build_ms_first": round(build_ms_cold, 2),
@@ -367,7 +376,7 @@ def run_pcpm(args, world, rank, local):
                                             "paper_eq3_bytes": round(model.pdpr_comm(n, m, c_mr, l=l_sec)),
                                             "gbs": round(pull / (pull_ms / iters * 1e-3) / 1e9, 1)})
     pcpm.pcpm_destroy(h)
-    if not args.no_e2e:
+    if not args.no_e2e and args.engine == "pcpm":
         line["e2e"] = e2e(args, g, b, iters, op, world)
     del out
     torch.cuda.empty_cache()
@@ -791,6 +800,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--out", default="")
     ap.add_argument("--opt", action="append", default=[], help="pcpm_set_option key=value (A/B experiments)")
+    ap.add_argument("--engine", default="pcpm", choices=["pcpm", "bvgas"],
+                    help="bvgas: the BVGAS comparison engine (Alg. 3, PCPM_BVGAS) on the same bins")
     ap.add_argument("--no-compress", action="store_true",
                     help="uncompressed bins: one update per edge (the BVGAS-like traffic of Eq. 4)")
     ap.add_argument("--sharded", action="store_true", help="use the destination-sharded path even at N=1")

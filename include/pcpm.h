@@ -56,6 +56,13 @@ extern "C" {
                                   stages instead of 4.  Results are identical; ignored (layout as
                                   without the flag) for weighted / shard / wide handles or when the
                                   condition fails (pcpm_get_info().compact_slots says which). */
+#define PCPM_BVGAS 0x20u       /* the BVGAS comparison engine (Alg. 3; implies PCPM_NO_COMPRESS):
+                                  destination IDs written once at build (the paper's own BVGAS,
+                                  P:313), and every iteration's scatter traverses the CSR vertex-
+                                  centrically, inserting each edge's update (u's value) at its bin's
+                                  insertion point -- one update per edge instead of one per (u, j) run.
+                                  The handle keeps a copy of the CSR.  Square, unweighted, compact
+                                  layout only (else PCPM_EINVAL). */
 #define PCPM_WIDE_IDS 0x8u     /* iterate on the paper's 4-byte layout (global 31-bit IDs + MSB flag in
                                   destID bins, 4-byte PNG sources) instead of the default
                                   compact one (2-byte partition-local IDs: 15-bit offset + MSB flag,
@@ -96,6 +103,7 @@ typedef struct {
   int32_t fused_iterations;   /* 1: the last pcpm_pagerank ran the fused iteration (each gather kernel also
                                  scatters the next iteration's updates; phase times then read: init, the
                                  first scatter, one entry per iteration) */
+  int32_t bvgas;              /* 1: the BVGAS comparison engine (PCPM_BVGAS) */
 } pcpm_info;
 
 /* Device pointers to the built layout, for bit-exact tests (read-only).

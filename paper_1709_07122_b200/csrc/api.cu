@@ -188,7 +188,7 @@ int mark(pcpm_handle* h, cudaStream_t s) {
 int enqueue_iteration(pcpm_handle* h, double d, int t, float* pr_new, cudaStream_t s) {
   int rc;
   const bool wpr = h->opt_weighted_pr && h->inv_wdeg && h->w;      // weighted PageRank (R24)
-  if ((rc = launch_scatter(h, h->spr, s))) return rc;              // Alg. 4
+  if ((rc = h->bvgas ? launch_bvgas_scatter(h, h->spr, s) : launch_scatter(h, h->spr, s))) return rc;   // Alg. 4 / Alg. 3
   if ((rc = mark(h, s))) return rc;
   GatherArgs a = base_args(h, h->fixed_bits);
   a.d = d;
@@ -207,7 +207,7 @@ int enqueue_iteration(pcpm_handle* h, double d, int t, float* pr_new, cudaStream
 // The fused iteration (gather + apply + the next iteration's scatter in one kernel, DESIGN.md
 // §5) applies to square, compact, single-GPU handles on the persistent gather path.
 bool fused_ok(const pcpm_handle* h) {
-  return h->opt_fuse && !h->wide && !h->shard && h->n_src == h->n_dst && h->k_src == h->k_dst && !h->slot16 &&
+  return h->opt_fuse && !h->bvgas && !h->wide && !h->shard && h->n_src == h->n_dst && h->k_src == h->k_dst && !h->slot16 &&
          !(h->cl_cs >= 2 && h->opt_cluster_gather) && h->opt_gather_variant == 1 && h->e_prime > 0;
 }
 
@@ -708,7 +708,7 @@ int pcpm_spmv(pcpm_handle* h, const float* x, float* y) {
   h->launches = 0;
   int rc = launch_absmax(h, xd, h->n_src, h->xmax, s);                    // fixed-point scale of this x
   if (rc) return rc;
-  rc = launch_scatter(h, xd, s);                                           // Alg. 4 on x
+  rc = h->bvgas ? launch_bvgas_scatter(h, xd, s) : launch_scatter(h, xd, s);   // Alg. 4 (Alg. 3) on x
   if (rc) return rc;
   h->last_was_spmv = true;
   GatherArgs a = base_args(h, 0);
@@ -735,7 +735,7 @@ int pcpm_scatter(pcpm_handle* h, const float* x) {
     xd = h->xbuf;
   }
   h->launches = 0;
-  return launch_scatter(h, xd, h->stream);
+  return h->bvgas ? launch_bvgas_scatter(h, xd, h->stream) : launch_scatter(h, xd, h->stream);
 }
 
 void pcpm_destroy(pcpm_handle* h) {
@@ -798,6 +798,7 @@ int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
   i.scatter_items = h->n_sitems;
   i.fixed_point_bits = h->fixed_bits;
   i.compact_slots = h->slot16 ? 1 : 0;
+  i.bvgas = h->bvgas ? 1 : 0;
   i.fused_iterations = h->last_fused ? 1 : 0;
   if (h->last_was_spmv && h->xmax) {   // same rule as spmv_fbits() in gather.cu
     float xm = 0.f;

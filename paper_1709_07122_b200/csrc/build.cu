@@ -1685,9 +1685,13 @@ struct BucketArgs {
   int nbk;                  // buckets = ceil(k_dst / 32)
   uint64_t* rec;            // [m] records
   float* recw;              // [m] weights (WEIGHTED)
+  const float* xval;        // BV: the scatter input (the record carries x[u] instead of the payload)
+  float* upd;               // BV: the update bins
 };
 
-template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED, bool BUCKET = false>
+// BV (with BUCKET; the BVGAS engine's per-iteration scatter, Alg. 3): the record
+// carries the source value x[u] instead of the layout payload; no validation.
+template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED, bool BUCKET = false, bool BV = false>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
     const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst, int kbits,
@@ -1855,7 +1859,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
           const bool flag = !COMPRESS || first || prj != j;
           T.key0[i] = (uint16_t)j;
           T.idx0[i] = (uint16_t)i;
-          T.pay0[i] = (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
+          T.pay0[i] = BV ? __float_as_uint(__ldg(ba.xval + u)) : (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
           if (!PLACE) {
             atomicAdd(&T.ci[j], 1u);
             if (flag) atomicAdd(&T.cr[j], 1u);
@@ -2196,7 +2200,7 @@ size_t bucket_place_smem(bool weighted) {
   return 2 * ((size_t)kBpTile + 2) * 8 + (weighted ? 2 * ((size_t)kBpTile + 4) * 4 : 0) + 2 * sizeof(BpUnit) + 64;
 }
 
-template <bool WIDE, bool WEIGHTED>
+template <bool WIDE, bool WEIGHTED, bool BV = false>
 __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
     const uint32_t* __restrict__ units, const uint32_t* nheavy_nlight, int64_t n_units, uint32_t* ctr,
     const BSeg* __restrict__ segs, int b, int64_t k_dst, const uint32_t* __restrict__ CI,
@@ -2242,7 +2246,7 @@ __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
     const uint32_t p = segs[sg].p;
     const int64_t j = (int64_t)h * 32 + lane;
     un[us].ci[lane] = j < k_dst ? CI[sg * k_dst + j] : 0u;
-    un[us].cr[lane] = j < k_dst ? CR[sg * k_dst + j] + G[(int64_t)p * k_dst + j] : 0u;
+    un[us].cr[lane] = (!BV && j < k_dst) ? CR[sg * k_dst + j] + G[(int64_t)p * k_dst + j] : 0u;
     if (lane == 0) {
       un[us].r0 = ba.SB[sg * (ba.nbk + 1) + h];
       un[us].r1 = ba.SB[sg * (ba.nbk + 1) + h + 1];
@@ -2366,6 +2370,10 @@ __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
       if (rc[k] != ~0ull) {
         const uint32_t jl = (uint32_t)(rc[k] >> 32), pw = (uint32_t)rc[k];
         const uint32_t pos = wI[warp][jl] + (rk[k] & 0xFFFFu);
+        if (BV) {                                    // uncompressed bins: update slot = ID slot
+          ba.upd[pos] = __uint_as_float(pw);
+          continue;
+        }
         ids16[pos] = (uint16_t)(pw & 0xFFFFu);
         if (WIDE) ids32[pos] = (((j0 + jl) << b) | (pw & qmask)) | ((pw & 0x8000u) ? 0x80000000u : 0u);
         if (WEIGHTED) w[pos] = wsv[base + 32 * k + lane];
@@ -2600,7 +2608,7 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   SegPassFn place_fn = seg_pass_fn<true>(h->compressed, h->wide, weighted_ids);
   TilePassFn tcnt_fn = tile_pass_fn<false>(h->compressed, h->wide, weighted_ids);
   // two-level placement for many bins (PCPM_BUILD_ONE_LEVEL=1 keeps the one-level pass, A/B)
-  const bool two_level = !warp_mode && k_dst > kBucketMinK && !getenv("PCPM_BUILD_ONE_LEVEL");
+  const bool two_level = (!warp_mode && k_dst > kBucketMinK && !getenv("PCPM_BUILD_ONE_LEVEL")) || h->bvgas;
   TilePassFn tplace_fn = two_level ? tile_pass_fn<true, true>(h->compressed, h->wide, weighted_ids)
                                    : tile_pass_fn<true>(h->compressed, h->wide, weighted_ids);
   if (warp_mode) {
@@ -2671,10 +2679,22 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     const int nbk = (int)((k_dst + 31) / 32);
     const int64_t n_units = n_seg * nbk;
     uint32_t *SB, *units, *nhl;
-    TK(tmp.alloc(&SB, n_seg * (nbk + 1)));
-    TK(tmp.alloc(&units, n_units));
-    TK(tmp.alloc(&nhl, 4));
-    TK(tmp.alloc(&ba.rec, m + 2));                 // the bulk copies read whole 16-byte words
+    if (h->bvgas) {                                // the per-iteration scatter replays this placement
+      if ((rc = dev_alloc_t(h, &SB, n_seg * (nbk + 1)))) return rc;
+      if ((rc = dev_alloc_t(h, &units, n_units))) return rc;
+      if ((rc = dev_alloc_t(h, &nhl, 4))) return rc;
+      if ((rc = dev_alloc_t(h, &ba.rec, m + 2))) return rc;
+      h->bv_SB = SB;
+      h->bv_units = units;
+      h->bv_nhl = nhl;
+      h->bv_rec = ba.rec;
+      h->bv_nbk = nbk;
+    } else {
+      TK(tmp.alloc(&SB, n_seg * (nbk + 1)));
+      TK(tmp.alloc(&units, n_units));
+      TK(tmp.alloc(&nhl, 4));
+      TK(tmp.alloc(&ba.rec, m + 2));               // the bulk copies read whole 16-byte words
+    }
     if (weighted_ids) TK(tmp.alloc(&ba.recw, m + 4));
     ba.SB = SB;
     ba.nbk = nbk;
@@ -2702,6 +2722,18 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
                                                CI, CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
                                                h->png16, h->wide ? h->png_src : nullptr, ba);
   TK(cudaGetLastError());
+  if (h->bvgas) {
+    // keep what the per-iteration scatter needs: the CSR, the segment plan, the ID bases
+    if ((rc = dev_alloc_t(h, &h->bv_rp, n_src + 1))) return rc;
+    if ((rc = dev_alloc_t(h, &h->bv_col, m + 4))) return rc;
+    if ((rc = dev_alloc(h, &h->bv_segs, sizeof(BSeg) * n_seg))) return rc;
+    if ((rc = dev_alloc_t(h, &h->bv_CI, n_seg * k_dst))) return rc;
+    TK(cudaMemcpyAsync(h->bv_rp, row_ptr, sizeof(int64_t) * (n_src + 1), cudaMemcpyDeviceToDevice, s));
+    TK(cudaMemcpyAsync(h->bv_col, col, sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, s));
+    TK(cudaMemcpyAsync(h->bv_segs, d_segs, sizeof(BSeg) * n_seg, cudaMemcpyDeviceToDevice, s));
+    TK(cudaMemcpyAsync(h->bv_CI, CI, sizeof(uint32_t) * n_seg * k_dst, cudaMemcpyDeviceToDevice, s));
+    h->bv_nseg = n_seg;
+  }
   if (h->weighted && !values) {
     // PCPM_KEEP_VALUES without values: every weight is 1
     k_fill_f32<<<grid_for(m), kT, 0, s>>>(m, 1.0f, h->w);
@@ -2738,6 +2770,18 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
 // Layout construction: the chunked sort (default) or the two-sort legacy path
 // (PCPM_BUILD_LEGACY=1, and graphs without edges).
 int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
+  if (flags & PCPM_BVGAS) {
+    // the BVGAS engine: uncompressed bins from the counting build, whose placement it replays
+    const int64_t q = int64_t(1) << h->b;
+    if (csr->n_src != csr->n_dst || csr->values || (flags & (PCPM_WIDE_IDS | PCPM_KEEP_VALUES | PCPM_BUILD_PULL)) ||
+        csr->nnz == 0 || (csr->n_dst + q - 1) / q > kCountMaxK) {
+      set_error(PCPM_EINVAL, "PCPM_BVGAS needs a square, unweighted graph with edges, the compact layout and "
+                             "k <= 2048 partitions");
+      return PCPM_EINVAL;
+    }
+    h->bvgas = true;
+    return build_layout_count(h, csr, flags | PCPM_NO_COMPRESS);
+  }
   const bool legacy = getenv("PCPM_BUILD_LEGACY") != nullptr;
   if (legacy || csr->nnz == 0 || csr->n_src <= 0 || csr->n_dst <= 0) return build_layout_legacy(h, csr, flags);
   // the counting construction (default) unless the pull CSC is wanted or the bins are too many
@@ -2751,6 +2795,43 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       (!host_in || force_count))
     return build_layout_count(h, csr, flags);
   return csr->values ? build_layout_chunked<PayW>(h, csr, flags) : build_layout_chunked<uint32_t>(h, csr, flags);
+}
+
+// BVGAS scatter (Alg. 3 lines 1-5): every edge (u, v) of the kept CSR inserts
+// x[u] into bin v >> b at its insertion point -- the counting build's two-level placement
+// replayed on values (records carry x[u]; the ranks, hence the slots, are the build's).
+int launch_bvgas_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
+  if (!h->bvgas) {
+    set_error(PCPM_ESTATE, "not a BVGAS handle");
+    return PCPM_ESTATE;
+  }
+  BucketArgs ba{};
+  ba.SB = h->bv_SB;
+  ba.nbk = h->bv_nbk;
+  ba.rec = h->bv_rec;
+  ba.xval = x;
+  ba.upd = h->upd;
+  const int64_t n_units = h->bv_nseg * h->bv_nbk;
+  const int kbits = std::max(1, bits_for((uint64_t)std::max<int64_t>(h->k_dst - 1, 0)));
+  const size_t smem = tile_smem_bytes(h->k_dst);
+  TilePassFn f = k_tile_pass<true, false, false, false, true, true>;
+  PCPM_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const BSeg* segs = static_cast<const BSeg*>(h->bv_segs);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->bv_nseg, h->num_sms));
+  PCPM_CK(cudaMemsetAsync(h->bv_nhl + 2, 0, 8, s));
+  f<<<grid, kTileThreads, smem, s>>>(segs, (int)h->bv_nseg, h->bv_nhl + 2, h->bv_rp, h->bv_col, nullptr, h->b,
+                                     h->k_dst, h->n_dst, kbits, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                     nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ba);
+  PCPM_CK(cudaGetLastError());
+  const size_t bpsm = bucket_place_smem(false);
+  auto g = k_bucket_place<false, false, true>;
+  PCPM_CK(cudaFuncSetAttribute(g, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bpsm));
+  g<<<h->num_sms * PCPM_BP_CTAS, kBpThreads, bpsm, s>>>(h->bv_units, h->bv_nhl, n_units, h->bv_nhl + 3, segs, h->b,
+                                                        h->k_dst, h->bv_CI, nullptr, nullptr, ba, nullptr,
+                                                        nullptr, nullptr, nullptr, nullptr);
+  PCPM_CK(cudaGetLastError());
+  h->launches += 2;
+  return PCPM_OK;
 }
 
 // Claim order of the scatter items.  Default (opt_scatter_lpt = 0): ascending p, so the

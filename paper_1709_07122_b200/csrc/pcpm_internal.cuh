@@ -104,6 +104,20 @@ struct pcpm_handle {
   float* xmax = nullptr;            // [1] device max|x| of the last pcpm_spmv
   bool last_was_spmv = false;
 
+  // BVGAS comparison engine (PCPM_BVGAS, Alg. 3): uncompressed bins, and a
+  // per-iteration vertex-centric scatter over the kept CSR (build.cu launch_bvgas_scatter)
+  bool bvgas = false;
+  int64_t* bv_rp = nullptr;         // [n_src+1] the CSR (the scatter traverses it every iteration)
+  uint32_t* bv_col = nullptr;       // [m]
+  void* bv_segs = nullptr;          // [bv_nseg] segment plan of the counting build
+  int64_t bv_nseg = 0;
+  int bv_nbk = 0;                   // buckets of 32 bins
+  uint32_t* bv_CI = nullptr;        // [bv_nseg * k_dst] first ID (= update) slot of (segment, bin)
+  uint32_t* bv_SB = nullptr;        // [bv_nseg * (bv_nbk + 1)] record slots of (segment, bucket)
+  uint32_t* bv_units = nullptr;     // [bv_nseg * bv_nbk] (segment, bucket) work list
+  uint32_t* bv_nhl = nullptr;       // [4] heavy / light unit counts, claim counters
+  uint64_t* bv_rec = nullptr;       // [m + 2] records (bucket pass -> bin pass)
+
   // pull comparison (CSC)
   uint32_t* in_ptr = nullptr;       // [n_dst+1]
   uint32_t* in_src = nullptr;       // [m]
@@ -176,6 +190,7 @@ int dev_alloc_t(pcpm_handle* h, T** p, size_t count) {
   return dev_alloc(h, reinterpret_cast<void**>(p), count * sizeof(T));
 }
 bool is_device_ptr(const void* p);
+int launch_bvgas_scatter(pcpm_handle* h, const float* x, cudaStream_t s);   // build.cu
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

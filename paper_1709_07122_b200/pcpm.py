@@ -27,6 +27,7 @@ PCPM_BUILD_PULL = 0x2
 PCPM_KEEP_VALUES = 0x4
 PCPM_WIDE_IDS = 0x8
 PCPM_COMPACT_SLOTS = 0x10
+PCPM_BVGAS = 0x20
 
 EXPORTED = ["pcpm_build", "pcpm_build_ex", "pcpm_pagerank", "pcpm_spmv", "pcpm_pull_pagerank", "pcpm_destroy",
             "pcpm_set_stream", "pcpm_last_error", "pcpm_last_status", "pcpm_get_info", "pcpm_export_layout",
@@ -56,7 +57,7 @@ class pcpm_info(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("build_ms", ctypes.c_double),
                 ("gather_items", ctypes.c_int64), ("scatter_items", ctypes.c_int64),
                 ("fixed_point_bits", ctypes.c_int32), ("compact_slots", ctypes.c_int32),
-                ("fused_iterations", ctypes.c_int32)]
+                ("fused_iterations", ctypes.c_int32), ("bvgas", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -717,3 +717,59 @@ def test_fused_iteration_matches_unfused_and_oracle(pcpm, name, mk, b, wpr):
         pr_check(outs[1][0], ref, name)
     finally:
         pcpm.pcpm_destroy(h)
+
+
+BVGAS_CASES = [
+    ("c1", lambda: graphs.make_config("c1"), 8),
+    ("rmat12_b4", lambda: graphs.make_graph("rmat", 7, scale=12, permute=True), 4),
+    ("rmat13_b6", lambda: graphs.make_graph("rmat", 8, scale=13, permute=True), 6),
+    ("er_ragged_b15", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 15),
+    ("outstar_b10", lambda: star_graph(100000), 10),
+    ("instar_b3", lambda: star_graph(5000, inward=True), 3),
+]
+
+
+@pytest.mark.parametrize("name,mk,b", BVGAS_CASES, ids=[c[0] for c in BVGAS_CASES])
+def test_bvgas_engine(pcpm, name, mk, b):
+    """The BVGAS comparison engine (Alg. 3): its vertex-centric scatter fills the
+    uncompressed bins -- every edge (u, v) one update, bins in (v >> b, u, v) order, i.e.
+    upd[x] = x[u] for the x-th edge of that order (a sort-based construction written here,
+    not the kernels' counting placement) -- and its PageRank matches the oracle and is
+    bit-identical to PCPM's on the same uncompressed layout."""
+    g = mk()
+    h = build(pcpm, g, b, flags=pcpm.PCPM_BVGAS)
+    hp = build(pcpm, g, b, flags=pcpm.PCPM_NO_COMPRESS)
+    try:
+        info = pcpm.pcpm_get_info(h)
+        assert info.bvgas == 1 and info.compressed == 0 and info.e_prime == g.m
+        x = np.random.default_rng(3).random(g.n_src).astype(np.float32)
+        pcpm.pcpm_scatter(h, torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        got = d2h(pcpm.pcpm_export_layout(h).upd, g.m, np.float32)
+        src = np.repeat(np.arange(g.n_src, dtype=np.int64), np.diff(g.row_ptr))
+        dst = g.col.astype(np.int64)
+        order = np.lexsort((dst, src, dst >> b))         # bin, then u, then v
+        np.testing.assert_array_equal(got.view(np.uint32), x[src[order]].view(np.uint32))
+        ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 12)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 12, out)
+        outp = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(hp, 0.85, 12, outp)
+        got_pr = out.cpu().numpy()
+        pr_check(got_pr, ref, f"bvgas {name}")
+        np.testing.assert_array_equal(got_pr.view(np.uint32), outp.cpu().numpy().view(np.uint32))
+    finally:
+        pcpm.pcpm_destroy(h)
+        pcpm.pcpm_destroy(hp)
+
+
+def test_bvgas_rejects(pcpm):
+    g = graphs.make_graph("rmat", 9, scale=10, permute=True, values=True, transpose=True)
+    with pytest.raises(pcpm.PcpmError) as e:
+        build(pcpm, g, 6, flags=pcpm.PCPM_BVGAS)                 # weighted
+    assert e.value.code == pcpm.PCPM_EINVAL
+    gr = graphs.make_graph("er", 4, n=3000, m_raw=20000)
+    rp, col = gr.row_ptr, gr.col
+    with pytest.raises(pcpm.PcpmError) as e:                      # non-square
+        pcpm.pcpm_build_ex(pcpm.make_csr(gr.n_src, gr.n_src + 100, rp, col), 6, pcpm.PCPM_BVGAS, None)
+    assert e.value.code == pcpm.PCPM_EINVAL
