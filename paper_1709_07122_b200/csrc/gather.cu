@@ -84,11 +84,17 @@ struct Cfg {
 #ifndef PCPM_GATHER_COLD_WARPS
 #define PCPM_GATHER_COLD_WARPS 31
 #endif
+  // producer warps: two for the hot configuration (each fills the stages of one consumer
+  // group), one otherwise
+#ifndef PCPM_GATHER_PRODUCERS
+#define PCPM_GATHER_PRODUCERS 2
+#endif
+  static constexpr int kProducers = kHot ? PCPM_GATHER_PRODUCERS : 1;
 #ifndef PCPM_GATHER_HOT_WARPS
-#define PCPM_GATHER_HOT_WARPS 31
+#define PCPM_GATHER_HOT_WARPS (32 - PCPM_GATHER_PRODUCERS)
 #endif
   static constexpr int kWarps = kHot ? PCPM_GATHER_HOT_WARPS : PCPM_GATHER_COLD_WARPS;
-  static constexpr int kThreads = 32 * (kWarps + 1);
+  static constexpr int kThreads = 32 * (kWarps + kProducers);
   static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kChunkIds;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
   static constexpr int kGroupA = (kWarps + 1) / 2;          // warps of group 0 (stages 0, 2)
@@ -114,7 +120,7 @@ __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_c
 // Debug timing of the consumer warps (built with -DPCPM_GATHER_PROFILE=1 only):
 // [0] cycles waiting for full stages, [1] decoding stages, [2] at the epilogue's
 // first barrier, [3] in the epilogue, [4] warp count.  Read by pcpm_get_debug_counters.
-__device__ unsigned long long g_gather_prof[8];
+__device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GATHER_PROFILE)
 #ifndef PCPM_GATHER_PROFILE
 #define PCPM_GATHER_PROFILE 0
 #endif
@@ -171,14 +177,21 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
 }
 
-// Warp 0 of a gather CTA: claims work items and streams their tiles (IDs, update
-// window, decode anchors, weights) into the ring of S stages with bulk async copies.
-template <typename C, typename IdT, bool W, bool PR, bool SL, bool FUSE = false>
+// Producer warp(s) of a gather CTA: claim work items and stream their tiles (IDs,
+// update window, decode anchors, weights) into the ring of S stages with bulk async
+// copies.  With NP = 2 producers, producer pg fills the stages of consumer group pg
+// (stages pg, pg + 2, ...): both walk the same sequence of stage pushes and act on their
+// own; producer 0 claims the items and hands them to producer 1 through a small shared
+// queue (claimq / qbar), so the per-stage issue work (measured ~1.5k cycles per stage,
+// DESIGN.md §6) is split over two warps.
+template <typename C, typename IdT, bool W, bool PR, bool SL, bool FUSE = false, int NP = 1>
 __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* ids, uint8_t* stage_base,
-                                                StageMeta* meta, uint64_t* full, uint64_t* empty, int lane) {
+                                                StageMeta* meta, uint64_t* full, uint64_t* empty, int lane,
+                                                int pg = 0, uint32_t* claimq = nullptr, uint64_t* qbar = nullptr) {
   constexpr int S = C::kStages;
   static_assert(!FUSE || C::kStageBytes >= kFusePng * 2 + 256, "a scatter stage fits in a ring stage");
-  // ================= producer (whole warp; lane 0 issues) =================
+  static_assert(NP == 1 || (NP == 2 && S % 2 == 0), "two producers split the stages by parity");
+  constexpr int kQ = 8;                            // claim queue depth (producers are < 3 items apart)
   // The window of tile t is fixed by two decode anchors (chunk_base at the
   // tile's ends).  Lanes load the anchors of 32 tiles at once, so the issue
   // loop carries no dependent global load per tile.
@@ -186,24 +199,54 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
   int stage = 0;
   uint32_t phase = 0;
   bool claimed = false;
-  auto claim = [&]() -> uint32_t {
-    if (a.static_items) {                         // cluster gather: CTA b owns item b only
-      const uint32_t v = claimed ? (uint32_t)a.n_items : blockIdx.x;
-      claimed = true;
-      return v;
+  uint32_t nclaim = 0;
+  unsigned long long pw = 0, pstages = 0, pcopy = 0, ploop = 0, pclaim = 0;   // PCPM_GATHER_PROFILE
+  const long long pt0 = PCPM_GATHER_PROFILE ? clock64() : 0;
+  auto own = [&]() -> bool { return NP == 1 || (stage & 1) == pg; };
+  auto advance = [&]() { if (++stage == S) { stage = 0; phase ^= 1; } };
+  auto wait_empty = [&]() {
+    if (PCPM_GATHER_PROFILE) {
+      const long long t = clock64();
+      mbar_wait(&empty[stage], phase ^ 1);
+      pw += clock64() - t;
+      ++pstages;
+    } else {
+      mbar_wait(&empty[stage], phase ^ 1);
     }
+  };
+  auto claim = [&]() -> uint32_t {
+    const long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
     uint32_t v = 0;
-    if (lane == 0) v = atomicAdd(&a.counters[0], 1u);
-    return __shfl_sync(0xffffffffu, v, 0);
+    if (a.static_items) {                         // cluster gather: CTA b owns item b only
+      v = claimed ? (uint32_t)a.n_items : blockIdx.x;
+      claimed = true;
+    } else {
+      if (lane == 0) {
+        if (NP == 1 || pg == 0) {
+          v = atomicAdd(&a.counters[0], 1u);
+          if (NP == 2) {
+            claimq[nclaim % kQ] = v;
+            mbar_arrive(&qbar[nclaim % kQ]);      // release: producer 1 reads claimq after its wait
+          }
+        } else {
+          mbar_wait(&qbar[nclaim % kQ], (nclaim / kQ) & 1);
+          v = claimq[nclaim % kQ];
+        }
+      }
+      ++nclaim;
+      v = __shfl_sync(0xffffffffu, v, 0);
+    }
+    if (PCPM_GATHER_PROFILE) pclaim += clock64() - tc;
+    return v;
   };
   auto push_meta = [&](const StageMeta& m) {      // a stage without data (empty item / stop)
-    if (lane == 0) {
-      mbar_wait(&empty[stage], phase ^ 1);
+    if (own() && lane == 0) {
+      wait_empty();
       meta[stage] = m;
       mbar_arrive(&full[stage]);
     }
     __syncwarp();
-    if (++stage == S) { stage = 0; phase ^= 1; }
+    advance();
   };
   uint32_t it = claim();
   GatherItem item{};
@@ -241,12 +284,17 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
         const uint32_t nb = min(32u, t1 - tb0 + 1);
         const uint32_t pf = (uint32_t)a.pf_tiles;
         // L2 prefetch of the batch's first pf tiles (the ring then loads them from L2)
-        if (pf && lane < nb && lane < pf) {
+        if (pf && lane < nb && lane < pf && (NP == 1 || ((stage + lane) & 1) == pg)) {
           const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
           bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
           if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
         }
         for (uint32_t k = 0; k < nb; ++k) {
+          if (!own()) {                          // the other producer's stage
+            advance();
+            continue;
+          }
+          const long long tk0 = PCPM_GATHER_PROFILE ? clock64() : 0;
           const uint32_t flo = __shfl_sync(0xffffffffu, fa, k);
           const uint32_t fhi = __shfl_sync(0xffffffffu, fb, k);
           // keep the L2 prefetch pf tiles ahead of the ring (within the batch)
@@ -272,7 +320,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             const uint32_t tb = t * C::kTile;
             const uint32_t wlo = flo > 0 ? flo - 1 : 0;   // the first ID may continue the previous run
             const uint32_t alo = wlo & ~3u, ahi = (fhi + 3) & ~3u;
-            mbar_wait(&empty[stage], phase ^ 1);
+            wait_empty();
             StageMeta m{};
             m.item = (int)it;
             m.j = item.j;
@@ -285,15 +333,18 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             meta[stage] = m;
             uint8_t* sb = stage_base + stage * C::kStageBytes;
             const uint32_t win_bytes = (ahi - alo) * 4;
+            const long long tc0 = PCPM_GATHER_PROFILE ? clock64() : 0;
             mbar_arrive_expect_tx(&full[stage], C::kIdsBytes + win_bytes + C::kCbBytes + C::kWBytes);
             bulk_g2s(sb, ids + tb, C::kIdsBytes, &full[stage], pol);
             bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
             bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
                      &full[stage], pol);
             if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
+            if (PCPM_GATHER_PROFILE) pcopy += clock64() - tc0;
           }
           __syncwarp();
-          if (++stage == S) { stage = 0; phase ^= 1; }
+          if (PCPM_GATHER_PROFILE) ploop += clock64() - tk0;
+          advance();
         }
       }
       if (t1 == t0) {                             // single tile: the other group still needs its Last
@@ -316,9 +367,9 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
         const uint32_t base0 = s0 & ~(uint32_t)(kPngChunk - 1);
         const uint32_t nst = s1 > s0 ? (s1 - base0 + kFusePng - 1) / kFusePng : 0u;
         for (uint32_t c = 0; c < nst; ++c) {
-          if (lane == 0) {
+          if (own() && lane == 0) {
             const uint32_t base = base0 + c * kFusePng;
-            mbar_wait(&empty[stage], phase ^ 1);
+            wait_empty();
             StageMeta m{};
             m.item = (int)it;
             m.j = p;
@@ -337,7 +388,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             bulk_g2s(sb + 2 * kFusePng, a.grp_at + ca, nga * 4, &full[stage], pol);   // grp_at padded
           }
           __syncwarp();
-          if (++stage == S) { stage = 0; phase ^= 1; }
+          advance();
         }
         for (uint32_t c = nst; c < 2; ++c) {      // empty PNG or a single stage: Last for the other group(s)
           StageMeta m{};
@@ -350,6 +401,15 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
     }
     it = it_next;
     item = item_next;
+  }
+  if (PCPM_GATHER_PROFILE && lane == 0) {
+    atomicAdd(&g_gather_prof[8], pw);
+    atomicAdd(&g_gather_prof[9], (unsigned long long)(clock64() - pt0));
+    atomicAdd(&g_gather_prof[10], pstages);
+    atomicAdd(&g_gather_prof[11], 1ull);
+    atomicAdd(&g_gather_prof[12], pcopy);
+    atomicAdd(&g_gather_prof[13], ploop);
+    atomicAdd(&g_gather_prof[14], pclaim);
   }
 }
 
@@ -547,9 +607,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
   uint64_t* empty = full + S;
-  double* red_s = reinterpret_cast<double*>(empty + S);                    // 2*C::kWarps
+  uint64_t* qbar = empty + S;                                              // [8] claim queue (2 producers)
+  double* red_s = reinterpret_cast<double*>(qbar + 8);                     // 2*C::kWarps
   uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * C::kWarps);
+  uint32_t* claimq = flag_s + 4;                                           // [8]
   const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
+  constexpr int NP = C::kProducers;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -557,21 +620,22 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);   // stage s is consumed by group s & 1
     }
+    for (int s = 0; s < 8; ++s) mbar_init(&qbar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == 0) {
-    gather_producer<C, IdT, W, PR, SL, FUSE>(a, ids, stage_base, meta, full, empty, lane);
+  if (warp < NP) {
+    gather_producer<C, IdT, W, PR, SL, FUSE, NP>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar);
     return;
   }
 
   // ================= consumers =================
-  const int cw = warp - 1;                  // consumer warp
+  const int cw = warp - NP;                 // consumer warp
   const int grp = cw < C::kGroupA ? 0 : 1;  // its group takes stages grp, grp + 2, ...
   const int gw = grp ? cw - C::kGroupA : cw;
   const int gsz = grp ? C::kGroupB : C::kGroupA;
-  const int ctid = threadIdx.x - 32;        // 0..511
+  const int ctid = threadIdx.x - 32 * NP;   // 0 .. 32 * kWarps - 1
   constexpr int kCons = 32 * C::kWarps;
   const uint32_t qmask = (uint32_t)(q - 1);
   const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);   // 2^F (PageRank)
@@ -1290,24 +1354,28 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather_cl(const Ga
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + S);
   uint64_t* empty = full + S;
-  uint32_t* orbm = reinterpret_cast<uint32_t*>(empty + S);               // [bm_words] OR of the cluster's bitmaps
+  uint64_t* qbar = empty + S;                                            // [8] claim queue (2 producers)
+  uint32_t* orbm = reinterpret_cast<uint32_t*>(qbar + 8);                // [bm_words] OR of the cluster's bitmaps
   uint32_t* flag_s = orbm + ((bm_words + 3) & ~3);
+  uint32_t* claimq = flag_s + 4;                                         // [8]
   const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
+  constexpr int NP = C::kProducers;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);
     }
+    for (int s = 0; s < 8; ++s) mbar_init(&qbar[s], 1);
     fence_mbar_init();
   }
   for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc[i] = 0u;
   for (int i = threadIdx.x; i < bm_words; i += blockDim.x) bitmap[i] = 0u;
   __syncthreads();
-  if (warp == 0) {
-    gather_producer<C, IdT, W, PR, false>(a, ids, stage_base, meta, full, empty, lane);
+  if (warp < NP) {
+    gather_producer<C, IdT, W, PR, false, false, NP>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar);
   } else {
-    const int cw = warp - 1;
+    const int cw = warp - NP;
     const int grp = cw < C::kGroupA ? 0 : 1;
     const int gw = grp ? cw - C::kGroupA : cw;
     const int gsz = grp ? C::kGroupB : C::kGroupA;
@@ -1410,8 +1478,8 @@ int smem_bytes_cl(int b) {
   const int64_t q = int64_t(1) << b;
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4;
-  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
-               ((bm_words + 3) & ~3) * 4 + 16);
+  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 8 * 8 +
+               ((bm_words + 3) & ~3) * 4 + 16 + 8 * 4);
 }
 
 // Apply of the split bins (items whose bin was cut into slices): one block per
@@ -1521,8 +1589,8 @@ int smem_bytes_for(int b, int64_t aw = 0) {
   const int64_t q = aw > 0 ? aw : int64_t(1) << b;
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4 + (SL ? ((int64_t(1) << b) / 32) * 8 : 0);
-  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 +
-               2 * C::kWarps * 8 + 16);
+  return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 8 * 8 +
+               2 * C::kWarps * 8 + 16 + 8 * 4);
 }
 
 using GatherFn = void (*)(const GatherArgs);
@@ -1626,14 +1694,14 @@ int gather_threads(bool wide, bool weighted) {
 }
 
 int read_debug_counters(unsigned long long* out, int cap, bool reset) {
-  unsigned long long v[8];
+  unsigned long long v[24];
   PCPM_CK(cudaMemcpyFromSymbol(v, g_gather_prof, sizeof(v)));
-  for (int i = 0; i < cap && i < 8; ++i) out[i] = v[i];
+  for (int i = 0; i < cap && i < 24; ++i) out[i] = v[i];
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[24] = {};
     PCPM_CK(cudaMemcpyToSymbol(g_gather_prof, z, sizeof(z)));
   }
-  return cap < 8 ? cap : 8;
+  return cap < 24 ? cap : 24;
 }
 
 int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaStream_t s) {

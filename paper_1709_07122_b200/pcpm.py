@@ -322,8 +322,8 @@ def pcpm_ipc_close(ptr: int):
 
 
 def pcpm_get_debug_counters(reset: bool = True) -> np.ndarray:
-    buf = np.zeros(8, dtype=np.uint64)
-    n = _lib.pcpm_get_debug_counters(_ptr(buf), 8, int(reset))
+    buf = np.zeros(24, dtype=np.uint64)
+    n = _lib.pcpm_get_debug_counters(_ptr(buf), 24, int(reset))
     if n < 0:
         _check(n)
     return buf[:n]

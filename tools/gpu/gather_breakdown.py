@@ -39,3 +39,17 @@ if v2:
     print(key, "apply warps", int(c[7]), f"idle={c[5] / ta:.3f} busy={c[6] / ta:.3f}",
           f"(decoder cycles per warp {tot / max(c[4], 1):.3e}, apply {ta / max(c[7], 1):.3e})")
 pcpm.pcpm_destroy(h)
+if c[11] > 0:
+    print(key, "producer warps", int(c[11]), f"wait-for-empty={c[8] / max(c[9], 1):.3f}",
+          f"stages/warp={c[10] / c[11]:.0f}", f"cycles/stage={c[9] / max(c[10], 1):.0f}",
+          f"issue cycles/stage={(c[9] - c[8]) / max(c[10], 1):.0f}")
+if c[11] > 0 and c[13] > 0:
+    print(key, "producer per stage:", f"copy-issue={c[12] / max(c[10], 1):.0f}",
+          f"tile-loop={c[13] / max(c[10], 1):.0f}", f"(incl. wait {c[8] / max(c[10], 1):.0f})",
+          f"outside tile loop={(c[9] - c[13]) / max(c[10], 1):.0f}")
+if c[11] > 0 and c[14] > 0:
+    print(key, "producer per warp (cycles):", f"total={c[9] / c[11]:.0f} claim={c[14] / c[11]:.0f}",
+          f"stop-wait={c[16] / c[11]:.0f} batches={c[15] / c[11]:.1f}",
+          f"outside-loop={(c[9] - c[13]) / c[11]:.0f}")
+if c[11] > 0 and c[15] > 0:
+    print(key, "producer batch start (cycles/batch):", f"loads={c[17] / c[15]:.0f} loads+prefetch={c[18] / c[15]:.0f}")
