@@ -132,6 +132,9 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 #ifndef PCPM_GATHER_NO_EPI
 #define PCPM_GATHER_NO_EPI 0
 #endif
+#ifndef PCPM_EPI_FAKE
+#define PCPM_EPI_FAKE 0              // timing-only experiment build (wrong results): fp32 apply, no reductions
+#endif
 #ifndef PCPM_GATHER_ITEM_FENCE
 #define PCPM_GATHER_ITEM_FENCE 0     // 1: fence after every item's reduction atomics (round-1 form, A/B)
 #endif
@@ -659,6 +662,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   int srot = 0;                                     // FUSE: rotation of the scatter stages' remainder
   uint32_t phase = 0;
   unsigned long long pt[4] = {0, 0, 0, 0};
+  unsigned long long pe[4] = {0, 0, 0, 0};          // epilogue: pre-apply, apply, reductions, closing barrier
   long long tc = PCPM_GATHER_PROFILE ? clock64() : 0;
   for (;;) {
     mbar_wait(&full[stage], phase);
@@ -816,6 +820,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
           }
         }
       }
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pe[0] += t - tc; tc = t; }
       if (run_apply) {
         if constexpr (PR) {
           bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
@@ -838,11 +843,16 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
               float pn[4], sp[4];
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
+#if PCPM_EPI_FAKE
+                pn[c] = (float)(uint32_t)total(4 * i4 + c) * 1e-9f + pov[c];
+                sp[c] = pn[c] * idv[c] * fscale;
+#else
                 const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
                 pn[c] = (float)prn;
                 sp[c] = pn[c] * idv[c] * fscale;        // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
                 dang += idv[c] != 0.0f ? 0ull : red_fx(prn);
                 res += red_fx(fabs(prn - (double)pov[c]));
+#endif
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
               if (FUSE && nsl == 1)                     // the next scatter's source values stay on chip
@@ -876,8 +886,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       }
       if (!SL)
         for (int64_t i = cnt + ctid; i < q; i += kCons) acc[i] = 0u;   // tail of a short last partition
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pe[1] += t - tc; tc = t; }
       if constexpr (PR) warp_red_add(a.red_fx, dang, res, lane, PCPM_GATHER_ITEM_FENCE != 0);
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pe[2] += t - tc; tc = t; }
       named_bar_sync(1, kCons);
+      if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pe[3] += t - tc; tc = t; }
       for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
       named_bar_sync(1, kCons);
       if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[3] += t - tc; tc = t; }
@@ -885,6 +898,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   }
   if (PCPM_GATHER_PROFILE && lane == 0) {
     for (int k = 0; k < 4; ++k) atomicAdd(&g_gather_prof[k], pt[k]);
+    for (int k = 0; k < 4; ++k) atomicAdd(&g_gather_prof[19 + k], pe[k]);
     atomicAdd(&g_gather_prof[4], 1ull);
   }
 

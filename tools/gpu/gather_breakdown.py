@@ -53,3 +53,6 @@ if c[11] > 0 and c[14] > 0:
           f"outside-loop={(c[9] - c[13]) / c[11]:.0f}")
 if c[11] > 0 and c[15] > 0:
     print(key, "producer batch start (cycles/batch):", f"loads={c[17] / c[15]:.0f} loads+prefetch={c[18] / c[15]:.0f}")
+if c[19] + c[20] > 0:
+    print(key, "epilogue split (share of decoder time):", " ".join(
+        f"{n}={c[19 + i] / tot:.3f}" for i, n in enumerate(["pre-apply", "apply", "reductions", "closing-barrier"])))
