@@ -132,9 +132,6 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 #ifndef PCPM_GATHER_NO_EPI
 #define PCPM_GATHER_NO_EPI 0
 #endif
-#ifndef PCPM_EPI_FAKE
-#define PCPM_EPI_FAKE 0              // timing-only experiment build (wrong results): fp32 apply, no reductions
-#endif
 #ifndef PCPM_GATHER_ITEM_FENCE
 #define PCPM_GATHER_ITEM_FENCE 0     // 1: fence after every item's reduction atomics (round-1 form, A/B)
 #endif
@@ -843,16 +840,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
               float pn[4], sp[4];
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-#if PCPM_EPI_FAKE
-                pn[c] = (float)(uint32_t)total(4 * i4 + c) * 1e-9f + pov[c];
-                sp[c] = pn[c] * idv[c] * fscale;
-#else
                 const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
                 pn[c] = (float)prn;
                 sp[c] = pn[c] * idv[c] * fscale;        // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
                 dang += idv[c] != 0.0f ? 0ull : red_fx(prn);
                 res += red_fx(fabs(prn - (double)pov[c]));
-#endif
               }
               pn4[i4] = make_float4(pn[0], pn[1], pn[2], pn[3]);
               if (FUSE && nsl == 1)                     // the next scatter's source values stay on chip
