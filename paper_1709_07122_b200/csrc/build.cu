@@ -1774,8 +1774,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       // the previous tile, which every thread has finished)
       if (tid == 0 && x1 < e1) issue_cols(cb ^ 1, x1, min(e1, x1 + kTileE));
       // ---- prep: columns, row marks
+      // (the count pass needs only the row-start bits: no per-edge row, no payload)
       uint32_t* mark = T.pay1;
-      for (int i = tid; i < kTileE; i += kTileThreads) mark[i] = 0u;
+      if (PLACE)
+        for (int i = tid; i < kTileE; i += kTileThreads) mark[i] = 0u;
       for (int i = tid; i < kTileE / 32; i += kTileThreads) T.sbits[i] = 0u;
       uint32_t* vfull = (cb ? T.colb1 : T.colb0) + (x0 & 3);   // vfull[i] = col[x0 + i]
       {
@@ -1790,7 +1792,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       mbar_wait(&cbar[cb], (cphase >> cb) & 1u);
       cphase ^= 1u << cb;
       __syncthreads();
-      if (tid == 0) mark[0] = rcur + 1;   // edges before the first row start belong to rcur
+      if (PLACE && tid == 0) mark[0] = rcur + 1;   // edges before the first row start belong to rcur
       for (uint32_t rb = rnext;; rb += kTileThreads) {
         const uint32_t r = rb + tid;
         int64_t rs = x1, re = x1;
@@ -1800,7 +1802,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
         }
         const bool in = r < sg.u1 && rs < x1;
         if (in && re > rs) {              // a non-empty row starting inside the tile
-          atomicMax(&mark[rs - x0], r + 1);
+          if (PLACE) atomicMax(&mark[rs - x0], r + 1);
           atomicOr(&T.sbits[(rs - x0) >> 5], 1u << ((rs - x0) & 31));
         }
         const int cnt = __syncthreads_count(in);
@@ -1812,7 +1814,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       __syncthreads();
       // block max-scan of the marks: element i's row (+1); warp-striped, 16 per thread; the 16
       // rounds are scanned independently, then chained by their maxima (ILP instead of a chain)
-      {
+      if (PLACE) {
         const int base = warp * (kTileE / kTileWarps);
         uint32_t loc[kTileItems];
 #pragma unroll
@@ -1840,12 +1842,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
       }
       __syncthreads();
       // carries for the next tile (the marks are overwritten by the payloads below)
-      if (tid == 0) T.wsum[kTileWarps * kRadixB + 2] = mark[n - 1] - 1u;
+      if (PLACE && tid == 0) T.wsum[kTileWarps * kRadixB + 2] = mark[n - 1] - 1u;
       // ---- per edge: bin, run flag, payload
       for (int i = tid; i < kTileE; i += kTileThreads) {
         if (i < n) {
           const uint32_t v = vfull[i];
-          const uint32_t u = mark[i] - 1u;
+          const uint32_t u = PLACE ? mark[i] - 1u : 0u;
           const bool first = (T.sbits[i >> 5] >> (i & 31)) & 1u;
           const uint32_t prv = i ? vfull[i - 1] : pv;
           uint32_t j = v >> b;
@@ -1857,14 +1859,15 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
           uint32_t prj = i ? (prv >> b) : pj;
           if (i && prj >= (uint32_t)k_dst) prj = (uint32_t)k_dst - 1;
           const bool flag = !COMPRESS || first || prj != j;
-          T.key0[i] = (uint16_t)j;
-          T.idx0[i] = (uint16_t)i;
-          T.pay0[i] = BV ? __float_as_uint(__ldg(ba.xval + u)) : (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
-          if (!PLACE) {
+          if (PLACE) {
+            T.key0[i] = (uint16_t)j;
+            T.idx0[i] = (uint16_t)i;
+            T.pay0[i] = BV ? __float_as_uint(__ldg(ba.xval + u)) : (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
+          } else {
             atomicAdd(&T.ci[j], 1u);
             if (flag) atomicAdd(&T.cr[j], 1u);
           }
-        } else {
+        } else if (PLACE) {
           T.key0[i] = 0xFFFFu;          // padding sorts last
           T.idx0[i] = 0;
           T.pay0[i] = 0u;
