@@ -2199,8 +2199,16 @@ struct BpUnit {
   uint32_t ci[32], cr[32];   // the 32 bins' first ID slot / first PNG slot for this segment
   uint32_t valid, pad[3];
 };
+// STAGED (compact layout, the default): a tile's destination IDs and PNG sources are first
+// written into shared memory grouped by bin (each bin's records contiguous, in rank order),
+// then copied out with consecutive threads writing consecutive slots of a bin (coalesced
+// 2-byte stores) instead of every lane storing into a different bin's range.
+#ifndef PCPM_BP_STAGED
+#define PCPM_BP_STAGED 1
+#endif
 size_t bucket_place_smem(bool weighted) {
-  return 2 * ((size_t)kBpTile + 2) * 8 + (weighted ? 2 * ((size_t)kBpTile + 4) * 4 : 0) + 2 * sizeof(BpUnit) + 64;
+  return 2 * ((size_t)kBpTile + 2) * 8 + (weighted ? 2 * ((size_t)kBpTile + 4) * 4 : 0) + 2 * sizeof(BpUnit) + 64 +
+         (PCPM_BP_STAGED ? (size_t)kBpTile * (2 + 2 + 1 + 1) : 0);
 }
 
 template <bool WIDE, bool WEIGHTED, bool BV = false>
@@ -2216,6 +2224,12 @@ __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
   float* wbuf = reinterpret_cast<float*>(rbuf + 2 * (kBpTile + 2));           // [2][kBpTile + 4]
   BpUnit* un = reinterpret_cast<BpUnit*>(reinterpret_cast<uint8_t*>(wbuf) + (WEIGHTED ? 2 * (kBpTile + 4) * 4 : 0));
   uint64_t* bar = reinterpret_cast<uint64_t*>(un + 2);                         // [2]
+  constexpr bool kStaged = PCPM_BP_STAGED && !WIDE && !BV;
+  uint16_t* stI = reinterpret_cast<uint16_t*>(bar + 8);                        // [kBpTile] staged IDs
+  uint16_t* stF = stI + kBpTile;                                               // [kBpTile] staged PNG sources
+  uint8_t* tgI = reinterpret_cast<uint8_t*>(stF + kBpTile);                    // [kBpTile] bin of staged ID
+  uint8_t* tgF = tgI + kBpTile;                                                // [kBpTile] bin of staged PNG
+  __shared__ uint32_t offI[33], offF[33], gI[32], gF[32];   // staged: per-bin tile offsets / global starts
   __shared__ uint32_t wI[kBpWarps][33], wF[kBpWarps][33];   // per-warp totals -> per-warp bases
   __shared__ uint32_t ciS[32], crS[32];                      // running ID / PNG slot of bin 32 h + l
   __shared__ uint32_t tile_s[4];                             // next tile: x0, unit slot, first-of-unit, valid
@@ -2341,7 +2355,40 @@ __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
     wI[warp][lane] = cI;
     wF[warp][lane] = cF;
     __syncthreads();
-    {
+    if (kStaged) {
+      // warp 0, lane = bin: per-warp bases within the bin's tile run, the bins' offsets in the
+      // staging arrays, their global starts; then the running slots advance
+      if (warp == 0) {
+        uint32_t rI = 0, rF = 0;
+#pragma unroll 4
+        for (int ww = 0; ww < kBpWarps; ++ww) {
+          const uint32_t a = wI[ww][lane], c = wF[ww][lane];
+          wI[ww][lane] = rI;
+          wF[ww][lane] = rF;
+          rI += a;
+          rF += c;
+        }
+        uint32_t sI = rI, sF = rF;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t yI = __shfl_up_sync(0xffffffffu, sI, o), yF = __shfl_up_sync(0xffffffffu, sF, o);
+          if (lane >= o) {
+            sI += yI;
+            sF += yF;
+          }
+        }
+        offI[lane] = sI - rI;
+        offF[lane] = sF - rF;
+        if (lane == 31) {
+          offI[32] = sI;
+          offF[32] = sF;
+        }
+        gI[lane] = ciS[lane];
+        gF[lane] = crS[lane];
+        ciS[lane] += rI;
+        crS[lane] += rF;
+      }
+    } else {
       // bins kBpB w .. kBpB w + kBpB - 1: exclusive scans of the kBpWarps warps' counts
       // (segments of kBpWarps lanes), plus the bins' running slots
       constexpr int kBpB = 32 / kBpWarps;            // bins per warp
@@ -2368,6 +2415,36 @@ __global__ void __launch_bounds__(kBpThreads, PCPM_BP_CTAS) k_bucket_place(
       }
     }
     __syncthreads();
+    if (kStaged) {
+#pragma unroll
+      for (int k = 0; k < kBpItems; ++k) {
+        if (rc[k] != ~0ull) {
+          const uint32_t jl = (uint32_t)(rc[k] >> 32), pw = (uint32_t)rc[k];
+          const uint32_t si = offI[jl] + wI[warp][jl] + (rk[k] & 0xFFFFu);
+          stI[si] = (uint16_t)(pw & 0xFFFFu);
+          tgI[si] = (uint8_t)jl;
+          if (WEIGHTED) w[gI[jl] + wI[warp][jl] + (rk[k] & 0xFFFFu)] = wsv[base + 32 * k + lane];
+          if (pw & 0x8000u) {
+            const uint32_t sf = offF[jl] + wF[warp][jl] + (rk[k] >> 16);
+            stF[sf] = (uint16_t)(pw >> 16);
+            tgF[sf] = (uint8_t)jl;
+          }
+        }
+      }
+      __syncthreads();
+      const uint32_t nI = offI[32], nF = offF[32];
+      for (uint32_t x = tid; x < nI; x += kBpThreads) {
+        const uint32_t jl = tgI[x];
+        ids16[gI[jl] + (x - offI[jl])] = stI[x];
+      }
+      for (uint32_t x = tid; x < nF; x += kBpThreads) {
+        const uint32_t jl = tgF[x];
+        png16[gF[jl] + (x - offF[jl])] = stF[x];
+      }
+      __syncthreads();                               // staging / wI / wF / this buffer are reused
+      bf ^= 1;
+      continue;
+    }
 #pragma unroll
     for (int k = 0; k < kBpItems; ++k) {
       if (rc[k] != ~0ull) {
