@@ -1762,6 +1762,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
     }
     const int64_t e0 = row_ptr[sg.u0], e1 = row_ptr[sg.u1];
     uint32_t rnext = sg.u0;               // first row whose start is >= the tile's first edge
+    uint32_t pbase = 0xFFFFFFFFu;         // rows pbase + tid: row starts prefetched in prs / pre
+    int64_t prs = 0, pre = 0;
     uint32_t rcur = sg.u0;                // row of the edge before the tile
     uint32_t pj = 0xFFFFFFFFu, pv = 0;    // bin / column of the edge before the tile
     int cb = 0;                           // column buffer of the current tile
@@ -1797,8 +1799,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
         const uint32_t r = rb + tid;
         int64_t rs = x1, re = x1;
         if (r < sg.u1) {
-          rs = row_ptr[r];
-          re = row_ptr[r + 1];
+          if (rb == pbase) {                // loaded during the previous tile
+            rs = prs;
+            re = pre;
+          } else {
+            rs = row_ptr[r];
+            re = row_ptr[r + 1];
+          }
         }
         const bool in = r < sg.u1 && rs < x1;
         if (in && re > rs) {              // a non-empty row starting inside the tile
@@ -1810,6 +1817,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
           rnext = rb + cnt;
           break;
         }
+      }
+      // the next tile's first round of row starts, loaded now (consumed one tile later)
+      pbase = rnext;
+      if (rnext + tid < sg.u1) {
+        prs = row_ptr[rnext + tid];
+        pre = row_ptr[rnext + tid + 1];
       }
       __syncthreads();
       // block max-scan of the marks: element i's row (+1); warp-striped, 16 per thread; the 16
