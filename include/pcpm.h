@@ -273,7 +273,9 @@ int pcpm_scatter(pcpm_handle* h, const float* x);
  * gather applies each finished partition itself, the default; 2: k_gather2, which parks
  * the partition's accumulator in tensor memory and lets 4 dedicated warps apply it
  * while 27 warps decode the next one -- measured slower), "scatter_lpt",
- * "scatter_prefetch", "gather_prefetch", "epilogue_prefetch" (kernel variants:
+ * "scatter_prefetch", "gather_prefetch", "epilogue_prefetch", "cluster_gather", "pdl"
+ * (1, default: the scatter and gather are launched as programmatic dependents, so a
+ * kernel's prologue overlaps its predecessor's tail; 0: plain stream order) (kernel variants:
  * every one computes the same result) and "weighted_pagerank" (1: pcpm_pagerank
  * uses the edge values as weights, u passing PR(u) w(u,v) / W(u) to v with
  * W(u) = sum of u's weights (reading R24); needs a non-shard handle

@@ -895,6 +895,11 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     free_graph(h);
     return PCPM_OK;
   }
+  if (!strcmp(key, "pdl")) {
+    h->opt_pdl = value ? 1 : 0;
+    free_graph(h);
+    return PCPM_OK;
+  }
   if (!strcmp(key, "gather_prefetch")) {
     if (value < 0 || value > 16) {
       set_error(PCPM_EINVAL, "gather_prefetch must be in [0, 16]");

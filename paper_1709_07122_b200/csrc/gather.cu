@@ -248,6 +248,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
     __syncwarp();
     advance();
   };
+  pdl_wait();                                      // the update bins (scatter) are complete
   uint32_t it = claim();
   GatherItem item{};
   if (it < (uint32_t)a.n_items) item = a.items[it];
@@ -624,6 +625,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_trigger();
 
   if (warp < NP) {
     gather_producer<C, IdT, W, PR, SL, FUSE, NP>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar);
@@ -642,6 +644,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   const double inv_scale = 1.0 / (double)fscale;
   for (int64_t i = ctid; i < aw; i += kCons) acc[i] = 0u;
   for (int i = ctid; i < bm_words; i += kCons) bitmap[i] = 0u;
+  pdl_wait();                                      // D_t (red_in) and the scatter's bins are complete
   double base_pr = 0.0;
   if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
   // SpMV scale: F = 30 - ceil(log2 max|w|) - ceil(log2 max|x|), so |w x| 2^F <= 2^30
@@ -1378,6 +1381,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W>::kThreads, 1) k_gather_cl(const Ga
   for (int64_t i = threadIdx.x; i < q; i += blockDim.x) acc[i] = 0u;
   for (int i = threadIdx.x; i < bm_words; i += blockDim.x) bitmap[i] = 0u;
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();
   if (warp < NP) {
     gather_producer<C, IdT, W, PR, false, false, NP>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar);
   } else {
@@ -1747,13 +1752,18 @@ int launch_gather_cl(pcpm_handle* h, const GatherArgs& a0, bool weighted, bool p
   cfg.blockDim = dim3(gather_threads(h->wide, weighted));
   cfg.dynamicSmemBytes = gather_cl_smem_bytes(a.b, h->wide, weighted);
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)h->cl_cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (h->opt_pdl) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   if (getenv("PCPM_DEBUG_CLUSTER")) {          // how many clusters fit at once (A/B diagnostics)
     int ncl = 0;
     cudaOccupancyMaxActiveClusters(&ncl, (const void*)gather_cl_fn(h->wide, weighted, pagerank), &cfg);
@@ -1787,9 +1797,8 @@ int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pager
   }
   const int smem = slots ? smem_bytes_for<uint16_t, false, true>(a.b, a.acc_words) : gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
-  gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted, slots)<<<grid, gather_threads(h->wide, weighted),
-                                                                                smem, s>>>(a);
-  PCPM_CK(cudaGetLastError());
+  PCPM_CK(launch_k(h->opt_pdl != 0, gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted, slots), grid,
+                   gather_threads(h->wide, weighted), smem, s, a));
   h->launches += 1;
   return launch_apply_split(h, a, pagerank, s);     // split bins (small k), if any
 }

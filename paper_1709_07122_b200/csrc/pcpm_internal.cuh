@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -154,6 +155,7 @@ struct pcpm_handle {
   int opt_use_graph = 1;
   int opt_gather_variant = 1;
   int opt_cluster_gather = 1;       // 1: k_gather_cl for graphs with few partitions (when built), 0: off
+  int opt_pdl = 1;                  // 1: scatter / gather / apply launched as programmatic dependents
   int opt_fuse = 0;                 // 1: gather + next scatter fused (PageRank, compact, square, not shard; measured slower), 0: off
   bool last_fused = false;          // the last pcpm_pagerank ran the fused iteration       // 1: in-line epilogue (k_gather), 2: apply overlapped through tensor memory (k_gather2)
   int opt_gather_pf = 2;            // gather: tiles prefetched into L2 ahead of the ring (0 = off)
@@ -236,6 +238,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic stream
+// serialization attribute may start while its predecessor drains; pdl_wait() blocks until
+// the predecessor grid has completed and its memory is visible (a no-op otherwise), and
+// pdl_trigger() lets this grid's dependents start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -294,6 +302,22 @@ constexpr double kRedScale = 4611686018427387904.0;     // 2^62
 __device__ __forceinline__ unsigned long long red_fx(double x) { return __double2ull_rn(x * kRedScale); }
 
 // ---------------------------------------------------------------- launchers
+// <<<grid, block, smem, s>>>(args...) with the PDL attribute when pdl is set
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 struct GatherArgs {
   const void* ids;         // uint16_t* (compact) or uint32_t* (wide)
   const uint16_t* slot16;  // accumulator slots (PCPM_COMPACT_SLOTS) or null

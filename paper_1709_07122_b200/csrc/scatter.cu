@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
     fence_mbar_init();
   }
   __syncthreads();
+  pdl_trigger();
+  pdl_wait();                                      // x (the previous gather's SPR) is complete
 
   if (warp == 0) {
     // ================= producer =================
@@ -483,11 +485,13 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out, b
     const int smem = scatter_tma_smem_bytes(h->b);
     const bool xg = h->opt_scatter_variant == 2, vec = h->opt_scatter_variant == 3;
     if (h->wide)
-      (xg ? k_scatter_tma<uint32_t, true> : vec ? k_scatter_tma<uint32_t, false, true> : k_scatter_tma<uint32_t>)
-          <<<grid, ScCfg<uint32_t>::kThreads, smem, s>>>(a);
+      PCPM_CK(launch_k(h->opt_pdl != 0,
+                       xg ? k_scatter_tma<uint32_t, true> : vec ? k_scatter_tma<uint32_t, false, true> : k_scatter_tma<uint32_t>,
+                       grid, ScCfg<uint32_t>::kThreads, smem, s, a));
     else
-      (xg ? k_scatter_tma<uint16_t, true> : vec ? k_scatter_tma<uint16_t, false, true> : k_scatter_tma<uint16_t>)
-          <<<grid, ScCfg<uint16_t>::kThreads, smem, s>>>(a);
+      PCPM_CK(launch_k(h->opt_pdl != 0,
+                       xg ? k_scatter_tma<uint16_t, true> : vec ? k_scatter_tma<uint16_t, false, true> : k_scatter_tma<uint16_t>,
+                       grid, ScCfg<uint16_t>::kThreads, smem, s, a));
   }
   PCPM_CK(cudaGetLastError());
   h->launches += 1;
