@@ -1650,17 +1650,30 @@ struct TileSmem {           // carved from dynamic shared memory (k_dst-sized ar
   uint32_t *colb0, *colb1;  // [kTileE + 8] the tile's columns (bulk-copied one tile ahead)
 };
 
-size_t tile_smem_bytes(int64_t k_dst) {
+// count_only (pass 1): the counts, row-start bits, scan scratch and column buffers only
+// (~85 KB at k = 2048), so two CTAs share an SM and hide each other's barrier waits
+size_t tile_smem_bytes(int64_t k_dst, bool count_only = false) {
   const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
+  if (count_only)
+    return kd * 4 * 2 + kTileE / 32 * 4 + (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileE + 8) * 4 + 64;
   return kd * 4 * 2 + kd * 2 * 2 + (size_t)kTileE * (2 + 4 + 2) * 2 + kTileE / 32 * 4 +
          (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileE + 8) * 4 + 64;
 }
 
-__device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst) {
+__device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst, bool count_only = false) {
   const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
   TileSmem t;
   t.ci = reinterpret_cast<uint32_t*>(base);
   t.cr = t.ci + kd;
+  if (count_only) {
+    t.sbits = t.cr + kd;
+    t.wsum = t.sbits + kTileE / 32;
+    t.colb0 = t.wsum + kTileWarps * kRadixB + 64;
+    t.colb1 = t.colb0 + kTileE + 8;
+    t.pay0 = t.pay1 = nullptr;
+    t.key0 = t.key1 = t.idx0 = t.idx1 = t.bstart = t.bfstart = nullptr;
+    return t;
+  }
   t.pay0 = t.cr + kd;
   t.pay1 = t.pay0 + kTileE;
   t.sbits = t.pay1 + kTileE;
@@ -1692,14 +1705,14 @@ struct BucketArgs {
 // BV (with BUCKET; the BVGAS engine's per-iteration scatter, Alg. 3): the record
 // carries the source value x[u] instead of the layout payload; no validation.
 template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED, bool BUCKET = false, bool BV = false>
-__global__ void __launch_bounds__(kTileThreads, 1) k_tile_pass(
+__global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
     const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
     const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst, int kbits,
     uint32_t* CI, uint32_t* CR, const uint32_t* __restrict__ G, uint32_t* outdeg, float* inv_deg,
     unsigned long long* n_dang, uint32_t* err, uint16_t* ids16, uint32_t* ids32, float* w, uint16_t* png16,
     uint32_t* png32, const BucketArgs ba) {
   extern __shared__ __align__(16) uint8_t tsm[];
-  const TileSmem T = tile_carve(tsm, k_dst);
+  const TileSmem T = tile_carve(tsm, k_dst, !PLACE);
   const int tid = threadIdx.x;
   __shared__ uint32_t seg_s;
   __shared__ __align__(8) uint64_t cbar[2];
@@ -2708,7 +2721,7 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   } else {
-    TK(cudaFuncSetAttribute(tcnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TK(cudaFuncSetAttribute(tcnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem_bytes(k_dst, true)));
     TK(cudaFuncSetAttribute(tplace_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
   const int grid = warp_mode
@@ -2721,7 +2734,8 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
                                               nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr, nullptr,
                                               nullptr, nullptr);
   else
-    tcnt_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+    tcnt_fn<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(n_seg, 2 * h->num_sms)), kTileThreads,
+              tile_smem_bytes(k_dst, true), s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
                                              CI, CR, nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, BucketArgs{});
   TK(cudaGetLastError());
