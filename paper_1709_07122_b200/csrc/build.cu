@@ -1631,8 +1631,15 @@ __global__ void __launch_bounds__(32 * kCntWarps) k_seg_pass(
 //            whole sectors while they are still in L2 (148 CTAs x k_dst open sectors,
 //            ~10 MB, instead of one open sector per (warp, bin)).
 constexpr int kTileThreads = 512, kTileWarps = kTileThreads / 32;
-constexpr int kTileE = 8192;                        // edges per tile
-constexpr int kTileItems = kTileE / kTileThreads;   // 16 per thread, warp-striped: element w*512 + l + 32 k
+#ifndef PCPM_TILE_E
+#define PCPM_TILE_E 4096
+#endif
+#ifndef PCPM_TILE_BUCKET_CTAS
+#define PCPM_TILE_BUCKET_CTAS 2      // CTAs per SM of the bucket pass (2 needs PCPM_TILE_E <= 4096)
+#endif
+constexpr int kTileE = PCPM_TILE_E;                 // edges per tile
+constexpr int kTileItems = kTileE / kTileThreads;   // 8 per thread, warp-striped: element w*512 + l + 32 k
+constexpr int kTileECnt = 8192;                      // edges per tile of the count pass
 constexpr int kRadixBits = 4, kRadixB = 1 << kRadixBits;
 
 struct TileSmem {           // carved from dynamic shared memory (k_dst-sized arrays first)
@@ -1650,26 +1657,43 @@ struct TileSmem {           // carved from dynamic shared memory (k_dst-sized ar
   uint32_t *colb0, *colb1;  // [kTileE + 8] the tile's columns (bulk-copied one tile ahead)
 };
 
-// count_only (pass 1): the counts, row-start bits, scan scratch and column buffers only
-// (~85 KB at k = 2048), so two CTAs share an SM and hide each other's barrier waits
-size_t tile_smem_bytes(int64_t k_dst, bool count_only = false) {
+// mode 1 (pass 1, count): the counts, row-start bits, scan scratch and column buffers only;
+// mode 2 (bucket pass): 64 bucket slots, keys, payloads, marks, tags, bits, scratch, columns.
+// Both fit twice per SM (two CTAs hide each other's barrier waits); mode 0: everything.
+size_t tile_smem_bytes(int64_t k_dst, int mode = 0) {
   const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
-  if (count_only)
-    return kd * 4 * 2 + kTileE / 32 * 4 + (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileE + 8) * 4 + 64;
+  if (mode == 1)
+    return kd * 4 * 2 + kTileECnt / 32 * 4 + (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileECnt + 8) * 4 + 64;
+  if (mode == 2)
+    return 64 * 4 + (size_t)kTileE * (4 + 4 + 2 + 2) + kTileE / 32 * 4 + (kTileWarps * kRadixB + 64) * 4 +
+           2 * ((size_t)kTileE + 8) * 4 + 64;
   return kd * 4 * 2 + kd * 2 * 2 + (size_t)kTileE * (2 + 4 + 2) * 2 + kTileE / 32 * 4 +
          (kTileWarps * kRadixB + 64) * 4 + 2 * ((size_t)kTileE + 8) * 4 + 64;
 }
 
-__device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst, bool count_only = false) {
+__device__ __forceinline__ TileSmem tile_carve(uint8_t* base, int64_t k_dst, int mode = 0) {
   const size_t kd = (size_t)((k_dst + 3) & ~int64_t(3));
   TileSmem t;
   t.ci = reinterpret_cast<uint32_t*>(base);
-  t.cr = t.ci + kd;
-  if (count_only) {
-    t.sbits = t.cr + kd;
+  if (mode == 2) {
+    t.cr = nullptr;
+    t.pay0 = t.ci + 64;
+    t.pay1 = t.pay0 + kTileE;
+    t.sbits = t.pay1 + kTileE;
     t.wsum = t.sbits + kTileE / 32;
     t.colb0 = t.wsum + kTileWarps * kRadixB + 64;
     t.colb1 = t.colb0 + kTileE + 8;
+    t.key0 = reinterpret_cast<uint16_t*>(t.colb1 + kTileE + 8);
+    t.idx0 = t.key0 + kTileE;
+    t.key1 = t.idx1 = t.bstart = t.bfstart = nullptr;
+    return t;
+  }
+  t.cr = t.ci + kd;
+  if (mode == 1) {
+    t.sbits = t.cr + kd;
+    t.wsum = t.sbits + kTileECnt / 32;
+    t.colb0 = t.wsum + kTileWarps * kRadixB + 64;
+    t.colb1 = t.colb0 + kTileECnt + 8;
     t.pay0 = t.pay1 = nullptr;
     t.key0 = t.key1 = t.idx0 = t.idx1 = t.bstart = t.bfstart = nullptr;
     return t;
@@ -1705,14 +1729,17 @@ struct BucketArgs {
 // BV (with BUCKET; the BVGAS engine's per-iteration scatter, Alg. 3): the record
 // carries the source value x[u] instead of the layout payload; no validation.
 template <bool PLACE, bool COMPRESS, bool WIDE, bool WEIGHTED, bool BUCKET = false, bool BV = false>
-__global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
+__global__ void __launch_bounds__(kTileThreads, BUCKET ? PCPM_TILE_BUCKET_CTAS : (PLACE ? 1 : 2)) k_tile_pass(
     const BSeg* __restrict__ segs, int n_seg, uint32_t* seg_ctr, const int64_t* __restrict__ row_ptr,
     const uint32_t* __restrict__ col, const float* __restrict__ val, int b, int64_t k_dst, int64_t n_dst, int kbits,
     uint32_t* CI, uint32_t* CR, const uint32_t* __restrict__ G, uint32_t* outdeg, float* inv_deg,
     unsigned long long* n_dang, uint32_t* err, uint16_t* ids16, uint32_t* ids32, float* w, uint16_t* png16,
     uint32_t* png32, const BucketArgs ba) {
+  // the count pass walks 8192-edge tiles (two CTAs per SM), the placing passes kTileE
+  constexpr int TE = PLACE ? kTileE : kTileECnt;
+  constexpr int TI = TE / kTileThreads;
   extern __shared__ __align__(16) uint8_t tsm[];
-  const TileSmem T = tile_carve(tsm, k_dst, !PLACE);
+  const TileSmem T = tile_carve(tsm, k_dst, !PLACE ? 1 : (BUCKET ? 2 : 0));
   const int tid = threadIdx.x;
   __shared__ uint32_t seg_s;
   __shared__ __align__(8) uint64_t cbar[2];
@@ -1780,20 +1807,20 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
     uint32_t rcur = sg.u0;                // row of the edge before the tile
     uint32_t pj = 0xFFFFFFFFu, pv = 0;    // bin / column of the edge before the tile
     int cb = 0;                           // column buffer of the current tile
-    if (tid == 0 && e0 < e1) issue_cols(0, e0, min(e1, e0 + kTileE));
+    if (tid == 0 && e0 < e1) issue_cols(0, e0, min(e1, e0 + TE));
     __syncthreads();
-    for (int64_t x0 = e0; x0 < e1; x0 += kTileE, cb ^= 1) {
-      const int n = (int)min((int64_t)kTileE, e1 - x0);
+    for (int64_t x0 = e0; x0 < e1; x0 += TE, cb ^= 1) {
+      const int n = (int)min((int64_t)TE, e1 - x0);
       const int64_t x1 = x0 + n;
       // next tile's columns in flight under this tile's work (its buffer was last read by
       // the previous tile, which every thread has finished)
-      if (tid == 0 && x1 < e1) issue_cols(cb ^ 1, x1, min(e1, x1 + kTileE));
+      if (tid == 0 && x1 < e1) issue_cols(cb ^ 1, x1, min(e1, x1 + TE));
       // ---- prep: columns, row marks
       // (the count pass needs only the row-start bits: no per-edge row, no payload)
       uint32_t* mark = T.pay1;
       if (PLACE)
-        for (int i = tid; i < kTileE; i += kTileThreads) mark[i] = 0u;
-      for (int i = tid; i < kTileE / 32; i += kTileThreads) T.sbits[i] = 0u;
+        for (int i = tid; i < TE; i += kTileThreads) mark[i] = 0u;
+      for (int i = tid; i < TE / 32; i += kTileThreads) T.sbits[i] = 0u;
       uint32_t* vfull = (cb ? T.colb1 : T.colb0) + (x0 & 3);   // vfull[i] = col[x0 + i]
       {
         const int64_t a = (x0 + 3) & ~int64_t(3), c = x1 & ~int64_t(3);
@@ -1841,20 +1868,20 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
       // block max-scan of the marks: element i's row (+1); warp-striped, 16 per thread; the 16
       // rounds are scanned independently, then chained by their maxima (ILP instead of a chain)
       if (PLACE) {
-        const int base = warp * (kTileE / kTileWarps);
-        uint32_t loc[kTileItems];
+        const int base = warp * (TE / kTileWarps);
+        uint32_t loc[TI];
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) loc[k] = mark[base + 32 * k + lane];
+        for (int k = 0; k < TI; ++k) loc[k] = mark[base + 32 * k + lane];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
-          for (int k = 0; k < kTileItems; ++k) {
+          for (int k = 0; k < TI; ++k) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, loc[k], o);
             if (lane >= o) loc[k] = max(loc[k], y);
           }
         uint32_t mx = 0;
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const uint32_t top = __shfl_sync(0xffffffffu, loc[k], 31);
           loc[k] = max(loc[k], mx);
           mx = max(mx, top);
@@ -1864,13 +1891,13 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         uint32_t before = 0;
         for (int ww = 0; ww < warp; ++ww) before = max(before, T.wsum[ww]);
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) mark[base + 32 * k + lane] = max(loc[k], before);
+        for (int k = 0; k < TI; ++k) mark[base + 32 * k + lane] = max(loc[k], before);
       }
       __syncthreads();
       // carries for the next tile (the marks are overwritten by the payloads below)
       if (PLACE && tid == 0) T.wsum[kTileWarps * kRadixB + 2] = mark[n - 1] - 1u;
       // ---- per edge: bin, run flag, payload
-      for (int i = tid; i < kTileE; i += kTileThreads) {
+      for (int i = tid; i < TE; i += kTileThreads) {
         if (i < n) {
           const uint32_t v = vfull[i];
           const uint32_t u = PLACE ? mark[i] - 1u : 0u;
@@ -1887,7 +1914,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
           const bool flag = !COMPRESS || first || prj != j;
           if (PLACE) {
             T.key0[i] = (uint16_t)j;
-            T.idx0[i] = (uint16_t)i;
+            if (!BUCKET) T.idx0[i] = (uint16_t)i;
             T.pay0[i] = BV ? __float_as_uint(__ldg(ba.xval + u)) : (v & qmask) | (flag ? 0x8000u : 0u) | ((u & qmask) << 16);
           } else {
             atomicAdd(&T.ci[j], 1u);
@@ -1924,11 +1951,11 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         // SB's running slot + base + rank.
         constexpr int kWs = 65;                       // padded stride of the per-warp totals
         uint32_t* wc = T.pay1;                        // [kTileWarps][kWs] (the row marks are consumed)
-        const int base = warp * (kTileE / kTileWarps);
-        uint32_t rk[kTileItems];
+        const int base = warp * (TE / kTileWarps);
+        uint32_t rk[TI];
         uint32_t c_lo = 0, c_hi = 0;
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const int i = base + 32 * k + lane;
           const bool ok = i < n;
           const uint32_t hb = ok ? (uint32_t)(T.key0[i] >> 5) : 0u;
@@ -1971,7 +1998,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const int i = base + 32 * k + lane;
           if (i < n) {
             const uint32_t j = T.key0[i];
@@ -1993,14 +2020,14 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         uint16_t* kout = cur ? T.key0 : T.key1;
         uint32_t* pout = cur ? T.pay0 : T.pay1;
         uint16_t* iout = cur ? T.idx0 : T.idx1;
-        const int base = warp * (kTileE / kTileWarps);
-        uint32_t rnk[kTileItems];
-        uint32_t dig[kTileItems];
+        const int base = warp * (TE / kTileWarps);
+        uint32_t rnk[TI];
+        uint32_t dig[TI];
         uint32_t cnt = 0;                         // lane d < 16: this warp's count of digit d
         const uint32_t dd = lane & (kRadixB - 1);
         // rounds are independent: ballots per round, then lane dd's running count of digit dd
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const uint32_t d = (kin[base + 32 * k + lane] >> sh) & (kRadixB - 1);
           uint32_t peers = 0xffffffffu, mdd = 0xffffffffu;   // lanes with my digit / with digit dd
 #pragma unroll
@@ -2014,7 +2041,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
           cnt += __popc(mdd);
         }
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k)
+        for (int k = 0; k < TI; ++k)
           rnk[k] = __shfl_sync(0xffffffffu, rnk[k] & 0xFFFFu, dig[k]) + (rnk[k] >> 16);
         if (lane >= kRadixB) cnt = 0;
         // warp totals per digit -> block bases: base(w, d) = sum_{d' < d} total(d') + sum_{w' < w} cnt(w', d)
@@ -2043,7 +2070,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         __syncthreads();
         const int nxt = cur ^ 1;
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const int src = base + 32 * k + lane;
           const uint32_t dst = T.wsum[dig[k] * kTileWarps + warp] + rnk[k];
           kout[dst] = kin[src];
@@ -2058,11 +2085,11 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         const uint16_t* ks = cur ? T.key1 : T.key0;
         const uint32_t* ps = cur ? T.pay1 : T.pay0;
         const uint16_t* is = cur ? T.idx1 : T.idx0;
-        const int base = warp * (kTileE / kTileWarps);
-        uint32_t fpre[kTileItems];
+        const int base = warp * (TE / kTileWarps);
+        uint32_t fpre[TI];
         uint32_t fw = 0;
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const uint32_t f = (ps[base + 32 * k + lane] >> 15) & 1u;
           const uint32_t bal = __ballot_sync(0xffffffffu, f);
           fpre[k] = fw + __popc(bal & lt);
@@ -2074,7 +2101,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         for (int ww = 0; ww < warp; ++ww) fbase += T.wsum[ww];
         // run starts: bstart[j] = first sorted index of j, bfstart[j] = flags before it
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const int i = base + 32 * k + lane;
           if (i < n) {
             const uint32_t j = ks[i];
@@ -2085,9 +2112,9 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
           }
         }
         __syncthreads();
-        uint32_t nci[kTileItems], ncr[kTileItems];
+        uint32_t nci[TI], ncr[TI];
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k) {
+        for (int k = 0; k < TI; ++k) {
           const int i = base + 32 * k + lane;
           nci[k] = ncr[k] = 0xFFFFFFFFu;
           if (i < n) {
@@ -2112,7 +2139,7 @@ __global__ void __launch_bounds__(kTileThreads, PLACE ? 1 : 2) k_tile_pass(
         }
         __syncthreads();
 #pragma unroll
-        for (int k = 0; k < kTileItems; ++k)
+        for (int k = 0; k < TI; ++k)
           if (nci[k] != 0xFFFFFFFFu) {
             const uint32_t j = ks[base + 32 * k + lane];
             T.ci[j] = nci[k];
@@ -2721,8 +2748,9 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     TK(cudaFuncSetAttribute(cnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TK(cudaFuncSetAttribute(place_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   } else {
-    TK(cudaFuncSetAttribute(tcnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem_bytes(k_dst, true)));
-    TK(cudaFuncSetAttribute(tplace_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TK(cudaFuncSetAttribute(tcnt_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem_bytes(k_dst, 1)));
+    TK(cudaFuncSetAttribute(tplace_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tile_smem_bytes(k_dst, two_level ? 2 : 0)));
   }
   const int grid = warp_mode
                        ? (int)std::max<int64_t>(1, std::min<int64_t>((n_seg + kCntWarps - 1) / kCntWarps, h->num_sms))
@@ -2735,7 +2763,7 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
                                               nullptr, nullptr);
   else
     tcnt_fn<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(n_seg, 2 * h->num_sms)), kTileThreads,
-              tile_smem_bytes(k_dst, true), s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+              tile_smem_bytes(k_dst, 1), s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
                                              CI, CR, nullptr, h->outdeg, h->inv_deg, d_dang, err, nullptr, nullptr,
                                              nullptr, nullptr, nullptr, BucketArgs{});
   TK(cudaGetLastError());
@@ -2807,7 +2835,9 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     ba.nbk = nbk;
     TK(cudaMemsetAsync(nhl, 0, 16, s));
     k_seg_buckets<<<(unsigned)n_seg, 1024, 0, s>>>(n_seg, k_dst, nbk, d_segs, row_ptr, CI, h->bin_id_start, SB);
-    tplace_fn<<<grid, kTileThreads, smem, s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst, n_dst, kbits,
+    tplace_fn<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(n_seg, PCPM_TILE_BUCKET_CTAS * h->num_sms)),
+                kTileThreads, tile_smem_bytes(k_dst, 2), s>>>(d_segs, (int)n_seg, ctr, row_ptr, col, values, b, k_dst,
+                                                              n_dst, kbits,
                                                CI, CR, G, nullptr, nullptr, nullptr, nullptr, h->ids16, ids32, h->w,
                                                h->png16, h->wide ? h->png_src : nullptr, ba);
     TK(cudaGetLastError());
@@ -2920,11 +2950,11 @@ int launch_bvgas_scatter(pcpm_handle* h, const float* x, cudaStream_t s) {
   ba.upd = h->upd;
   const int64_t n_units = h->bv_nseg * h->bv_nbk;
   const int kbits = std::max(1, bits_for((uint64_t)std::max<int64_t>(h->k_dst - 1, 0)));
-  const size_t smem = tile_smem_bytes(h->k_dst);
+  const size_t smem = tile_smem_bytes(h->k_dst, 2);
   TilePassFn f = k_tile_pass<true, false, false, false, true, true>;
   PCPM_CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const BSeg* segs = static_cast<const BSeg*>(h->bv_segs);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->bv_nseg, h->num_sms));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(h->bv_nseg, PCPM_TILE_BUCKET_CTAS * h->num_sms));
   PCPM_CK(cudaMemsetAsync(h->bv_nhl + 2, 0, 8, s));
   f<<<grid, kTileThreads, smem, s>>>(segs, (int)h->bv_nseg, h->bv_nhl + 2, h->bv_rp, h->bv_col, nullptr, h->b,
                                      h->k_dst, h->n_dst, kbits, nullptr, nullptr, nullptr, nullptr, nullptr,
