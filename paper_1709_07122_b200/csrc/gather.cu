@@ -132,6 +132,9 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 #ifndef PCPM_GATHER_NO_EPI
 #define PCPM_GATHER_NO_EPI 0
 #endif
+#ifndef PCPM_CARRY_CC
+#define PCPM_CARRY_CC 1              // carry test with add.cc / addc (A/B: 0 = NOT + compare)
+#endif
 #ifndef PCPM_GATHER_ITEM_FENCE
 #define PCPM_GATHER_ITEM_FENCE 0     // 1: fence after every item's reduction atomics (round-1 form, A/B)
 #endif
@@ -518,8 +521,22 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
         // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
         // ok = false have lo = hi = 0 (val = 0) and never carry
         uint32_t any = 0;
+#if PCPM_CARRY_CC
+        // carry-outs of old + lo counted with add.cc / addc (one add and one add-with-carry
+        // per step instead of a NOT and a compare), OR-ed with the high parts
+        static_assert(P == 4, "four steps per sub-chunk");
+        asm("{\n\t.reg .u32 t;\n\t"
+            "add.cc.u32 t, %1, %2;\n\taddc.u32 %0, 0, 0;\n\t"
+            "add.cc.u32 t, %3, %4;\n\taddc.u32 %0, %0, 0;\n\t"
+            "add.cc.u32 t, %5, %6;\n\taddc.u32 %0, %0, 0;\n\t"
+            "add.cc.u32 t, %7, %8;\n\taddc.u32 %0, %0, 0;\n\t}"
+            : "=r"(any)
+            : "r"(old[0]), "r"(tlo[0]), "r"(old[1]), "r"(tlo[1]), "r"(old[2]), "r"(tlo[2]), "r"(old[3]), "r"(tlo[3]));
+        any |= thi[0] | thi[1] | thi[2] | thi[3];
+#else
 #pragma unroll
         for (int c = 0; c < P; ++c) any |= thi[c] | (tlo[c] > ~old[c] ? 1u : 0u);
+#endif
         if (any) {                                   // rare: carry into the global high word
 #pragma unroll
           for (int c = 0; c < P; ++c) {
