@@ -474,12 +474,10 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
   const float* win_s = reinterpret_cast<const float*>(sb + C::kIdsBytes);
   const float* w_s = reinterpret_cast<const float*>(sb + C::kIdsBytes + C::kWinBytes);
   const uint32_t* cb_s = reinterpret_cast<const uint32_t*>(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes);
-  auto process = [&](const int sc) {
-  const uint32_t xs = m.tile_base + sc * C::kSub;        // first ID position of the sub-chunk
-  if (!PCPM_GATHER_NOOP && xs < m.hi && xs + C::kSub > m.lo) {
-    const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
-    auto body = [&](auto WHOLE) {
+  const uint32_t acc_s = smem_u32(acc);     // 32-bit shared address of the accumulator (ATOMS operand)
+    auto body = [&](const int sc, auto WHOLE) {
       constexpr bool kWhole = decltype(WHOLE)::value;
+      const uint32_t xs = m.tile_base + sc * C::kSub;      // first ID position of the sub-chunk
       // lane-strided decode: step c covers the 32 consecutive IDs c*32 .. c*32+31
       // of the sub-chunk, so the window reads of a step hit ~32/r consecutive
       // words (one or two smem wavefronts)
@@ -517,7 +515,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
           thi[c] = (uint32_t)(T >> 32);
         }
 #pragma unroll
-        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atoms_add_u32(acc_s + ((id[c] & qmask) << 2), tlo[c]) : 0u;
         // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
         // ok = false have lo = hi = 0 (val = 0) and never carry
         uint32_t any = 0;
@@ -565,7 +563,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
           thi[c] = 0;
         }
 #pragma unroll
-        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atomicAdd(&acc[id[c] & qmask], tlo[c]) : 0u;
+        for (int c = 0; c < P; ++c) old[c] = ok[c] ? atoms_add_u32(acc_s + ((id[c] & qmask) << 2), tlo[c]) : 0u;
         uint32_t any = 0;
         int32_t hinc[P];
 #pragma unroll
@@ -586,14 +584,24 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
         }
       }
     };
-    if (whole) body(std::true_type{});
-    else body(std::false_type{});
-  }
+  auto process = [&](const int sc) {
+    const uint32_t xs = m.tile_base + sc * C::kSub;      // first ID position of the sub-chunk
+    if (!PCPM_GATHER_NOOP && xs < m.hi && xs + C::kSub > m.lo) {
+      const bool whole = xs >= m.lo && xs + C::kSub <= m.hi;   // warp-uniform: no per-ID range test
+      if (whole) body(sc, std::true_type{});
+      else body(sc, std::false_type{});
+    }
   };
   // sub-chunks gw, gw + gsz, ... of the stage; the remaining kNsc mod gsz
   // sub-chunks rotate over the group's warps from stage to stage
   const int nmain = (C::kNsc / gsz) * gsz;
-  for (int sc = gw; sc < nmain; sc += gsz) process(sc);
+  // a stage inside its item (all but an item's first and last tiles): no range tests
+  const bool stage_whole = !PCPM_GATHER_NOOP && m.lo == m.tile_base && m.hi == m.tile_base + (uint32_t)C::kTile;
+  if (stage_whole) {
+    for (int sc = gw; sc < nmain; sc += gsz) body(sc, std::true_type{});
+  } else {
+    for (int sc = gw; sc < nmain; sc += gsz) process(sc);
+  }
   int who = rot;
   for (int sc = nmain; sc < C::kNsc; ++sc) {
     if (gw == who) process(sc);

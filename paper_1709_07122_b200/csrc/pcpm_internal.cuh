@@ -198,6 +198,12 @@ int launch_bvgas_scatter(pcpm_handle* h, const float* x, cudaStream_t s);   // b
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// shared-memory atomic add at a 32-bit shared address, returning the old value
+__device__ __forceinline__ uint32_t atoms_add_u32(uint32_t saddr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(saddr), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
