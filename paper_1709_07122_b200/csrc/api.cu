@@ -877,8 +877,10 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     return PCPM_OK;
   }
   if (!strcmp(key, "gather_variant")) {
-    if (value < 1 || value > 2) {
-      set_error(PCPM_EINVAL, "gather_variant must be 1 (in-line epilogue) or 2 (apply through tensor memory)");
+    if (value < 1 || value > 3) {
+      set_error(PCPM_EINVAL,
+                "gather_variant must be 1 (in-line epilogue), 2 (apply warps from tensor memory) or 3 (apply in the "
+                "producer warps from tensor memory)");
       return PCPM_EINVAL;
     }
     h->opt_gather_variant = (int)value;

@@ -1067,7 +1067,7 @@ int build_layout_legacy(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     }
     if ((rc = dev_alloc_t(h, &h->png16, ep + 16))) return rc;
     if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
-    TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+    TK(cudaMemsetAsync(h->upd + ep, 0, sizeof(float) * 8, s));   // the scatter writes [0, E') before any read
     TK(cudaMemsetAsync(h->png16, 0, sizeof(uint16_t) * (ep + 16), s));
     uint32_t *pk, *pv, *pk_s;
     TK(tmp.alloc(&pk, ep));
@@ -1394,7 +1394,7 @@ int build_layout_chunked(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   TK(cudaMemcpyAsync(h->png16, png16_t, sizeof(uint16_t) * ep, cudaMemcpyDeviceToDevice, s));
   TK(cudaMemsetAsync(h->png16 + ep, 0, sizeof(uint16_t) * 16, s));
   if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
-  TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+  TK(cudaMemsetAsync(h->upd + ep, 0, sizeof(float) * 8, s));   // the scatter writes [0, E') before any read
   {
     const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
     if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;
@@ -2879,7 +2879,7 @@ int build_layout_count(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
   pt.mark("count build: pass 2 (place)");
 
   if ((rc = dev_alloc_t(h, &h->upd, ep + 8))) return rc;
-  TK(cudaMemsetAsync(h->upd, 0, sizeof(float) * (ep + 8), s));
+  TK(cudaMemsetAsync(h->upd + ep, 0, sizeof(float) * 8, s));   // the scatter writes [0, E') before any read
   {
     const int64_t nga = ep / kPngChunk + 64;     // the scatter copies aligned supersets
     if ((rc = dev_alloc_t(h, &h->grp_at, nga))) return rc;

@@ -180,6 +180,48 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
   if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(mx));  // mx >= 0
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+
+// Producer-side apply (gather_variant 3, DESIGN.md §6 "producer apply"): at an item's end
+// the decoders move the finished accumulator into tensor memory -- local vertex
+// i = 64 c + 32 h + l in TMEM lane 32 h + l, column c (h = 0, 1: the lane quadrants of
+// producer warps 0 and 1) -- zero the shared copy and go on with the next item; the two
+// producer warps run Eq. 1 on it from TMEM (tcgen05.ld) whenever they would otherwise
+// wait (for an empty ring stage or a claimed item).  One buffer: a handoff waits until
+// both producers released the previous one (tempty).
+struct PaRec {             // the item parked in TMEM (written by decoder 0)
+  uint32_t j, nsl, slot, stop;
+  uint32_t bm[32];         // carry bitmap of its accumulator (1 bit per 32 vertices)
+};
+struct PaCtx {
+  PaRec* rec;
+  uint64_t* tfull;         // decoders -> producers, 1 arrival
+  uint64_t* tempty;        // producers -> decoders, 2 arrivals
+  uint32_t tbase;          // TMEM base address (512 columns)
+};
+
 // Producer warp(s) of a gather CTA: claim work items and stream their tiles (IDs,
 // update window, decode anchors, weights) into the ring of S stages with bulk async
 // copies.  With NP = 2 producers, producer pg fills the stages of consumer group pg
@@ -187,11 +229,13 @@ __global__ void k_absmax(int64_t n, const float* __restrict__ x, float* out) {
 // own; producer 0 claims the items and hands them to producer 1 through a small shared
 // queue (claimq / qbar), so the per-stage issue work (measured ~1.5k cycles per stage,
 // DESIGN.md §6) is split over two warps.
-template <typename C, typename IdT, bool W, bool PR, bool SL, bool FUSE = false, int NP = 1>
+template <typename C, typename IdT, bool W, bool PR, bool SL, bool FUSE = false, int NP = 1, bool PA = false>
 __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* ids, uint8_t* stage_base,
                                                 StageMeta* meta, uint64_t* full, uint64_t* empty, int lane,
-                                                int pg = 0, uint32_t* claimq = nullptr, uint64_t* qbar = nullptr) {
+                                                int pg = 0, uint32_t* claimq = nullptr, uint64_t* qbar = nullptr,
+                                                const PaCtx* px = nullptr) {
   constexpr int S = C::kStages;
+  static_assert(!PA || (NP == 2 && !SL && !FUSE), "producer apply: two producers, plain accumulator");
   static_assert(!FUSE || C::kStageBytes >= kFusePng * 2 + 256, "a scatter stage fits in a ring stage");
   static_assert(NP == 1 || (NP == 2 && S % 2 == 0), "two producers split the stages by parity");
   constexpr int kQ = 8;                            // claim queue depth (producers are < 3 items apart)
@@ -205,6 +249,104 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
   uint32_t nclaim = 0;
   unsigned long long pw = 0, pstages = 0, pcopy = 0, ploop = 0, pclaim = 0;   // PCPM_GATHER_PROFILE
   const long long pt0 = PCPM_GATHER_PROFILE ? clock64() : 0;
+  // ---- producer apply (PA): state of the TMEM buffer this warp works on
+  bool pa_have = false, pa_done = false;
+  uint32_t pa_tph = 0, pa_col = 0;
+  unsigned long long pa_dang = 0, pa_res = 0;     // 2^-62 fixed point (red_fx)
+  double pa_base = 0.0, pa_spinv = 1.0;           // set after pdl_wait
+  // one step: the next 8 TMEM columns of this warp's lane quadrant (256 vertices), or
+  // nothing when no buffer is ready.  Warp-wide; block = wait for a buffer.
+  auto pa_step = [&](bool block) {
+    if constexpr (PA) {
+      if (!pa_have) {
+        if (pa_done) return;
+        uint32_t ok = 1;
+        if (block) {
+          mbar_wait(px->tfull, pa_tph);
+        } else {
+          if (lane == 0) ok = mbar_test(px->tfull, pa_tph) ? 1u : 0u;
+          ok = __shfl_sync(0xffffffffu, ok, 0);
+        }
+        if (!ok) return;
+        tmem_fence_after();
+        pa_col = 0;
+        if (px->rec->stop) {
+          pa_done = true;
+          return;
+        }
+        pa_have = true;
+      }
+      const PaRec& H = *px->rec;
+      const uint32_t q = 1u << a.b;
+      const uint32_t v0 = H.j << a.b;
+      const uint32_t cnt = (uint32_t)min((int64_t)q, a.n_dst - (int64_t)v0);
+      const uint32_t nsl = H.nsl;
+      const uint32_t ib = 32u * (uint32_t)pg + (uint32_t)lane;     // i = 64 c + ib
+      uint32_t r[8];
+      tmem_ld8(px->tbase + ((32u * (uint32_t)pg) << 16) + pa_col, r);
+      if (nsl > 1) {
+        // a slice of a split bin: its low words to its slot buffer (k_apply_split applies)
+        uint32_t* sbuf = a.slot_buf + (size_t)H.slot * (size_t)q;
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) __stcg(sbuf + ((pa_col + k) << 6) + ib, r[k]);
+      } else {
+        float idg[8], po[8];
+        if constexpr (PR) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t i = ((pa_col + k) << 6) + ib;
+            idg[k] = i < cnt ? __ldg(a.inv_deg + v0 + i) : 0.0f;
+            po[k] = i < cnt ? __ldg(a.pr_old + v0 + i) : 0.0f;
+          }
+        }
+        tmem_wait_ld();
+        const float fscale = __uint_as_float((uint32_t)(127 + a.fbits) << 23);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t i = ((pa_col + k) << 6) + ib;
+          if (i >= cnt) continue;
+          const uint32_t v = v0 + i;
+          uint64_t tot = PR ? (uint64_t)r[k] : (uint64_t)(long long)(int32_t)r[k];
+          if ((H.bm[i >> 10] >> ((i >> 5) & 31)) & 1u) {
+            tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
+            a.hi[v] = 0u;
+          }
+          if constexpr (PR) {
+            const double prn = pa_base + a.d * ((double)(long long)tot * __longlong_as_double((long long)(1023 - a.fbits) << 52));
+            const float pn = (float)prn;
+            a.pr_new[v] = pn;
+            a.spr_new[v] = pn * idg[k] * fscale;      // SPR * 2^F (R23)
+            if (idg[k] == 0.0f) pa_dang += red_fx(prn);
+            pa_res += red_fx(fabs(prn - (double)po[k]));
+          } else {
+            a.y[v] = (float)((double)(long long)tot * pa_spinv);
+          }
+        }
+      }
+      pa_col += 8;
+      if (pa_col >= (q >> 6) || (nsl <= 1 && (pa_col << 6) >= cnt)) {   // buffer done: release it
+        tmem_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(px->tempty);
+        pa_have = false;
+        pa_tph ^= 1u;
+      }
+    }
+  };
+  // warp-wide wait for phase `parity` of bar, applying while it is not complete (PA)
+  auto pa_wait = [&](uint64_t* bar, uint32_t parity) {
+    if constexpr (PA) {
+      for (;;) {
+        uint32_t ok = 0;
+        // no apply work in hand: suspend on the barrier (up to ~0.5 us) instead of spinning
+        // on the decoders' issue slots, then look for a parked item
+        if (lane == 0) ok = (pa_have ? mbar_test(bar, parity) : mbar_try_wait_hint(bar, parity, 500u)) ? 1u : 0u;
+        if (__shfl_sync(0xffffffffu, ok, 0)) break;
+        pa_step(false);
+      }
+    }
+  };
   auto own = [&]() -> bool { return NP == 1 || (stage & 1) == pg; };
   auto advance = [&]() { if (++stage == S) { stage = 0; phase ^= 1; } };
   auto wait_empty = [&]() {
@@ -231,9 +373,15 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             claimq[nclaim % kQ] = v;
             mbar_arrive(&qbar[nclaim % kQ]);      // release: producer 1 reads claimq after its wait
           }
-        } else {
+        } else if (!PA) {
           mbar_wait(&qbar[nclaim % kQ], (nclaim / kQ) & 1);
           v = claimq[nclaim % kQ];
+        }
+      }
+      if constexpr (PA) {
+        if (pg == 1) {                            // wait for producer 0's claim while applying
+          pa_wait(&qbar[nclaim % kQ], (nclaim / kQ) & 1);
+          if (lane == 0) v = claimq[nclaim % kQ];
         }
       }
       ++nclaim;
@@ -243,6 +391,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
     return v;
   };
   auto push_meta = [&](const StageMeta& m) {      // a stage without data (empty item / stop)
+    if (PA && own()) pa_wait(&empty[stage], phase ^ 1);
     if (own() && lane == 0) {
       wait_empty();
       meta[stage] = m;
@@ -252,6 +401,10 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
     advance();
   };
   pdl_wait();                                      // the update bins (scatter) are complete
+  if constexpr (PA) {
+    if constexpr (PR) pa_base = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
+    else pa_spinv = ldexp(1.0, -spmv_fbits(*a.xmax, a.wexp));
+  }
   uint32_t it = claim();
   GatherItem item{};
   if (it < (uint32_t)a.n_items) item = a.items[it];
@@ -319,6 +472,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
               }
             }
           }
+          if constexpr (PA) pa_wait(&empty[stage], phase ^ 1);
           if (lane == 0) {
             const uint32_t t = tb0 + k;
             const uint32_t tb = t * C::kTile;
@@ -405,6 +559,10 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
     }
     it = it_next;
     item = item_next;
+  }
+  if constexpr (PA) {
+    while (!pa_done) pa_step(true);               // the items still parked in TMEM
+    if constexpr (PR) warp_red_add(a.red_fx, pa_dang, pa_res, lane, false);
   }
   if (PCPM_GATHER_PROFILE && lane == 0) {
     atomicAdd(&g_gather_prof[8], pw);
@@ -617,7 +775,9 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
 // partition j the SPR values stay in the accumulator's shared memory and the CTA scatters
 // source partition j of the next iteration from them (kFlagScatter stages); SPR is not
 // written to global memory.
-template <typename IdT, bool W, bool PR, bool MULTI = false, bool SL = false, bool FUSE = false>
+// PA (gather_variant 3, compact PageRank / SpMV without weights): the apply runs in the
+// producer warps from tensor memory (PaRec / PaCtx above); the decoders only hand over.
+template <typename IdT, bool W, bool PR, bool MULTI = false, bool SL = false, bool FUSE = false, bool PA = false>
 __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const GatherArgs a) {
   using C = Cfg<IdT, W, SL>;
   constexpr int S = C::kStages;
@@ -637,8 +797,12 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   double* red_s = reinterpret_cast<double*>(qbar + 8);                     // 2*C::kWarps
   uint32_t* flag_s = reinterpret_cast<uint32_t*>(red_s + 2 * C::kWarps);
   uint32_t* claimq = flag_s + 4;                                           // [8]
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(claimq + 8);                // PA: [0] tfull, [1] tempty
+  uint32_t* tmem_s = reinterpret_cast<uint32_t*>(tbar + 2);                // PA: TMEM base (+ pad)
+  PaRec* parec = reinterpret_cast<PaRec*>(tmem_s + 4);                     // PA: the parked item
   const IdT* ids = reinterpret_cast<const IdT*>(a.ids);
   constexpr int NP = C::kProducers;
+  static_assert(!PA || (NP == 2 && C::kThreads == 1024 && !MULTI && !SL && !FUSE), "producer apply layout");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -647,13 +811,30 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       mbar_init(&empty[s], (s & 1) ? C::kGroupB : C::kGroupA);   // stage s is consumed by group s & 1
     }
     for (int s = 0; s < 8; ++s) mbar_init(&qbar[s], 1);
+    if (PA) {
+      mbar_init(&tbar[0], 1);
+      mbar_init(&tbar[1], 2);
+    }
     fence_mbar_init();
   }
+  if (PA && warp == 0) tmem_alloc(tmem_s, 512);     // all of TMEM: one CTA per SM
+  if (PA) tmem_fence_before();
   __syncthreads();
+  if (PA) tmem_fence_after();
   pdl_trigger();
+  PaCtx px{parec, &tbar[0], &tbar[1], PA ? *tmem_s : 0u};
 
   if (warp < NP) {
-    gather_producer<C, IdT, W, PR, SL, FUSE, NP>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar);
+    gather_producer<C, IdT, W, PR, SL, FUSE, NP, PA>(a, ids, stage_base, meta, full, empty, lane, warp, claimq, qbar,
+                                                     &px);
+    if constexpr (PA) {
+      __threadfence();                              // this warp's apply stores and red_fx atomics
+      named_bar_sync(3, C::kThreads);               // with the consumers' completion count below
+      if (warp == 0) {
+        tmem_fence_after();
+        tmem_dealloc(px.tbase, 512);
+      }
+    }
     return;
   }
 
@@ -683,6 +864,48 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   named_bar_sync(1, kCons);
   const uint32_t lemask = lanemask_le();
 
+  // PA: move the finished accumulator into TMEM for the producers (see PaRec): wait until
+  // they released the previous item, then the decoders of lane quadrants 0 and 1 (warps
+  // 4 + 4 r + h) copy column groups of 8 and zero the shared words, decoder 0 writes the
+  // record; stop = no more items.
+  uint32_t tpar = 0;
+  auto pa_handoff = [&](const StageMeta& m, bool stop) {
+    if constexpr (PA) {
+      mbar_wait(px.tempty, tpar ^ 1u);
+      tpar ^= 1u;
+      tmem_fence_after();
+      if (!stop) {
+        const int h = warp & 3;
+        if (h < 2) {
+          const uint32_t ngrp = (uint32_t)(q >> 9);  // 8-column groups (q / 64 columns)
+          for (uint32_t cg = (uint32_t)((warp >> 2) - 1); cg < ngrp; cg += 7u) {
+            uint32_t r[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = acc[((cg * 8 + k) << 6) + 32 * h + lane];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[((cg * 8 + k) << 6) + 32 * h + lane] = 0u;
+            tmem_st8(px.tbase + ((uint32_t)(32 * h) << 16) + cg * 8, r);
+          }
+          tmem_wait_st();
+        }
+        if (cw == 0) {
+          if (lane == 0) {
+            px.rec->j = m.j;
+            px.rec->nsl = a.bin_nslices[m.j];
+            px.rec->slot = a.items[m.item].pad[0];
+            px.rec->stop = 0u;
+          }
+          px.rec->bm[lane] = lane < bm_words ? bitmap[lane] : 0u;
+          if (lane < bm_words) bitmap[lane] = 0u;
+        }
+      } else if (cw == 0 && lane == 0) {
+        px.rec->stop = 1u;
+      }
+      tmem_fence_before();
+      named_bar_sync(1, kCons);                      // every share copied and zeroed
+      if (cw == 0 && lane == 0) mbar_arrive(px.tfull);
+    }
+  };
   int stage = grp, rot = 0;
   int srot = 0;                                     // FUSE: rotation of the scatter stages' remainder
   uint32_t phase = 0;
@@ -724,6 +947,11 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       // ---------------- epilogue of this item ----------------
       named_bar_sync(1, kCons);
       if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[2] += t - tc; tc = t; }
+      if constexpr (PA) {
+        pa_handoff(m, false);
+        if (PCPM_GATHER_PROFILE) { const long long t = clock64(); pt[3] += t - tc; tc = t; }
+        continue;
+      }
       const int64_t cnt = min(q, a.n_dst - (int64_t)v0);
       const uint32_t nsl = a.bin_nslices[m.j];
       bool run_apply = true;
@@ -922,10 +1150,15 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
     atomicAdd(&g_gather_prof[4], 1ull);
   }
 
+  if constexpr (PA) {
+    StageMeta ms{};
+    pa_handoff(ms, true);                          // the producers drain the TMEM buffer and stop
+  }
   if constexpr (MULTI) __threadfence_system();     // peer stores performed before the kernel completes
   else __threadfence();                            // this warp's red_fx atomics before the completion count
   // ---------------- last CTA: fixed-order reduction, counter reset ----------------
-  named_bar_sync(1, kCons);
+  if constexpr (PA) named_bar_sync(3, C::kThreads);   // the producers' applies are complete
+  else named_bar_sync(1, kCons);
   if (ctid == 0) {
     __threadfence();
     const uint32_t done = atomicAdd(&a.counters[1], 1u);
@@ -994,18 +1227,6 @@ int smem_bytes2(int b) {
   const int64_t head = ((q + 31) / 32) * 32 * 4 + C::kBmWords * 4;
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 4 * 8 +
                2 * sizeof(HandoffRec) + 32);
-}
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
 }
 
 // The apply of one item's accumulator straight from shared memory by nthr threads
@@ -1626,7 +1847,7 @@ int smem_bytes_for(int b, int64_t aw = 0) {
   const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4 + (SL ? ((int64_t(1) << b) / 32) * 8 : 0);
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 8 * 8 +
-               2 * C::kWarps * 8 + 16 + 8 * 4);
+               2 * C::kWarps * 8 + 16 + 8 * 4 + 2 * 8 + 16 + sizeof(PaRec));
 }
 
 using GatherFn = void (*)(const GatherArgs);
@@ -1640,6 +1861,8 @@ GatherFn gather_fn(bool wide, bool weighted, bool pagerank, bool multi = false, 
   return weighted ? (pagerank ? k_gather<uint16_t, true, true> : k_gather<uint16_t, true, false>)
                   : (pagerank ? k_gather<uint16_t, false, true> : k_gather<uint16_t, false, false>);
 }
+
+GatherFn gather_pa_fn() { return k_gather<uint16_t, false, true, false, false, false, true>; }
 
 GatherFn gather_fuse_fn(bool weighted) {       // compact PageRank with the next scatter fused in
   return weighted ? k_gather<uint16_t, true, true, false, false, true> : k_gather<uint16_t, false, true, false, false, true>;
@@ -1712,6 +1935,7 @@ int prepare_gather(pcpm_handle* h) {
         PCPM_CK(cudaFuncSetAttribute(gather_cl_fn(wd, w, p), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   for (int w = 0; w < 2; ++w)
     PCPM_CK(cudaFuncSetAttribute(gather_fuse_fn(w), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  PCPM_CK(cudaFuncSetAttribute(gather_pa_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   return PCPM_OK;
 }
 
@@ -1822,6 +2046,13 @@ int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pager
   }
   const int smem = slots ? smem_bytes_for<uint16_t, false, true>(a.b, a.acc_words) : gather_smem_bytes(a.b, h->wide, weighted);
   const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
+  // gather_variant 3: the apply in the producer warps from tensor memory (compact,
+  // unweighted PageRank, 2^9 <= q <= 2^15)
+  if (h->opt_gather_variant == 3 && !slots && !multi && !h->wide && !weighted && pagerank && a.b >= 9 && a.b <= 15) {
+    PCPM_CK(launch_k(h->opt_pdl != 0, gather_pa_fn(), grid, gather_threads(false, false), smem, s, a));
+    h->launches += 1;
+    return launch_apply_split(h, a, pagerank, s);
+  }
   PCPM_CK(launch_k(h->opt_pdl != 0, gather_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted, slots), grid,
                    gather_threads(h->wide, weighted), smem, s, a));
   h->launches += 1;

@@ -366,6 +366,7 @@ def test_spmv_non_square(pcpm):
 
 @pytest.mark.parametrize("opts", [{"scatter_variant": 1}, {"scatter_variant": 2}, {"scatter_variant": 3}, {"scatter_lpt": 1}, {"gather_prefetch": 0},
                                   {"cluster_gather": 0}, {"gather_variant": 2},
+                                  {"gather_variant": 3, "cluster_gather": 0},
                                   {"epilogue_prefetch": 0}, {"gather_prefetch": 8, "epilogue_prefetch": 16},
                                   {"use_graph": 0}],
                          ids=lambda o: ",".join(f"{k}={v}" for k, v in o.items()))
@@ -388,6 +389,41 @@ def test_kernel_variants_keep_parity(pcpm, opts):
         got = d2h(v.upd, info.e_prime, np.float32)
         want = oracle.scatter(oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, 10), x)
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+PA_CASES = [
+    ("rmat18_b11", lambda: graphs.make_graph("rmat", 21, scale=18, permute=True), 11),
+    ("rmat20_b15", lambda: graphs.make_graph("rmat", 22, scale=20, permute=True), 15),
+    ("rmat19_bfs_b13", lambda: graphs.make_graph("rmat", 23, scale=19, permute=False), 13),
+    ("er_ragged_b9", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000), 9),
+]
+
+
+@pytest.mark.parametrize("name,mk,b", PA_CASES, ids=[c[0] for c in PA_CASES])
+def test_producer_apply_bit_identical(pcpm, name, mk, b):
+    """gather_variant 3 (the apply in the producer warps from tensor memory) gives the
+    oracle's PageRank within the BASELINE bounds and the same bits as the in-line
+    epilogue (both sum the same integers), including split bins, a ragged last partition
+    and the residual / dangling reductions."""
+    g = mk()
+    h = build(pcpm, g, b)
+    try:
+        pcpm.pcpm_set_option(h, "cluster_gather", 0)
+        iters = 9
+        outs, res = [], []
+        for var in (1, 3):
+            pcpm.pcpm_set_option(h, "gather_variant", var)
+            out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, iters, out)
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy())
+            res.append(np.asarray(pcpm.pcpm_get_residuals(h, iters)))
+        np.testing.assert_array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+        np.testing.assert_array_equal(res[0], res[1])
+        ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, iters)
+        pr_check(outs[1], ref, name)
     finally:
         pcpm.pcpm_destroy(h)
 
