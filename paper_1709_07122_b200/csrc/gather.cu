@@ -8,12 +8,13 @@
 //  * Persistent CTAs (one per SM, 128 KB accumulator = one destination
 //    partition of q = 2^15 vertices in shared memory).  Work items are slices
 //    of destination bins, largest first, claimed with an atomic counter.
-//  * Warp 0 is the producer: for each tile it issues bulk async copies (TMA
-//    engine, cp.async.bulk) into a 4-stage ring: the IDs (4096 2-byte IDs in
-//    the compact layout), the window of update values they reference, and
-//    the decode anchors.
-//  * 31 consumer warps in two groups that take alternate stages; each warp
-//    decodes two 128-ID sub-chunks of a stage (the group of 15 rotates the
+//  * Warps 0 and 1 are the producers (one per consumer group; one producer
+//    outside the compact PageRank configuration): for each tile a producer
+//    issues bulk async copies (TMA engine, cp.async.bulk) into a 4-stage ring:
+//    the IDs (4096 2-byte IDs in the compact layout), the window of update
+//    values they reference, and the decode anchors.
+//  * 30 consumer warps in two groups of 15 that take alternate stages; each
+//    warp decodes two 128-ID sub-chunks of a stage (the group rotates the
 //    remaining two) in steps of 32 consecutive IDs (lane l takes ID 32 c + l).
 //    The producer also prefetches the tiles (and, near an item's end, the
 //    apply's vertex arrays) into L2 ahead of the ring.  The update pointer of Alg. 5
