@@ -8,8 +8,7 @@
 //  * Persistent CTAs (one per SM, 128 KB accumulator = one destination
 //    partition of q = 2^15 vertices in shared memory).  Work items are slices
 //    of destination bins, largest first, claimed with an atomic counter.
-//  * Warps 0 and 1 are the producers (one per consumer group; one producer
-//    outside the compact PageRank configuration): for each tile a producer
+//  * Warps 0 and 1 are the producers (one per consumer group): for each tile a producer
 //    issues bulk async copies (TMA engine, cp.async.bulk) into a 4-stage ring:
 //    the IDs (4096 2-byte IDs in the compact layout), the window of update
 //    values they reference, and the decode anchors.
@@ -85,16 +84,19 @@ struct Cfg {
 #ifndef PCPM_GATHER_COLD_WARPS
 #define PCPM_GATHER_COLD_WARPS 31
 #endif
-  // producer warps: two for the hot configuration (each fills the stages of one consumer
-  // group), one otherwise
+  // producer warps: two (each fills the stages of one consumer group); measured against one
+  // on the weighted / SpMV / 4-byte-ID configurations too
 #ifndef PCPM_GATHER_PRODUCERS
 #define PCPM_GATHER_PRODUCERS 2
 #endif
-  static constexpr int kProducers = kHot ? PCPM_GATHER_PRODUCERS : 1;
+#ifndef PCPM_GATHER_COLD_PRODUCERS
+#define PCPM_GATHER_COLD_PRODUCERS 2
+#endif
+  static constexpr int kProducers = kHot ? PCPM_GATHER_PRODUCERS : PCPM_GATHER_COLD_PRODUCERS;
 #ifndef PCPM_GATHER_HOT_WARPS
 #define PCPM_GATHER_HOT_WARPS (32 - PCPM_GATHER_PRODUCERS)
 #endif
-  static constexpr int kWarps = kHot ? PCPM_GATHER_HOT_WARPS : PCPM_GATHER_COLD_WARPS;
+  static constexpr int kWarps = kHot ? PCPM_GATHER_HOT_WARPS : (PCPM_GATHER_COLD_WARPS + 1 - PCPM_GATHER_COLD_PRODUCERS);
   static constexpr int kThreads = 32 * (kWarps + kProducers);
   static constexpr int kSub = kHot ? (kTile / 32 < kChunkIds ? kChunkIds : kTile / 32) : kChunkIds;   // IDs per sub-chunk
   static constexpr int kNsc = kTile / kSub;                // sub-chunks per tile
