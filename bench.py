@@ -812,6 +812,8 @@ def main():
     ap.add_argument("--wide", action="store_true", help="iterate on the paper's 4-byte ID layout")
     ap.add_argument("--slots", type=int, default=0, help="1: build with PCPM_COMPACT_SLOTS (accumulator slots)")
     args = ap.parse_args()
+    if args.bits == 16:
+        args.wide = True                           # q = 2^16 handles iterate on 4-byte IDs (pcpm.h)
     if args.lib:                                   # A/B variant build of libpcpm.so
         os.environ["PCPM_LIB"] = os.path.abspath(args.lib)
     world, rank, local = dist_setup(args)

@@ -21,10 +21,16 @@
  *  - Return value 0 = success, negative = PCPM_E* code; pcpm_last_error()
  *    gives a thread-local message for the last failure.
  *  - Limits: n_src, n_dst < 2^31 (the MSB of a 4-byte ID is the run flag,
- *    P:172-173); nnz < 2^32 (u32 bin positions); partition_bits in [1, 15]
- *    (one destination partition's accumulator, 2^b x 4 B, lives in one CTA's
- *    shared memory); k_src * k_dst <= 2^28 (the O(k^2) offset matrices of
- *    P:148 / P:246).
+ *    P:172-173); nnz < 2^32 (u32 bin positions); partition_bits in [1, 16]:
+ *    up to 15 one destination partition's accumulator (2^b x 4 B) lives in one
+ *    CTA's shared memory; 16 (the right end of the paper's partition-size
+ *    sweep; not for pcpm_build_shard or PCPM_BVGAS) implies
+ *    PCPM_WIDE_IDS -- a 16-bit local ID plus the run flag needs the 4-byte
+ *    format -- and the gather streams every bin twice, once per 2^15-vertex
+ *    half of its partition, while the scatter reads the source values through
+ *    L1/L2 (a 256 KB slice does not fit in shared memory); results are the
+ *    same bits as with 15.  k_src * k_dst <= 2^28 (the O(k^2) offset matrices
+ *    of P:148 / P:246).
  */
 #ifndef PCPM_H
 #define PCPM_H
@@ -123,7 +129,7 @@ typedef struct {
   const uint32_t* out_degree;    /* [n_src] |N_o(u)| */
   float* upd;                    /* [E'] update bins of the last scatter (scratch) */
   int64_t chunk_ids;             /* IDs per chunk_base entry (128) */
-  const uint16_t* ids16;         /* [nnz] compact destID bins: (v & (q-1)) | flag<<15 */
+  const uint16_t* ids16;         /* [nnz] compact destID bins: (v & (q-1)) | flag<<15 (b = 16: 15 local bits) */
   const uint16_t* png_src16;     /* [E'] compact PNG sources: u & (q-1) (u is in partition p) */
   int32_t wide;                  /* 1 when the kernels iterate on the 4-byte arrays */
 } pcpm_layout_view;

@@ -139,7 +139,7 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   GatherArgs a{};
   a.ids = h->wide ? static_cast<const void*>(h->ids) : static_cast<const void*>(h->ids16);
   a.slot16 = h->wide ? nullptr : h->slot16;
-  a.acc_words = h->slot16 ? h->acc_words : (int)h->q;
+  a.acc_words = h->slot16 ? h->acc_words : (int)(int64_t(1) << h->gb);
   a.slotmap = h->wide ? nullptr : h->slotmap;
   a.w = h->w;
   a.upd = h->upd;
@@ -154,7 +154,8 @@ GatherArgs base_args(pcpm_handle* h, int fbits) {
   a.bin_arrive = h->bin_arrive;
   a.hi = h->hi;
   a.red_fx = h->red_fx;
-  a.b = h->b;
+  a.b = h->gb;
+  a.pair = h->pair ? 1 : 0;
   a.n_dst = h->n_dst;
   a.fbits = fbits;
   a.inv_deg = h->inv_deg + h->shard_lo;  // apply: 1 / global out-degree of destination v (shards: lo + v)
@@ -373,10 +374,12 @@ static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsign
     set_error(PCPM_EINVAL, "NULL csr / row_ptr / col_idx");
     return nullptr;
   }
-  if (partition_bits < 1 || partition_bits > kMaxBits) {
-    set_error(PCPM_EINVAL, "partition_bits must be in [1, 15]");
+  if (partition_bits < 1 || partition_bits > kMaxBitsPair || (partition_bits > kMaxBits && lo >= 0)) {
+    set_error(PCPM_EINVAL, "partition_bits must be in [1, 16] (shards: [1, 15])");
     return nullptr;
   }
+  // q = 2^16: 4-byte IDs, two half-partition gather items per bin (pcpm.h)
+  if (partition_bits > kMaxBits) flags |= PCPM_WIDE_IDS;
   if (csr->n_src < 1 || csr->n_dst < 1 || csr->nnz < 0) {
     set_error(PCPM_EINVAL, "n_src, n_dst must be >= 1 and nnz >= 0");
     return nullptr;
@@ -405,6 +408,8 @@ static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsign
   pcpm_handle* h = new pcpm_handle();
   h->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   h->b = partition_bits;
+  h->gb = std::min(partition_bits, kMaxBits);
+  h->pair = partition_bits > kMaxBits;
   cudaGetDevice(&h->device);
   pool_setup(h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);

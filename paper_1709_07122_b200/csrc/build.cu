@@ -316,11 +316,12 @@ __global__ void k_outdeg(int64_t u0, int64_t n, const int64_t* __restrict__ row_
 }
 
 __global__ void k_item_f(int n_items, GatherItem* items, const uint32_t* __restrict__ chunk_base,
-                         const uint32_t* __restrict__ bin_upd_start) {
+                         const uint32_t* __restrict__ bin_upd_start, int jshift = 0) {
   GRID_STRIDE(i, n_items) {
     GatherItem it = items[i];
-    it.fx0 = (it.x0 % kChunkIds == 0) ? chunk_base[it.x0 / kChunkIds] : bin_upd_start[it.j];
-    it.fx1 = (it.x1 % kChunkIds == 0) ? chunk_base[it.x1 / kChunkIds] : bin_upd_start[it.j + 1];
+    const uint32_t bj = it.j >> jshift;               // pair handles: item j is a half of bin j >> 1
+    it.fx0 = (it.x0 % kChunkIds == 0) ? chunk_base[it.x0 / kChunkIds] : bin_upd_start[bj];
+    it.fx1 = (it.x1 % kChunkIds == 0) ? chunk_base[it.x1 / kChunkIds] : bin_upd_start[bj + 1];
     items[i] = it;
   }
 }
@@ -732,7 +733,11 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   // item exceeds ~m / (2 SMs) IDs; largest first (LPT, the GPU analogue of the
   // paper's dynamic scheduling).
   std::vector<GatherItem> gi;
-  std::vector<uint32_t> nsl(k_dst, 0), sbase(k_dst, 0);
+  // pair handles (q = 2^16): the gather sees 2 k_dst half-partitions of 2^15 vertices; half
+  // hf of bin j is item j' = 2 j + hf over the WHOLE bin (it skips the other half's IDs),
+  // never cut (slices and the cluster gather assume one accumulator per bin)
+  const int64_t k_g = h->pair ? 2 * k_dst : k_dst;
+  std::vector<uint32_t> nsl(k_g, 0), sbase(k_g, 0);
   uint32_t nslots = 0;
   // items per SM the cut aims at: 2 when bin sizes are skewed (the LPT order then has
   // small slices to fill the tail), 1 when every bin is within 2x of the mean (cutting
@@ -742,7 +747,17 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   int slice_div = (k_dst > 0 && max_bin * k_dst <= 2 * m) ? 1 : 2;
   if (const char* e = getenv("PCPM_GATHER_SLICE_DIV")) slice_div = std::max(1, atoi(e));
   int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (slice_div * h->num_sms)) / kTileAlign + 1) * kTileAlign);
-  for (int64_t j = 0; j < k_dst; ++j) {
+  for (int64_t j = 0; h->pair && j < k_g; ++j) {
+    nsl[j] = 1;
+    if ((j << h->gb) >= n_dst) continue;              // the last partition may have no upper half
+    GatherItem it{};
+    it.j = (uint32_t)j;
+    it.x0 = hbin[j >> 1];
+    it.x1 = hbin[(j >> 1) + 1];
+    it.pad[0] = 0xFFFFFFFFu;
+    gi.push_back(it);
+  }
+  for (int64_t j = 0; !h->pair && j < k_dst; ++j) {
     int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
     int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
     int64_t per = (sz + nslc - 1) / nslc;
@@ -770,7 +785,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
                    [](const GatherItem& a, const GatherItem& c) { return (a.x1 - a.x0) > (c.x1 - c.x0); });
   // cluster gather for few partitions: cs CTAs per bin (one tile-aligned slice each), cs = 2..8
   h->cl_cs = 0;
-  if (k_dst >= 1 && 2 * k_dst <= h->num_sms && !getenv("PCPM_NO_CLUSTER_GATHER")) {
+  if (!h->pair && k_dst >= 1 && 2 * k_dst <= h->num_sms && !getenv("PCPM_NO_CLUSTER_GATHER")) {
     int cs = 1, cs_max = 8;
     if (const char* e = getenv("PCPM_CLUSTER_MAX")) cs_max = std::max(2, std::min(8, atoi(e)));   // A/B
     while (cs * 2 <= cs_max && (int64_t)cs * 2 * k_dst <= h->num_sms) cs *= 2;
@@ -796,11 +811,11 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   }
   h->n_gitems = (int)gi.size();
   if ((rc = dev_alloc_t(h, &h->gitems, gi.size()))) return rc;
-  if ((rc = dev_alloc_t(h, &h->bin_nslices, k_dst))) return rc;
+  if ((rc = dev_alloc_t(h, &h->bin_nslices, k_g))) return rc;
   TK(cudaMemcpyAsync(h->gitems, gi.data(), sizeof(GatherItem) * gi.size(), cudaMemcpyHostToDevice, s));
-  TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
-  if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_dst))) return rc;
-  TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_dst, cudaMemcpyHostToDevice, s));
+  TK(cudaMemcpyAsync(h->bin_nslices, nsl.data(), sizeof(uint32_t) * k_g, cudaMemcpyHostToDevice, s));
+  if ((rc = dev_alloc_t(h, &h->bin_slot_base, k_g))) return rc;
+  TK(cudaMemcpyAsync(h->bin_slot_base, sbase.data(), sizeof(uint32_t) * k_g, cudaMemcpyHostToDevice, s));
   h->n_slots = nslots;
   {
     std::vector<uint32_t> sb;
@@ -826,7 +841,8 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
     }
   }
   if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
-  k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start);
+  k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start,
+                                                h->pair ? 1 : 0);
   TK(cudaGetLastError());
   if (h->cl_cs) {
     const int nc = (int)(k_dst * h->cl_cs);
@@ -843,8 +859,8 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   if ((rc = dev_alloc_t(h, &h->ybuf, n_dst + 8))) return rc;
   if ((rc = dev_alloc_t(h, &h->hi, n_dst))) return rc;
   if ((rc = dev_alloc_t(h, &h->counters, 8))) return rc;
-  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_dst))) return rc;
-  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_dst, s));
+  if ((rc = dev_alloc_t(h, &h->bin_arrive, k_g))) return rc;
+  TK(cudaMemsetAsync(h->bin_arrive, 0, sizeof(uint32_t) * k_g, s));
   if ((rc = dev_alloc_t(h, &h->xmax, 4))) return rc;
   if ((rc = dev_alloc_t(h, &h->red_fx, 2))) return rc;
   TK(cudaMemsetAsync(h->red_fx, 0, sizeof(unsigned long long) * 2, s));
@@ -1031,12 +1047,12 @@ int build_layout_legacy(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
       // weights travel with the IDs: sort edge indices, then gather IDs and weights
       TK(radix_sort_pairs(tmp, keyj, keyj_s, iota, perm, m, jbits, s));
       pt.mark("sort edges by j");
-      k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, (uint32_t)(q - 1), ids32, h->ids16, h->w);
+      k_gather_ids<<<grid_for(m), kT, 0, s>>>(m, perm, enc, values, (uint32_t)(q - 1) & 0x7FFFu, ids32, h->ids16, h->w);
     } else {
       // the encoded IDs are the sort's payload: no random gather afterwards
       TK(radix_sort_pairs(tmp, keyj, keyj_s, enc, ids32, m, jbits, s));
       pt.mark("sort edges by j");
-      k_ids16<<<grid_for(m), kT, 0, s>>>(m, ids32, (uint32_t)(q - 1), h->ids16);
+      k_ids16<<<grid_for(m), kT, 0, s>>>(m, ids32, (uint32_t)(q - 1) & 0x7FFFu, h->ids16);
     }
     TK(cudaGetLastError());
     k_boundaries<<<grid_for(m + 1), kT, 0, s>>>(m, keyj_s, k_dst, h->bin_id_start);
@@ -2920,7 +2936,9 @@ int build_layout(pcpm_handle* h, const pcpm_csr* csr, unsigned flags) {
     return build_layout_count(h, csr, flags | PCPM_NO_COMPRESS);
   }
   const bool legacy = getenv("PCPM_BUILD_LEGACY") != nullptr;
-  if (legacy || csr->nnz == 0 || csr->n_src <= 0 || csr->n_dst <= 0) return build_layout_legacy(h, csr, flags);
+  // q = 2^16 (pair handles): only the two-sort path carries 16-bit local IDs (its keys and
+  // payloads are whole 4-byte IDs; the other builds pack local ID, flag and source in 32 bits)
+  if (legacy || h->pair || csr->nnz == 0 || csr->n_src <= 0 || csr->n_dst <= 0) return build_layout_legacy(h, csr, flags);
   // the counting construction (default) unless the pull CSC is wanted or the bins are too many
   const char* mode = getenv("PCPM_BUILD");                   // "sort": the chunked sort (A/B)
   const int64_t q = int64_t(1) << h->b, k_dst = (csr->n_dst + q - 1) / q;

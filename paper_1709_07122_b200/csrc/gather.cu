@@ -661,6 +661,9 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
         run += __popc(bal);
         const uint32_t x = xs + c * 32 + lane;
         ok[c] = kWhole || (x >= m.lo && x < m.hi);
+        // pair handles (q = 2^16, 4-byte IDs): this item owns half (j & 1) of the bin's
+        // partition; the other half's IDs only advance the update pointer
+        if constexpr (sizeof(IdT) == 4) ok[c] = ok[c] && (!a.pair || ((id[c] >> kMaxBits) & 1u) == (m.j & 1u));
         val[c] = ok[c] ? win_s[ptr] : 0.0f;
       }
       if constexpr (PR) {
@@ -1909,7 +1912,7 @@ int prepare_gather(pcpm_handle* h) {
   PCPM_CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   for (int wd = 0; wd < 2; ++wd)
     for (int w = 0; w < 2; ++w) {
-      if (gather_smem_bytes(h->b, wd, w) > maxsm) {
+      if (gather_smem_bytes(h->gb, wd, w) > maxsm) {
         set_error(PCPM_ECUDA, "gather shared-memory plan exceeds the device limit for this partition size");
         return PCPM_ECUDA;
       }
@@ -1923,7 +1926,7 @@ int prepare_gather(pcpm_handle* h) {
                                  maxsm));
   for (int wd = 0; wd < 2; ++wd)
     for (int w = 0; w < 2; ++w) {
-      if (gather2_smem_bytes(h->b, wd, w) > maxsm) {
+      if (gather2_smem_bytes(h->gb, wd, w) > maxsm) {
         set_error(PCPM_ECUDA, "gather (v2) shared-memory plan exceeds the device limit for this partition size");
         return PCPM_ECUDA;
       }
@@ -2039,7 +2042,7 @@ int launch_gather(pcpm_handle* h, const GatherArgs& a, bool weighted, bool pager
     return launch_apply_split(h, a, pagerank, s);
   }
   if (h->cl_cs >= 2 && h->opt_cluster_gather && !slots && !multi) return launch_gather_cl(h, a, weighted, pagerank, s);
-  if (!slots && h->opt_gather_variant == 2) {
+  if (!slots && h->opt_gather_variant == 2 && !h->pair) {
     const int grid = std::min(h->num_sms, std::max(a.n_items, 1));
     gather2_fn(h->wide, weighted, pagerank, multi && pagerank && !weighted)<<<grid, 1024,
                                                                            gather2_smem_bytes(a.b, h->wide, weighted), s>>>(a);

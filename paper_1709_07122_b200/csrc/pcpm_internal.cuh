@@ -29,6 +29,11 @@ constexpr int kTileAlign = 4096;
 constexpr int kChunkIds = 128;                         // chunk_base granularity
 constexpr int kMaxPeers = 8;                           // fused exchange: SPR destinations besides spr_new
 constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB accumulator
+// q = 2^16 ("pair" handles, DESIGN.md §6 "partition size"): the 256 KB accumulator of a
+// destination partition does not fit one SM, so the gather runs every bin twice, as two
+// items that each own one 2^15-vertex half of the partition and skip the other half's IDs
+// (4-byte IDs only: a 16-bit local ID plus the run flag does not fit the 2-byte format)
+constexpr int kMaxBitsPair = 16;
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
 constexpr int kPngChunk = 256;                         // grp_at granularity (scatter warp sub-ranges)
@@ -59,6 +64,8 @@ struct Graph {             // cached CUDA graph of one pcpm_pagerank configurati
 struct pcpm_handle {
   int64_t n_src = 0, n_dst = 0, m = 0, m_pad = 0, e_prime = 0;
   int b = 0;
+  int gb = 0;                        // partition bits of the gather's accumulator: min(b, kMaxBits)
+  bool pair = false;                 // b = 16: two half-partition gather items per bin
   int64_t q = 0, k_src = 0, k_dst = 0, n_dangling = 0;
   bool weighted = false, compressed = true, has_pull = false;
   cudaStream_t stream = nullptr;
@@ -342,7 +349,8 @@ struct GatherArgs {
   uint32_t* bin_arrive;    // [k_dst] slices arrived per split bin (reset by the last)
   uint32_t* hi;
   unsigned long long* red_fx;   // [2] dangling mass / residual of this launch, 2^-62 fixed point (kept zero)
-  int b;
+  int b;                   // partition bits of the accumulator (h->gb)
+  int pair;                // 1: item j is half (j & 1) of bin j >> 1 and adds only that half's IDs (b = 16)
   int64_t n_dst;
   int fbits;
   // PageRank epilogue

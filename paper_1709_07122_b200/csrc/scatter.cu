@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
   static_assert(kSub % kPngChunk == 0 && kNsr >= kScW, "warp sub-ranges start on grp_at anchors");
   extern __shared__ __align__(128) uint8_t smem[];
   const int64_t q = int64_t(1) << a.b;
-  float* xs = reinterpret_cast<float*>(smem);                                        // q floats
-  uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + ((q * 4 + 127) & ~int64_t(127)));
+  float* xs = reinterpret_cast<float*>(smem);                                        // q floats (none with XG)
+  uint32_t* off_s = reinterpret_cast<uint32_t*>(smem + (XG ? int64_t(0) : ((q * 4 + 127) & ~int64_t(127))));
   uint32_t* uo_s = off_s + kScOffCap;
   uint8_t* ring = reinterpret_cast<uint8_t*>(uo_s + kScOffCap);
   uint32_t* grp_s = reinterpret_cast<uint32_t*>(ring + kScStages * kScStageBytes);       // [kScStages][kScGrpCap]
@@ -352,8 +352,8 @@ __global__ void __launch_bounds__(ScCfg<SrcT>::kThreads, 1) k_scatter_tma(const 
   (void)flag_s;
 }
 
-int scatter_tma_smem_bytes(int b) {
-  const int64_t q = int64_t(1) << b;
+int scatter_tma_smem_bytes(int b, bool xg = false) {
+  const int64_t q = xg ? 0 : int64_t(1) << b;          // XG reads the source values from global memory
   return (int)(((q * 4 + 127) & ~int64_t(127)) + 2 * kScOffCap * 4 + kScStages * kScStageBytes +
                kScStages * kScGrpCap * 4 + kScStages * sizeof(ScStageMeta) + sizeof(ScItemMeta) + (2 * kScStages + 2) * 8 + 16);
 }
@@ -449,7 +449,9 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out, b
   float* upd = out ? out : h->upd;
   if (n_items == 0) return PCPM_OK;
   const int grid = std::min(n_items, h->num_sms);
-  if (h->opt_scatter_variant == 1 || h->b < 2) {   // the bulk-copy variant needs 16 B aligned slices
+  // q = 2^16 (pair handles): a source partition's 256 KB slice does not fit in shared memory, so
+  // the source values are read through L1/L2 (the XG kernel)
+  if ((h->opt_scatter_variant == 1 && !h->pair) || h->b < 2) {   // the bulk-copy variant needs 16 B aligned slices
     const int smem = scatter_warp_smem_bytes(h->b);
     if (h->wide)
       k_scatter_warp<uint32_t><<<grid, kScatterThreads, smem, s>>>(items, n_items, x, h->n_src, h->b,
@@ -482,8 +484,8 @@ int launch_scatter(pcpm_handle* h, const float* x, cudaStream_t s, float* out, b
     a.upd = upd;
     a.counters = h->counters;
     a.pf_stages = h->opt_scatter_pf;
-    const int smem = scatter_tma_smem_bytes(h->b);
-    const bool xg = h->opt_scatter_variant == 2, vec = h->opt_scatter_variant == 3;
+    const bool xg = h->opt_scatter_variant == 2 || h->pair, vec = h->opt_scatter_variant == 3 && !h->pair;
+    const int smem = scatter_tma_smem_bytes(h->b, xg);
     if (h->wide)
       PCPM_CK(launch_k(h->opt_pdl != 0,
                        xg ? k_scatter_tma<uint32_t, true> : vec ? k_scatter_tma<uint32_t, false, true> : k_scatter_tma<uint32_t>,

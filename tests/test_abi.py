@@ -47,7 +47,7 @@ def test_invalid_arguments_rejected_without_gpu():
     rp = np.array([0, 1, 2], dtype=np.int64)
     col = np.array([1, 0], dtype=np.uint32)
     csr = pcpm.make_csr(2, 2, rp, col)
-    for bits in (0, 16, -3):
+    for bits in (0, 17, -3):
         with pytest.raises(pcpm.PcpmError) as e:
             pcpm.pcpm_build(csr, bits)
         assert e.value.code == pcpm.PCPM_EINVAL

@@ -83,7 +83,8 @@ def assert_layout_equal(g, lay_gpu, b, compress=True):
             np.testing.assert_array_equal(lay_gpu["ids"], ids)
             np.testing.assert_array_equal(lay_gpu["png_src"], ref.png_src)
         # compact layout = the same bins re-encoded: (v & (q-1)) | flag << 15, u & (q-1)
-        want16 = ((ids & qmask) | ((ids >> np.uint32(31)) << np.uint32(15))).astype(np.uint16)
+        # (q = 2^16 handles iterate on the 4-byte IDs; their 2-byte array keeps 15 local bits + the flag)
+        want16 = ((ids & qmask & np.uint32(0x7FFF)) | ((ids >> np.uint32(31)) << np.uint32(15))).astype(np.uint16)
         np.testing.assert_array_equal(lay_gpu["ids16"], want16)
         np.testing.assert_array_equal(lay_gpu["png_src16"], (ref.png_src & qmask).astype(np.uint16))
         np.testing.assert_array_equal(lay_gpu["png_off"], ref.png_off.astype(np.uint32))
@@ -809,3 +810,79 @@ def test_bvgas_rejects(pcpm):
     with pytest.raises(pcpm.PcpmError) as e:                      # non-square
         pcpm.pcpm_build_ex(pcpm.make_csr(gr.n_src, gr.n_src + 100, rp, col), 6, pcpm.PCPM_BVGAS, None)
     assert e.value.code == pcpm.PCPM_EINVAL
+
+
+# ---- q = 2^16 ("pair" handles): 4-byte IDs, two half-partition gather items per
+# bin, source values read through L1/L2 in the scatter.  Layout bit-exact against the oracle at
+# b = 16, PageRank / SpMV within the BASELINE bounds and -- the fixed-point sums being exact and
+# order-free -- bit-identical to the b = 15 handle's results.
+PAIR_CASES = [
+    ("er_ragged_70001", lambda: graphs.make_graph("er", 6, n=70001, m_raw=600000)),          # k = 2, no upper half in the last
+    ("er_98309", lambda: graphs.make_graph("er", 9, n=98309, m_raw=700000)),                 # upper half of 5 vertices
+    ("rmat17", lambda: graphs.make_graph("rmat", 21, scale=17, permute=True)),               # k = 2 full partitions
+    ("rmat18_bfs_like", lambda: graphs.make_graph("rmat", 22, scale=18, permute=False)),     # k = 4, skewed bins
+    ("small_1000", lambda: graphs.make_graph("er", 3, n=1000, m_raw=8000)),                  # one partial partition
+    ("instar", lambda: star_graph(150000, inward=True)),
+]
+
+
+@pytest.mark.parametrize("name,mk", PAIR_CASES, ids=[c[0] for c in PAIR_CASES])
+def test_pair_q16_layout_and_pagerank(pcpm, name, mk):
+    g = mk()
+    h = build(pcpm, g, 16)
+    h15 = build(pcpm, g, 15)
+    try:
+        lay = export(pcpm, h)
+        assert lay["view"].wide == 1 and lay["ids"] is not None and lay["info"].partition_bits == 16
+        assert_layout_equal(g, lay, 16)
+        x = np.random.default_rng(2).random(g.n_src).astype(np.float32)
+        pcpm.pcpm_scatter(h, torch.from_numpy(x).cuda())
+        torch.cuda.synchronize()
+        got = d2h(lay["view"].upd, lay["info"].e_prime, np.float32)
+        ref_u = oracle.scatter(oracle.layout(g.n_src, g.n_dst, g.row_ptr, g.col, 16), x)
+        np.testing.assert_array_equal(got.view(np.uint32), ref_u.view(np.uint32))
+        ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 12)
+        out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 12, out)
+        pr_check(out.cpu().numpy(), ref, name)
+        out15 = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(h15, 0.85, 12, out15)
+        assert torch.equal(out, out15)
+        # kernel options that do not apply to pair handles are ignored, not mis-run
+        for k, v in (("gather_variant", 2), ("scatter_variant", 3), ("scatter_variant", 1)):
+            pcpm.pcpm_set_option(h, k, v)
+        out2 = torch.zeros_like(out)
+        pcpm.pcpm_pagerank(h, 0.85, 12, out2)
+        assert torch.equal(out, out2)
+    finally:
+        pcpm.pcpm_destroy(h)
+        pcpm.pcpm_destroy(h15)
+
+
+@pytest.mark.parametrize("name,mk", [
+    ("rmat17_w", lambda: graphs.make_graph("rmat", 23, scale=17, permute=True, values=True, transpose=True)),
+    ("nonsquare", lambda: graphs.column_prefix(graphs.make_graph("er", 24, n=150001, m_raw=1500000, values=True), 70003)),
+], ids=["rmat17_w", "nonsquare"])
+def test_pair_q16_spmv(pcpm, name, mk):
+    g = mk()
+    h = build(pcpm, g, 16)
+    try:
+        assert_layout_equal(g, export(pcpm, h), 16)
+        x = graphs.make_x(g.n_src, 4)
+        y = torch.zeros(g.n_dst, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_spmv(h, torch.from_numpy(x).cuda(), y)
+        spmv_check(g, y.cpu().numpy(), x, spmv_fbits(g.values, x))
+    finally:
+        pcpm.pcpm_destroy(h)
+
+
+def test_pair_q16_rejections(pcpm):
+    g = graphs.make_graph("er", 3, n=1000, m_raw=8000)
+    rp, col, _ = to_device(g)
+    csr = pcpm.make_csr(g.n_src, g.n_dst, rp, col)
+    for call in (lambda: pcpm.pcpm_build(csr, 17),
+                 lambda: pcpm.pcpm_build_shard(csr, 16, 0, 1000, 0, None),
+                 lambda: pcpm.pcpm_build_ex(csr, 16, pcpm.PCPM_BVGAS, None)):
+        with pytest.raises(pcpm.PcpmError) as e:
+            call()
+        assert e.value.code == pcpm.PCPM_EINVAL
