@@ -410,6 +410,7 @@ static pcpm_handle* build_common(const pcpm_csr* csr, int partition_bits, unsign
   h->b = partition_bits;
   h->gb = std::min(partition_bits, kMaxBits);
   h->pair = partition_bits > kMaxBits;
+  if (h->pair) h->opt_pdl = 0;
   cudaGetDevice(&h->device);
   pool_setup(h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -903,7 +904,9 @@ int pcpm_set_option(pcpm_handle* h, const char* key, int64_t value) {
     return PCPM_OK;
   }
   if (!strcmp(key, "pdl")) {
-    h->opt_pdl = value ? 1 : 0;
+    // pair handles (q = 2^16) launch plainly: with programmatic dependent launch their
+    // iteration measured 30% slower (c3: 2.39 vs 1.83 ms)
+    h->opt_pdl = (value && !h->pair) ? 1 : 0;
     free_graph(h);
     return PCPM_OK;
   }

@@ -734,9 +734,12 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   // paper's dynamic scheduling).
   std::vector<GatherItem> gi;
   // pair handles (q = 2^16): the gather sees 2 k_dst half-partitions of 2^15 vertices; half
-  // hf of bin j is item j' = 2 j + hf over the WHOLE bin (it skips the other half's IDs),
-  // never cut (slices and the cluster gather assume one accumulator per bin)
+  // hf of bin j is the "bin" j' = 2 j + hf: the same ID range, of which its items add only
+  // that half's IDs.  Heavy bins are cut into slices per half like any other bin.
   const int64_t k_g = h->pair ? 2 * k_dst : k_dst;
+  const int jsh = h->pair ? 1 : 0;
+  const int64_t qa = int64_t(1) << h->gb;            // accumulator words = slot-buffer words per slice
+  const int64_t m_str = h->pair ? 2 * m : m;         // IDs the gather streams
   std::vector<uint32_t> nsl(k_g, 0), sbase(k_g, 0);
   uint32_t nslots = 0;
   // items per SM the cut aims at: 2 when bin sizes are skewed (the LPT order then has
@@ -746,19 +749,10 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   for (int64_t j = 0; j < k_dst; ++j) max_bin = std::max<int64_t>(max_bin, (int64_t)hbin[j + 1] - (int64_t)hbin[j]);
   int slice_div = (k_dst > 0 && max_bin * k_dst <= 2 * m) ? 1 : 2;
   if (const char* e = getenv("PCPM_GATHER_SLICE_DIV")) slice_div = std::max(1, atoi(e));
-  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m / (slice_div * h->num_sms)) / kTileAlign + 1) * kTileAlign);
-  for (int64_t j = 0; h->pair && j < k_g; ++j) {
-    nsl[j] = 1;
-    if ((j << h->gb) >= n_dst) continue;              // the last partition may have no upper half
-    GatherItem it{};
-    it.j = (uint32_t)j;
-    it.x0 = hbin[j >> 1];
-    it.x1 = hbin[(j >> 1) + 1];
-    it.pad[0] = 0xFFFFFFFFu;
-    gi.push_back(it);
-  }
-  for (int64_t j = 0; !h->pair && j < k_dst; ++j) {
-    int64_t s0 = hbin[j], s1 = hbin[j + 1], sz = s1 - s0;
+  int64_t slice = std::max<int64_t>(4 * kTileAlign, ((m_str / (slice_div * h->num_sms)) / kTileAlign + 1) * kTileAlign);
+  for (int64_t j = 0; j < k_g; ++j) {
+    if (h->pair && (j << h->gb) >= n_dst) continue;   // the last partition may have no upper half
+    int64_t s0 = hbin[j >> jsh], s1 = hbin[(j >> jsh) + 1], sz = s1 - s0;
     int64_t nslc = sz > 0 ? (sz + slice - 1) / slice : 1;
     int64_t per = (sz + nslc - 1) / nslc;
     std::vector<int64_t> cuts{s0};
@@ -819,7 +813,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
   h->n_slots = nslots;
   {
     std::vector<uint32_t> sb;
-    for (int64_t j = 0; j < k_dst; ++j)
+    for (int64_t j = 0; j < k_g; ++j)
       if (nsl[j] > 1) sb.push_back((uint32_t)j);
     h->n_split_bins = (int)sb.size();
     if ((rc = dev_alloc_t(h, &h->split_bins, std::max<size_t>(1, sb.size())))) return rc;
@@ -827,7 +821,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
       TK(cudaMemcpyAsync(h->split_bins, sb.data(), sizeof(uint32_t) * sb.size(), cudaMemcpyHostToDevice, s));
     // the fused iteration scatters a split partition after k_apply_split: its scatter items
     h->n_sitems_split = 0;
-    if (!sb.empty() && k_src == k_dst && h->n_sitems > 0) {
+    if (!sb.empty() && k_src == k_dst && h->n_sitems > 0 && !h->pair) {
       std::vector<ScatterItem> si(h->n_sitems), ss;
       TK(cudaMemcpyAsync(si.data(), h->sitems, sizeof(ScatterItem) * si.size(), cudaMemcpyDeviceToHost, s));
       TK(cudaStreamSynchronize(s));
@@ -840,7 +834,7 @@ int finish_layout(pcpm_handle* h, Temp& tmp, PhaseTimer& pt, uint32_t* G, unsign
       }
     }
   }
-  if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * q)))) return rc;
+  if ((rc = dev_alloc_t(h, &h->slot_buf, std::max<size_t>(1, (size_t)nslots * qa)))) return rc;
   k_item_f<<<grid_for(h->n_gitems), kT, 0, s>>>(h->n_gitems, h->gitems, h->chunk_base, h->bin_upd_start,
                                                 h->pair ? 1 : 0);
   TK(cudaGetLastError());

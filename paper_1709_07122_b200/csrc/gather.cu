@@ -1972,7 +1972,7 @@ int read_debug_counters(unsigned long long* out, int cap, bool reset) {
 
 int launch_apply_split(pcpm_handle* h, const GatherArgs& a, bool pagerank, cudaStream_t s) {
   if (h->n_split_bins == 0) return PCPM_OK;
-  const int chunks = (int)((h->q + kSplitChunk - 1) / kSplitChunk);
+  const int chunks = (int)(((int64_t(1) << h->gb) + kSplitChunk - 1) / kSplitChunk);
   const int blocks = h->n_split_bins * chunks;
   if (pagerank)
     k_apply_split<true><<<blocks, kSplitThreads, 0, s>>>(a, h->split_bins);

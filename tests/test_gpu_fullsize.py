@@ -255,3 +255,29 @@ def test_fullsize_scatter_bit_exact(pcpm):
     finally:
         pcpm.pcpm_destroy(h)
     print(f"{key}: scatter of E'={info.e_prime} updates bit-exact, digest {digests['upd'][0]}")
+
+
+def test_fullsize_pair_q16_bit_identical_to_q15(pcpm):
+    """q = 2^16 (pair handles) at c3's size: the fixed-point sums are exact and order-free and the
+    apply is the same arithmetic, so the output must equal the b = 15 handle's (which
+    test_fullsize_pagerank compares with the oracle) bit for bit; r must not fall."""
+    key = "c3"
+    cfg = graphs.CONFIGS[key]
+    g = graphs.make_config(key, backend="torch", device="cuda")
+    outs, eps = [], []
+    for b in (15, 16):
+        h = pcpm.pcpm_build_ex(pcpm.make_csr(g.n_src, g.n_dst, g.row_ptr, g.col, None), b, 0,
+                               torch.cuda.current_stream())
+        try:
+            info = pcpm.pcpm_get_info(h)
+            assert info.partition_bits == b and info.k_dst == (g.n_dst + (1 << b) - 1) >> b
+            out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, cfg["iters"], out)
+            torch.cuda.synchronize()
+            outs.append(out)
+            eps.append(info.e_prime)
+        finally:
+            pcpm.pcpm_destroy(h)
+    assert torch.equal(outs[0], outs[1])
+    assert eps[1] <= eps[0]                       # larger partitions compress more
+    assert abs(float(outs[1].double().sum()) - 1.0) <= 1e-5
