@@ -886,3 +886,34 @@ def test_pair_q16_rejections(pcpm):
         with pytest.raises(pcpm.PcpmError) as e:
             call()
         assert e.value.code == pcpm.PCPM_EINVAL
+
+
+def test_pair_q16_variants(pcpm):
+    """q = 2^16 with the other layouts and drivers: uncompressed bins, host CSR pointers,
+    weighted PageRank (R24), the tolerance driver and the pipelined job runtime."""
+    g = graphs.make_graph("er", 6, n=70001, m_raw=600000)
+    ref = oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, 10)
+    for flags, device in ((pcpm.PCPM_NO_COMPRESS, True), (0, False), (pcpm.PCPM_BUILD_PULL, True)):
+        h = build(pcpm, g, 16, flags=flags, device=device)
+        try:
+            out = torch.zeros(g.n_src, dtype=torch.float32, device="cuda")
+            pcpm.pcpm_pagerank(h, 0.85, 10, out)
+            pr_check(out.cpu().numpy(), ref, f"flags={flags}")
+            if flags & pcpm.PCPM_BUILD_PULL:
+                pull = torch.zeros_like(out)
+                pcpm.pcpm_pull_pagerank(h, 0.85, 10, pull)
+                pr_check(pull.cpu().numpy(), ref, "pull")
+                it = pcpm.pcpm_pagerank_tol(h, 0.85, 1e-7, 100, out)
+                assert 1 <= it < 100
+                pr_check(out.cpu().numpy(), oracle.pagerank(g.n_src, g.row_ptr, g.col, 0.85, it), "tol")
+        finally:
+            pcpm.pcpm_destroy(h)
+    gw = weighted(graphs.make_graph("er", 6, n=70001, m_raw=600000), 4, 0.3)
+    h = build(pcpm, gw, 16)
+    try:
+        pcpm.pcpm_set_option(h, "weighted_pagerank", 1)
+        out = torch.zeros(gw.n_src, dtype=torch.float32, device="cuda")
+        pcpm.pcpm_pagerank(h, 0.85, 15, out)
+        pr_check(out.cpu().numpy(), oracle.pagerank_weighted(gw.n_src, gw.row_ptr, gw.col, gw.values, 0.85, 15), "wpr16")
+    finally:
+        pcpm.pcpm_destroy(h)
