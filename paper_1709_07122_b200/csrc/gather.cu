@@ -38,6 +38,11 @@
 //    (staged with the IDs) before the fixed-point add.
 //  * The decode is bound by the shared-memory pipe (one random ATOMS per ID,
 //    ~4.4 wavefronts per warp instruction), see DESIGN.md §6.
+//  * q = 2^16 ("pair" handles, 4-byte IDs): the 256 KB accumulator of a partition does not
+//    fit one SM, so every bin is gathered as two half bins: item j' = 2 j + h streams the whole
+//    bin j, decodes every ID (all flags advance the update pointer) and adds only the IDs
+//    whose bit 15 equals h; accumulator, apply and split-bin slices then work on 2 k
+//    half-partitions of 2^15 vertices unchanged (a.b = 15, a.pair = 1).
 #include <cstdlib>
 #include <type_traits>
 
