@@ -143,6 +143,9 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 #ifndef PCPM_CARRY_CC
 #define PCPM_CARRY_CC 1              // carry test with add.cc / addc (A/B: 0 = NOT + compare)
 #endif
+#ifndef PCPM_GATHER_MATCH
+#define PCPM_GATHER_MATCH 0          // 1: match.any aggregation of same-destination lanes before the ATOMS (A/B)
+#endif
 #ifndef PCPM_GATHER_ITEM_FENCE
 #define PCPM_GATHER_ITEM_FENCE 0     // 1: fence after every item's reduction atomics (round-1 form, A/B)
 #endif
@@ -683,6 +686,28 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
           tlo[c] = (uint32_t)T;
           thi[c] = (uint32_t)(T >> 32);
         }
+#if PCPM_GATHER_MATCH
+        // A/B (DESIGN.md §6 "hub aggregation"): lanes of a step that hit the same destination
+        // are found with match.any; their terms are summed exactly with three redux.sync adds
+        // (16-bit halves of the low words, and the high words) and the lowest lane issues one
+        // ATOMS for the group.  Exact integer sums: the result is the same bits.
+#pragma unroll
+        for (int c = 0; c < P; ++c) {
+          const uint32_t key = ok[c] ? (id[c] & qmask) : (0x80000000u | (uint32_t)lane);
+          const uint32_t peers = __match_any_sync(0xffffffffu, key);
+          if (peers != (1u << lane)) {
+            const uint32_t slo = __reduce_add_sync(peers, tlo[c] & 0xFFFFu);
+            const uint32_t shi = __reduce_add_sync(peers, tlo[c] >> 16);
+            const uint32_t sth = __reduce_add_sync(peers, thi[c]);
+            const unsigned long long tot = (unsigned long long)slo + ((unsigned long long)shi << 16) +
+                                           ((unsigned long long)sth << 32);
+            const bool lead = (__ffs(peers) - 1) == lane;
+            tlo[c] = lead ? (uint32_t)tot : 0u;
+            thi[c] = lead ? (uint32_t)(tot >> 32) : 0u;
+            ok[c] = ok[c] && lead;
+          }
+        }
+#endif
 #pragma unroll
         for (int c = 0; c < P; ++c) old[c] = ok[c] ? atoms_add_u32(acc_s + ((id[c] & qmask) << 2), tlo[c]) : 0u;
         // carry out of the low word: old + lo wraps  <=>  lo > ~old; lanes with
