@@ -34,8 +34,11 @@
 //    dangling mass and L1 residual, reduced in fixed order by the last CTA.
 //    Slices of split (heavy) bins store their low words to per-slice slot
 //    buffers; k_apply_split sums the slots and applies those bins afterwards.
-//  * Weighted PageRank (R24) and SpMV multiply each update by the edge weight
-//    (staged with the IDs) before the fixed-point add.
+//  * Weighted PageRank (R24) and SpMV multiply each update by the edge weight before the
+//    fixed-point add.  In the compact layout the decoders read the weights of a
+//    sub-chunk straight from global memory (coalesced, addresses known before the IDs are
+//    decoded, prefetched into L2 by the producer), so the ring holds the same 4096-ID tiles
+//    as unweighted PageRank; with 4-byte IDs the weights are staged beside the IDs.
 //  * The decode is bound by the shared-memory pipe (one random ATOMS per ID,
 //    ~4.4 wavefronts per warp instruction), see DESIGN.md §6.
 //  * q = 2^16 ("pair" handles, 4-byte IDs): the 256 KB accumulator of a partition does not
@@ -75,7 +78,14 @@ struct Cfg {
   // the extra one rotating; with the producer, 32 warps).  PCPM_GATHER_BIG_TILE
   // = 1 selects 8192-ID tiles double-buffered (2 x 48 KB; measured slower on
   // c4: 2.10 vs 1.98 ms).  Other variants: 2048-ID tiles, 16 warps of 128 IDs.
-  static constexpr bool kHot = kCompact && !W;
+#ifndef PCPM_GATHER_WG
+#define PCPM_GATHER_WG 1             // 0: weights staged in the ring with 2048-ID tiles (the earlier plan, A/B)
+#endif
+  // kWG: the edge weights are not staged in the ring; the decoders read them from global
+  // memory (coalesced 128 B per step, the producer prefetches them into L2), which lets the
+  // weighted compact configurations use the same 4096-ID tiles as unweighted PageRank
+  static constexpr bool kWG = W && kCompact && PCPM_GATHER_WG != 0;
+  static constexpr bool kHot = kCompact && (!W || kWG);
   static constexpr int kMode = kHot ? PCPM_GATHER_TILE_MODE : 0;
   static constexpr int kTile = kHot ? (kMode == 1 ? 4 * kTileIds : (kMode == 2 ? kTileIds : 2 * kTileIds)) : kTileIds;
 #ifndef PCPM_GATHER_STAGES
@@ -111,7 +121,7 @@ struct Cfg {
   static constexpr int kIdsBytes = kTile * (int)sizeof(IdT);
   static constexpr int kWinCap = kTile + 8;                // >= #flags + 1, 16 B aligned ends
   static constexpr int kWinBytes = kWinCap * 4;
-  static constexpr int kWBytes = W ? kTile * 4 : 0;
+  static constexpr int kWBytes = (W && !kWG) ? kTile * 4 : 0;
   static constexpr int kCbBytes = (kTile / kChunkIds) * 4;
   static constexpr int kStageBytes = kIdsBytes + kWinBytes + kWBytes + kCbBytes;
   static constexpr int kFlagShift = kCompact ? 15 : 31;
@@ -122,6 +132,12 @@ struct Cfg {
 };
 
 __device__ __forceinline__ uint32_t ldcg_u32(const uint32_t* p) { return __ldcg(p); }
+// streamed once: read-only path, no L1 allocation
+__device__ __forceinline__ float ldg_stream_f32(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 }  // namespace
 
@@ -456,6 +472,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
           const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
           bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
           if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+          if constexpr (C::kWG) bulk_prefetch_l2(a.w + tl * C::kTile, C::kTile * 4);
         }
         for (uint32_t k = 0; k < nb; ++k) {
           if (!own()) {                          // the other producer's stage
@@ -470,6 +487,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             const uint32_t alo = (fa > 0 ? fa - 1 : 0) & ~3u, ahi = (fb + 3) & ~3u;
             bulk_prefetch_l2(ids + tl * C::kTile, C::kIdsBytes);
             if (ahi > alo) bulk_prefetch_l2(a.upd + alo, (ahi - alo) * 4);
+            if constexpr (C::kWG) bulk_prefetch_l2(a.w + tl * C::kTile, C::kTile * 4);
           }
           if constexpr (PR) {
             // the apply's vertex arrays of partition j into L2 a few tiles before the epilogue
@@ -508,7 +526,7 @@ __device__ __forceinline__ void gather_producer(const GatherArgs& a, const IdT* 
             bulk_g2s(sb + C::kIdsBytes, a.upd + alo, win_bytes, &full[stage], pol);
             bulk_g2s(sb + C::kIdsBytes + C::kWinBytes + C::kWBytes, a.chunk_base + tb / kChunkIds, C::kCbBytes,
                      &full[stage], pol);
-            if constexpr (W) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
+            if constexpr (W && !C::kWG) bulk_g2s(sb + C::kIdsBytes + C::kWinBytes, a.w + tb, C::kWBytes, &full[stage], pol);
             if (PCPM_GATHER_PROFILE) pcopy += clock64() - tc0;
           }
           __syncwarp();
@@ -654,6 +672,11 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
       // compare per ID for the ballot
       using SIdT = typename std::conditional<sizeof(IdT) == 2, int16_t, int32_t>::type;
       const SIdT* sids = reinterpret_cast<const SIdT*>(ids_s);
+      float wv[P];                     // kWG: this sub-chunk's weights, loaded first (addresses known up front)
+      if constexpr (C::kWG) {
+#pragma unroll
+        for (int c = 0; c < P; ++c) wv[c] = ldg_stream_f32(a.w + xs + c * 32 + lane);
+      }
       uint32_t id[P];
 #pragma unroll
       for (int c = 0; c < P; ++c) id[c] = (uint32_t)(int32_t)sids[sc * C::kSub + c * 32 + lane];
@@ -681,7 +704,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
 #pragma unroll
         for (int c = 0; c < P; ++c) {
           // SPR is stored as SPR * 2^F; weighted PageRank (R24) applies w(u,v) here
-          const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+          const float tv = W ? val[c] * (C::kWG ? wv[c] : w_s[sc * C::kSub + c * 32 + lane]) : val[c];
           const unsigned long long T = __float2ull_rn(tv);
           tlo[c] = (uint32_t)T;
           thi[c] = (uint32_t)(T >> 32);
@@ -752,7 +775,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
         int32_t thi[P];
 #pragma unroll
         for (int c = 0; c < P; ++c) {
-          const float tv = W ? val[c] * w_s[sc * C::kSub + c * 32 + lane] : val[c];
+          const float tv = W ? val[c] * (C::kWG ? wv[c] : w_s[sc * C::kSub + c * 32 + lane]) : val[c];
           tlo[c] = (uint32_t)__float2int_rn(tv * sp_scale_f);
           thi[c] = 0;
         }
