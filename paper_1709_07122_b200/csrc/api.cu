@@ -811,7 +811,7 @@ int pcpm_get_info(const pcpm_handle* h, pcpm_info* out) {
     if (cudaMemcpy(&xm, h->xmax, 4, cudaMemcpyDeviceToHost) == cudaSuccess) {
       int ex = 0;
       if (xm > 0.f) frexpf(xm, &ex);
-      const int F = 30 - (h->weighted ? h->wexp : 0) - ex;
+      const int F = kSpmvHead - (h->weighted ? h->wexp : 0) - ex;
       i.fixed_point_bits = F < -120 ? -120 : (F > 62 ? 62 : F);
     } else {
       cudaGetLastError();

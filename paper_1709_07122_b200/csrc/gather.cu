@@ -169,7 +169,7 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 __device__ int spmv_fbits(float xmax, int wexp) {
   int ex = 0;
   if (xmax > 0.0f) frexpf(xmax, &ex);          // xmax <= 2^ex
-  const int F = 30 - wexp - ex;
+  const int F = kSpmvHead - wexp - ex;
   return F < -120 ? -120 : (F > 62 ? 62 : F);
 }
 
@@ -769,7 +769,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
         // around zero never wraps; only signed overflow of the low word
         // (|partial| >= 2^31 units) carries +-1 into the global high word.
         // w*x is rounded once to fp32 (<= 2^-24 |w x|, R22); F keeps
-        // |w x| 2^F <= 2^30, so each term T is an int32 and the high part of the
+        // |w x| 2^F <= 2^22 (kSpmvHead), so each term T is an int32 and the high part of the
         // balanced form is zero: only the low word's signed overflow carries.
         uint32_t tlo[P], old[P];
         int32_t thi[P];
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   pdl_wait();                                      // D_t (red_in) and the scatter's bins are complete
   double base_pr = 0.0;
   if constexpr (PR) base_pr = (1.0 - a.d) / a.n + a.d * (a.red_in[0] / a.n);
-  // SpMV scale: F = 30 - ceil(log2 max|w|) - ceil(log2 max|x|), so |w x| 2^F <= 2^30
+  // SpMV scale: F = 22 - ceil(log2 max|w|) - ceil(log2 max|x|), so |w x| 2^F <= 2^22 (kSpmvHead)
   double sp_inv = 1.0;
   float sp_scale_f = 1.0f;
   if constexpr (!PR) {

@@ -34,6 +34,16 @@ constexpr int kMaxBits = 15;                           // q <= 32768: 128 KB acc
 // items that each own one 2^15-vertex half of the partition and skip the other half's IDs
 // (4-byte IDs only: a 16-bit local ID plus the run flag does not fit the 2-byte format)
 constexpr int kMaxBitsPair = 16;
+// SpMV fixed point (R22): F = kSpmvHead - ceil(log2 max|w|) - ceil(log2 max|x|), so every
+// term |w x| 2^F <= 2^kSpmvHead of the signed 32-bit low word.  22 leaves 9 bits of headroom:
+// the low word overflows (a carry into the global high word: a divergent, serialised path) once
+// per >= 512 adds even when all terms have one sign; with 30 it overflowed on 0.7% of c5's adds
+// and 60% of the 128-ID sub-chunks took the carry path (c5 gather 1.259 -> 0.793 ms).  The grid
+// 2^-F is then 2^-23 of max|w| max|x|: the fp32 rounding of the largest products.
+#ifndef PCPM_SPMV_HEAD
+#define PCPM_SPMV_HEAD 22
+#endif
+constexpr int kSpmvHead = PCPM_SPMV_HEAD;
 constexpr int kScatterThreads = 1024;
 constexpr int kScatterMaxGroups = 2048;                // j-range of one scatter item (smem offsets)
 constexpr int kPngChunk = 256;                         // grp_at granularity (scatter warp sub-ranges)

@@ -42,11 +42,11 @@ def to_device(g):
 
 def spmv_fbits(values, x):
     """Fractional bits F of the SpMV fixed-point accumulator, computed from the INPUTS
-    as DESIGN.md R22 defines it (never read back from the library): F = 30 - e_w - e_x,
+    as DESIGN.md R22 defines it (never read back from the library): F = 22 - e_w - e_x,
     e(a) = the exponent with max|a| < 2^e (frexp), e_w = 0 for a structure-only matrix
-    (w = 1), clamped to [-120, 62].  Then every |w x| 2^F < 2^30."""
+    (w = 1), clamped to [-120, 62].  Then every |w x| 2^F < 2^22."""
     import math
     ex = lambda a: math.frexp(float(np.max(np.abs(a))))[1] if len(a) and np.max(np.abs(a)) > 0 else 0  # noqa: E731
     vals = None if values is None else np.asarray(values, dtype=np.float32)
-    f = 30 - (0 if vals is None else ex(vals)) - ex(np.asarray(x, dtype=np.float32))
+    f = 22 - (0 if vals is None else ex(vals)) - ex(np.asarray(x, dtype=np.float32))
     return max(-120, min(62, f))
