@@ -132,7 +132,10 @@ int ensure_red(pcpm_handle* h, int iters) {
 int pr_fixed_bits(int64_t n) {
   // F: typical SPR ~ 1/(n*deg) lands near 2^22 in the low word; PR <= 1 so the
   // u64 never overflows; resolution 2^-(F+1) ~ 1e-8 (1-d)/n per term.
-  return std::min(60, std::max(30, 26 + ceil_log2((uint64_t)n)));
+#ifndef PCPM_PR_FBASE
+#define PCPM_PR_FBASE 26
+#endif
+  return std::min(60, std::max(30, PCPM_PR_FBASE + ceil_log2((uint64_t)n)));
 }
 
 GatherArgs base_args(pcpm_handle* h, int fbits) {

@@ -159,6 +159,12 @@ __device__ unsigned long long g_gather_prof[24];   // [8..11]: producer (PCPM_GA
 #ifndef PCPM_CARRY_CC
 #define PCPM_CARRY_CC 1              // carry test with add.cc / addc (A/B: 0 = NOT + compare)
 #endif
+#ifndef PCPM_FINE_CARRY
+#define PCPM_FINE_CARRY 1            // 1: carry bitmap of k_gather with 1 bit per 4 vertices (0: per 32, A/B)
+#endif
+#ifndef PCPM_APPLY_HI4
+#define PCPM_APPLY_HI4 1             // 1: the vector apply reads a carried quad's high words with one 16-byte load (0: A/B)
+#endif
 #ifndef PCPM_GATHER_MATCH
 #define PCPM_GATHER_MATCH 0          // 1: match.any aggregation of same-destination lanes before the ATOMS (A/B)
 #endif
@@ -648,10 +654,24 @@ __device__ __noinline__ void fused_scatter_stage(const GatherArgs& a, const Stag
   rot = who;
 }
 
+// Carry bitmap: which accumulator words have a nonzero global high word.  Coarse: 1 bit per
+// 32 vertices (q / 1024 words); FINE (k_gather): 1 bit per 4 vertices (q / 128 words = 1 KB),
+// so the apply, which takes 4 vertices per thread, reads a.hi only for the quads that carried
+// -- with the coarse map ~10% of c4's vertices took that latency-bound path.
+template <bool FINE>
+__device__ __forceinline__ void carry_mark(uint32_t* bitmap, uint32_t li) {
+  if (FINE) atomicOr(&bitmap[li >> 7], 1u << ((li >> 2) & 31));
+  else atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+}
+template <bool FINE>
+__device__ __forceinline__ bool carry_test(const uint32_t* bitmap, uint32_t i) {
+  return FINE ? ((bitmap[i >> 7] >> ((i >> 2) & 31)) & 1u) != 0u : ((bitmap[i >> 10] >> ((i >> 5) & 31)) & 1u) != 0u;
+}
+
 // Decode of one full stage by one consumer warp (Alg. 5): the
 // warp takes sub-chunks gw, gw + gsz, ... of the stage's tile (plus its turn of the
 // rotating remainder) and adds each ID's update into the shared accumulator.
-template <typename C, typename IdT, bool W, bool PR>
+template <typename C, typename IdT, bool W, bool PR, bool FINE = false>
 __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMeta& m, const uint8_t* sb,
                                              uint32_t* acc, uint32_t* bitmap, const int gw, const int gsz,
                                              int& rot, const uint32_t qmask, const uint32_t lemask, const int lane,
@@ -759,7 +779,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
             if (hinc) {
               const uint32_t li = id[c] & qmask;
               atomicAdd(&a.hi[v0 + li], hinc);
-              atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+              carry_mark<FINE>(bitmap, li);
             }
           }
         }
@@ -796,7 +816,7 @@ __device__ __forceinline__ void decode_stage(const GatherArgs& a, const StageMet
             if (hinc[c]) {
               const uint32_t li = id[c] & qmask;
               atomicAdd(&a.hi[v0 + li], (uint32_t)hinc[c]);
-              atomicOr(&bitmap[li >> 10], 1u << ((li >> 5) & 31));
+              carry_mark<FINE>(bitmap, li);
             }
         }
       }
@@ -846,7 +866,9 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
   const int64_t aw = SL ? (int64_t)a.acc_words : q;                         // accumulator words (slots)
   uint32_t* acc = reinterpret_cast<uint32_t*>(smem);                       // aw words (128 B rounded)
   uint32_t* bitmap = acc + ((aw + 31) / 32) * 32;                          // 1 bit per 32 words
-  const int bm_words = (int)((aw + 1023) / 1024) < 4 ? 4 : (int)((aw + 1023) / 1024);
+  constexpr bool kFine = PCPM_FINE_CARRY != 0 && !PA && !SL;
+  const int bm_div = kFine ? 128 : 1024;
+  const int bm_words = (int)((aw + bm_div - 1) / bm_div) < 4 ? 4 : (int)((aw + bm_div - 1) / bm_div);
   uint2* smap = reinterpret_cast<uint2*>(bitmap + ((bm_words + 31) / 32) * 32);  // slots: q/32 words
   uint8_t* stage_base = reinterpret_cast<uint8_t*>(smap + (SL ? q / 32 : 0));
   StageMeta* meta = reinterpret_cast<StageMeta*>(stage_base + S * C::kStageBytes);
@@ -994,8 +1016,8 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
     }
     const uint32_t v0 = m.j << a.b;
     if (!(m.flags & kFlagEmpty))
-      decode_stage<C, IdT, W, PR>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
-                                  lemask, lane, sp_scale_f, v0);
+      decode_stage<C, IdT, W, PR, kFine>(a, m, stage_base + stage * C::kStageBytes, acc, bitmap, gw, gsz, rot, qmask,
+                                         lemask, lane, sp_scale_f, v0);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
     stage += 2;
@@ -1053,7 +1075,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
           a.hi[v] = 0u;
         } else {
           tot = PR ? (uint64_t)acc[i] : (uint64_t)(long long)(int32_t)acc[i];
-          if ((bitmap[i >> 10] >> ((i >> 5) & 31)) & 1u) {
+          if (carry_test<kFine>(bitmap, (uint32_t)i)) {
             tot += (uint64_t)ldcg_u32(&a.hi[v]) << 32;
             a.hi[v] = 0u;
           }
@@ -1136,7 +1158,7 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
       if (run_apply) {
         if constexpr (PR) {
           bool vec = (cnt & 3) == 0 && aligned16(a.pr_new + v0) && aligned16(a.pr_old + v0) &&
-                     aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0);
+                     aligned16(a.spr_new + v0) && aligned16(a.inv_deg + v0) && aligned16(a.hi + v0);
           if constexpr (MULTI)
             for (int r = 0; r < a.n_peer; ++r) vec = vec && aligned16(a.spr_peer[r] + v0);
           if (vec) {
@@ -1150,12 +1172,37 @@ __global__ void __launch_bounds__(Cfg<IdT, W, SL>::kThreads, 1) k_gather(const G
             for (int64_t i4 = ctid; i4 < cnt / 4; i4 += kCons) {
               const float4 idg = __ldg(id4 + i4);
               const float4 po = __ldg(po4 + i4);
+#if PCPM_APPLY_HI4
+              // a quad that carried (one bitmap bit covers it): its four global high words with
+              // ONE 16-byte load issued beside the loads above, and one 16-byte store to clear
+              // them -- total() would chain four dependent load/store pairs, and the whole CTA
+              // waits at the closing barrier for the threads that hit such quads
+              uint32_t hv[4] = {0u, 0u, 0u, 0u};
+              const bool whole = nsl == 1;
+              if (whole && carry_test<kFine>(bitmap, (uint32_t)(4 * i4))) {
+                uint4* h4p = reinterpret_cast<uint4*>(a.hi + v0) + i4;
+                const uint4 h4 = __ldcg(h4p);
+                *h4p = make_uint4(0u, 0u, 0u, 0u);
+                hv[0] = h4.x; hv[1] = h4.y; hv[2] = h4.z; hv[3] = h4.w;
+              }
+#endif
               const float idv[4] = {idg.x, idg.y, idg.z, idg.w};
               const float pov[4] = {po.x, po.y, po.z, po.w};
               float pn[4], sp[4];
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
+#if PCPM_APPLY_HI4
+                uint64_t tq;
+                if (whole) {
+                  tq = (uint64_t)acc[4 * i4 + c] + ((uint64_t)hv[c] << 32);
+                  acc[4 * i4 + c] = 0u;
+                } else {
+                  tq = total(4 * i4 + c);
+                }
+                const double prn = base_pr + a.d * ((double)(long long)tq * inv_scale);
+#else
                 const double prn = base_pr + a.d * ((double)(long long)total(4 * i4 + c) * inv_scale);
+#endif
                 pn[c] = (float)prn;
                 sp[c] = pn[c] * idv[c] * fscale;        // SPR * 2^F, SPR = PR / |N_o| (0 if dangling)
                 dang += idv[c] != 0.0f ? 0ull : red_fx(prn);
@@ -1903,7 +1950,8 @@ template <typename IdT, bool W, bool SL = false>
 int smem_bytes_for(int b, int64_t aw = 0) {
   using C = Cfg<IdT, W, SL>;
   const int64_t q = aw > 0 ? aw : int64_t(1) << b;
-  const int bm_words = (int)((q + 1023) / 1024) < 4 ? 4 : (int)((q + 1023) / 1024);
+  const int bm_div = (PCPM_FINE_CARRY != 0 && !SL) ? 128 : 1024;     // fine carry bitmap (k_gather without slots)
+  const int bm_words = (int)((q + bm_div - 1) / bm_div) < 4 ? 4 : (int)((q + bm_div - 1) / bm_div);
   const int64_t head = ((q + 31) / 32) * 32 * 4 + ((bm_words + 31) / 32) * 32 * 4 + (SL ? ((int64_t(1) << b) / 32) * 8 : 0);
   return (int)(head + C::kStages * C::kStageBytes + C::kStages * sizeof(StageMeta) + 2 * C::kStages * 8 + 8 * 8 +
                2 * C::kWarps * 8 + 16 + 8 * 4 + 2 * 8 + 16 + sizeof(PaRec));
